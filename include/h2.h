@@ -1,0 +1,142 @@
+/*
+ * h2.h -- C ABI of the B200-native distributed H^2 matrix-vector product
+ *
+ *     Y := alpha * A * X + beta * Y,    A = A_de + <U, S, V^T>
+ *
+ * for nv right-hand sides, computed by upsweep (alg:upsweep2), per-level
+ * coupling multiply (alg:mult), downsweep (alg:downsweep)
+ * and the dense near field, distributed by block rows (PAPER.md:195-206,
+ * 439-502, alg:optimized_dist_mult).  All arithmetic runs in CUDA kernels for sm_100a; there
+ * is no CPU fallback.  No torch types cross this boundary: plain pointers and sizes only.
+ *
+ * ---- Conventions ------------------------------------------------------------------------
+ * Levels: global numbering, root = 0, leaves = depth q (reading R2).  Node i of
+ *   level l (0 <= i < 2^l) has children 2i, 2i+1 (heap order).
+ * Small matrices: column-major.  A batch of r x c matrices is r*c contiguous elements each.
+ * Element type: dtype H2_F64 (double) or H2_F32 (float) for every floating array, X and Y.
+ * Distribution (nranks = P, a power of two, P <= 2^q; C = log2 P is the C-level): rank p owns
+ *   the branch rooted at node (C, p): at level l >= C the nodes p*2^(l-C) .. (p+1)*2^(l-C)-1,
+ *   its leaves, their rows of X and Y (a contiguous tree-order row range), and the block rows
+ *   of those nodes.  Levels l < C form the top tree, REPLICATED on every rank (reading R16).
+ *   With nranks == 1, C = 0 and the branch is the whole tree.
+ * X, Y: n_local x nv, column-major, leading dimension ld (>= n_local), rows in cluster-tree
+ *   order, device memory (h2_matvec*) or host memory (h2_matvec_host).
+ *
+ * ---- Errors -----------------------------------------------------------------------------
+ * Every entry point returns H2_OK (0) or a negative code and never throws or aborts.
+ * h2_last_error() describes the last failure on the calling thread.  A CUDA or NCCL failure
+ * inside a handle is sticky: later calls on it return H2_ERR_STATE.
+ */
+#ifndef H2_B200_H
+#define H2_B200_H
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    H2_OK = 0,
+    H2_ERR_ARG = -1,     /* bad argument (NULL, nv out of range, unknown dtype, ...)        */
+    H2_ERR_SHAPE = -2,   /* sizes inconsistent (k or m above the supported 64, ld < n, ...) */
+    H2_ERR_STRUCT = -3,  /* structural error in the tree / CSR description (see h2_create)  */
+    H2_ERR_CUDA = -4,    /* CUDA runtime error                                              */
+    H2_ERR_NCCL = -5,    /* NCCL error or NCCL library not loadable                         */
+    H2_ERR_OOM = -6,     /* device allocation failed                                        */
+    H2_ERR_STATE = -7    /* handle unusable after an earlier sticky error                   */
+};
+enum { H2_F64 = 0, H2_F32 = 1 };
+enum { H2_MEM_HOST = 0,     /* floating arrays are host memory: copied, caller may free      */
+       H2_MEM_DEVICE = 1 }; /* floating arrays are device memory: adopted (zero copy), the
+                               caller keeps them alive until h2_destroy                      */
+
+/* One rank's view of the H^2 matrix (PAPER.md:124-150 data; PAPER.md:195-206 distribution).
+ * "held nodes at level l" = the 2^(l-C) branch nodes for l >= C, all 2^l nodes for l < C.
+ * Integer arrays are always HOST memory (the plan is built on the host, once). */
+typedef struct {
+    int32_t dtype;               /* H2_F64 | H2_F32                                            */
+    int32_t mem;                 /* H2_MEM_HOST | H2_MEM_DEVICE (floating arrays only)         */
+    int32_t depth;               /* q: leaf level                                              */
+    int32_t leaf_size;           /* m: max rows per leaf; leaf blocks padded to m rows        */
+    int32_t rank, nranks;        /* p, P                                                       */
+    int64_t n_local;             /* rows of X / Y on this rank                                 */
+    const int32_t *level_rank;   /* [q+1] k^l, 1 <= k^l <= 64 ("fixed rank per level",
+                                    PAPER.md:124)                                              */
+    const int64_t *leaf_ptr;     /* [2^(q-C) + 1] local row offsets of my leaves; leaf_ptr[0]=0,
+                                    leaf_ptr[end] = n_local, each leaf 1..m rows (ragged ok)   */
+    const void *U_leaf;          /* my leaves: [2^(q-C)][m x k^q] col-major; padding rows 0     */
+    const void *V_leaf;          /* same shape; may alias U_leaf                               */
+    const void *const *E;        /* [q+1]; E[l] (l>=1): held nodes x [k^l x k^(l-1)] col-major,
+                                    the transfer of node c to its parent;
+                                    E[0] unused (reading R1)                                   */
+    const void *const *F;        /* same shape; may alias E                                    */
+    const int64_t *const *S_rowptr; /* [q+1]; level l: [held nodes + 1] CSR of coupling block
+                                    rows; level 0 may have no blocks            */
+    const int32_t *const *S_col; /* [q+1]; GLOBAL column node index at level l (may be remote) */
+    const void *const *S;        /* [q+1]; per block k^l x k^l col-major, CSR order            */
+    const int64_t *D_rowptr;     /* [2^(q-C) + 1] dense block rows of my leaves */
+    const int32_t *D_col;        /* GLOBAL leaf index (may be remote)                          */
+    const void *D;               /* per block m x m col-major, zero-padded                     */
+} h2_desc;
+
+typedef struct h2_ctx *h2_handle;
+
+/* Build a handle: validates the description, builds the static execution plan (replaces the
+ * paper's per-call marshaling), re-lays out V and F for the kernels' operand
+ * order, allocates the x^/y^ workspaces for up to nv_max vectors, and for nranks > 1 creates
+ * an NCCL communicator from `nccl_unique_id` (128 bytes, identical on all ranks; NULL when
+ * nranks == 1) and exchanges the compressed off-diagonal node lists.
+ * Collective over ranks.  On failure no handle is created (*out = NULL).
+ * Structural checks (H2_ERR_STRUCT): monotone row pointers, column ids in range, strictly
+ * ascending columns per row (no duplicate (t,s,l)), leaf sizes in [1, m], P a power of two
+ * with P <= 2^q.  Shape checks (H2_ERR_SHAPE): 1 <= k^l <= 64, 1 <= m <= 64, nv_max in [1, 64]. */
+int h2_create(const h2_desc *d, int nv_max, const void *nccl_unique_id, h2_handle *out);
+
+/* Y := alpha A X + beta Y on the handle's stream (asynchronous).  X, Y device pointers,
+ * ld = n_local.  alpha, beta are converted to dtype.  beta == 0: Y is write-only (NaNs in Y do
+ * not propagate).  alpha == 0: A X is not formed.  1 <= nv <= nv_max.  Collective over ranks
+ * (same nv, alpha, beta on every rank). */
+int h2_matvec(h2_handle h, double alpha, const void *X, double beta, void *Y, int nv);
+
+/* Same with explicit leading dimensions (>= n_local). */
+int h2_matvec_ld(h2_handle h, double alpha, const void *X, int64_t ldx, double beta, void *Y,
+                 int64_t ldy, int nv);
+
+/* End-to-end variant: X and Y are HOST arrays (ld = n_local; pinned memory gives async copies).
+ * Copies X (and Y if beta != 0) host->device, runs h2_matvec on internal device buffers, copies
+ * Y device->host, and synchronizes the handle's stream before returning. */
+int h2_matvec_host(h2_handle h, double alpha, const void *X, double beta, void *Y, int nv);
+
+/* Stream for subsequent work (a cudaStream_t cast to void*); default: the legacy stream. */
+int h2_set_stream(h2_handle h, void *stream);
+
+/* Static facts of the handle for nv vectors: flops (paper convention 2 nv x stored operator
+ * scalars), algorithmic bytes per matvec (operator once + X, Y, x^, y^ traffic),
+ * per-rank halo bytes exchanged, and the number of kernel launches one matvec makes.
+ * Any pointer may be NULL. */
+int h2_stats(h2_handle h, int nv, double *flops, double *bytes, double *xchg_bytes,
+             int *launches);
+
+/* Plan facts for tests: counts[0..7] = {diag coupling blocks, offdiag coupling blocks,
+ * root (top-tree) coupling blocks, diag dense blocks, offdiag dense blocks, peers,
+ * remote x^ nodes received, remote leaves received}. */
+int h2_plan_counts(h2_handle h, int64_t counts[8]);
+
+/* Release device memory, the NCCL communicator and streams.  NULL is a no-op. */
+int h2_destroy(h2_handle h);
+
+/* Fill out[0..127] with a fresh NCCL unique id (call on one rank, broadcast to the others,
+ * pass to h2_create).  H2_ERR_NCCL if the NCCL library cannot be loaded. */
+int h2_nccl_unique_id(void *out128);
+
+/* Message for the last failure on this thread (never NULL). */
+const char *h2_last_error(void);
+
+/* Library version string (never NULL). */
+const char *h2_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

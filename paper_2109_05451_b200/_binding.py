@@ -1,0 +1,204 @@
+"""ctypes binding of include/h2.h (argument marshalling only: every step of the matvec runs in
+the CUDA kernels of libh2b200.so).  Loading fails loudly when the library is missing; there is
+no CPU fallback."""
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libh2b200.so")
+
+H2_OK, H2_ERR_ARG, H2_ERR_SHAPE, H2_ERR_STRUCT, H2_ERR_CUDA, H2_ERR_NCCL, H2_ERR_OOM, H2_ERR_STATE = \
+    0, -1, -2, -3, -4, -5, -6, -7
+H2_F64, H2_F32 = 0, 1
+H2_MEM_HOST, H2_MEM_DEVICE = 0, 1
+
+EXPORTS = ["h2_create", "h2_matvec", "h2_matvec_ld", "h2_matvec_host", "h2_set_stream", "h2_stats",
+           "h2_plan_counts", "h2_destroy", "h2_nccl_unique_id", "h2_last_error", "h2_version"]
+
+
+class H2Error(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"h2 error {code}: {msg}")
+        self.code = code
+
+
+class h2_desc(C.Structure):
+    _fields_ = [
+        ("dtype", C.c_int32), ("mem", C.c_int32), ("depth", C.c_int32), ("leaf_size", C.c_int32),
+        ("rank", C.c_int32), ("nranks", C.c_int32), ("n_local", C.c_int64),
+        ("level_rank", C.c_void_p), ("leaf_ptr", C.c_void_p),
+        ("U_leaf", C.c_void_p), ("V_leaf", C.c_void_p),
+        ("E", C.c_void_p), ("F", C.c_void_p),
+        ("S_rowptr", C.c_void_p), ("S_col", C.c_void_p), ("S", C.c_void_p),
+        ("D_rowptr", C.c_void_p), ("D_col", C.c_void_p), ("D", C.c_void_p),
+    ]
+
+
+_lib = None
+
+
+def load_library(path=None):
+    """Load libh2b200.so (raises if absent: build with python -m paper_2109_05451_b200.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or LIB_PATH
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built (run python -m paper_2109_05451_b200.build); "
+                          "there is no CPU fallback")
+    lib = C.CDLL(path)
+    vp, i32, i64, d = C.c_void_p, C.c_int, C.c_int64, C.c_double
+    sig = {
+        "h2_create": ([C.POINTER(h2_desc), i32, vp, C.POINTER(vp)], i32),
+        "h2_matvec": ([vp, d, vp, d, vp, i32], i32),
+        "h2_matvec_ld": ([vp, d, vp, i64, d, vp, i64, i32], i32),
+        "h2_matvec_host": ([vp, d, vp, d, vp, i32], i32),
+        "h2_set_stream": ([vp, vp], i32),
+        "h2_stats": ([vp, i32, C.POINTER(d), C.POINTER(d), C.POINTER(d), C.POINTER(i32)], i32),
+        "h2_plan_counts": ([vp, C.POINTER(C.c_int64)], i32),
+        "h2_destroy": ([vp], i32),
+        "h2_nccl_unique_id": ([vp], i32),
+        "h2_last_error": ([], C.c_char_p),
+        "h2_version": ([], C.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes, f.restype = args, res
+    _lib = lib
+    return lib
+
+
+def _check(rc):
+    if rc != H2_OK:
+        raise H2Error(rc, _lib.h2_last_error().decode())
+
+
+def nccl_unique_id():
+    lib = load_library()
+    buf = (C.c_uint8 * 128)()
+    _check(lib.h2_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+def _is_torch(a):
+    return type(a).__module__.startswith("torch")
+
+
+class H2Operator:
+    """One rank's H² operator on the GPU (h2_create / h2_matvec / h2_destroy).
+
+    Floating arrays: numpy arrays (HOST: copied) or CUDA torch tensors (DEVICE: adopted and
+    kept alive by this object); all of one kind.  Integer arrays: numpy.  Shapes follow
+    include/h2.h (column-major small matrices)."""
+
+    def __init__(self, *, depth, leaf_size, level_rank, leaf_ptr, U_leaf, V_leaf, E, F, S_rowptr,
+                 S_col, S, D_rowptr, D_col, D, n_local, rank=0, nranks=1, dtype="f64", nv_max=16,
+                 nccl_id=None):
+        lib = load_library()
+        self._lib = lib
+        self.dtype = {"f64": H2_F64, "f32": H2_F32}[dtype]
+        self.np_dtype = np.float64 if self.dtype == H2_F64 else np.float32
+        self.n_local, self.nv_max, self.rank, self.nranks = int(n_local), int(nv_max), rank, nranks
+        fl = [U_leaf, V_leaf, D] + [a for a in list(E) + list(F) + list(S) if a is not None]
+        device = any(_is_torch(a) and a.is_cuda for a in fl)
+        self._keep = []
+
+        def fptr(a):
+            if a is None:
+                return None
+            if device:
+                if not (_is_torch(a) and a.is_cuda and a.is_contiguous()):
+                    raise ValueError("device mode needs contiguous CUDA tensors for every float array")
+                want = "torch.float64" if self.dtype == H2_F64 else "torch.float32"
+                if str(a.dtype) != want:
+                    raise ValueError(f"float arrays must be {want}")
+                self._keep.append(a)
+                return a.data_ptr()
+            a = np.ascontiguousarray(a, dtype=self.np_dtype)
+            self._keep.append(a)
+            return a.ctypes.data
+
+        def iptr(a, dt):
+            a = np.ascontiguousarray(a, dtype=dt)
+            self._keep.append(a)
+            return a.ctypes.data
+
+        q = int(depth)
+        arr = lambda vals: (C.c_void_p * (q + 1))(*vals)
+        self._E = arr([fptr(e) if e is not None else None for e in E])
+        self._F = arr([fptr(f) if f is not None else None for f in F])
+        self._Srp = arr([iptr(r, np.int64) for r in S_rowptr])
+        self._Scol = arr([iptr(c, np.int32) for c in S_col])
+        self._S = arr([fptr(s) if (s is not None and s.size if not _is_torch(s) else s.numel()) else None
+                       for s in S])
+        d = h2_desc()
+        d.dtype, d.mem, d.depth, d.leaf_size = self.dtype, H2_MEM_DEVICE if device else H2_MEM_HOST, q, int(leaf_size)
+        d.rank, d.nranks, d.n_local = int(rank), int(nranks), int(n_local)
+        d.level_rank = iptr(level_rank, np.int32)
+        d.leaf_ptr = iptr(leaf_ptr, np.int64)
+        d.U_leaf, d.V_leaf = fptr(U_leaf), fptr(V_leaf)
+        d.E, d.F = C.cast(self._E, C.c_void_p), C.cast(self._F, C.c_void_p)
+        d.S_rowptr, d.S_col, d.S = (C.cast(self._Srp, C.c_void_p), C.cast(self._Scol, C.c_void_p),
+                                    C.cast(self._S, C.c_void_p))
+        d.D_rowptr, d.D_col = iptr(D_rowptr, np.int64), iptr(D_col, np.int32)
+        d.D = fptr(D) if (D is not None and (D.numel() if _is_torch(D) else D.size)) else None
+        idbuf = None
+        if nranks > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("nccl_id (128 bytes) required when nranks > 1")
+            idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        h = C.c_void_p()
+        _check(lib.h2_create(C.byref(d), int(nv_max), C.cast(idbuf, C.c_void_p) if idbuf else None, C.byref(h)))
+        self.handle = h
+        if not device:
+            self._keep = []     # host arrays were copied by h2_create
+
+    # -- calls
+    def set_stream(self, stream_ptr):
+        _check(self._lib.h2_set_stream(self.handle, C.c_void_p(int(stream_ptr))))
+
+    def matvec(self, X, Y, alpha=1.0, beta=0.0, stream=None):
+        """Y := alpha A X + beta Y.  X, Y: CUDA tensors of shape (nv, n_local) (contiguous ==
+        n_local x nv column-major).  Asynchronous on `stream` (default: torch's current stream)."""
+        import torch
+        nv = X.shape[0]
+        if X.shape != (nv, self.n_local) or Y.shape != X.shape or not (X.is_contiguous() and Y.is_contiguous()):
+            raise ValueError("X, Y must be contiguous (nv, n_local)")
+        st = stream if stream is not None else torch.cuda.current_stream(X.device)
+        self.set_stream(st.cuda_stream)
+        _check(self._lib.h2_matvec(self.handle, float(alpha), X.data_ptr(), float(beta), Y.data_ptr(), nv))
+        return Y
+
+    def matvec_host(self, X, Y, alpha=1.0, beta=0.0, stream=None):
+        """End-to-end: X, Y host arrays (nv, n_local) (numpy or pinned CPU torch tensors)."""
+        ptr = lambda a: a.data_ptr() if _is_torch(a) else a.ctypes.data
+        nv = X.shape[0]
+        if stream is not None:
+            self.set_stream(stream.cuda_stream)
+        _check(self._lib.h2_matvec_host(self.handle, float(alpha), ptr(X), float(beta), ptr(Y), nv))
+        return Y
+
+    def stats(self, nv):
+        f, b, x, n = C.c_double(), C.c_double(), C.c_double(), C.c_int()
+        _check(self._lib.h2_stats(self.handle, int(nv), C.byref(f), C.byref(b), C.byref(x), C.byref(n)))
+        return {"flops": f.value, "bytes": b.value, "xchg_bytes": x.value, "launches": n.value}
+
+    def plan_counts(self):
+        c = (C.c_int64 * 8)()
+        _check(self._lib.h2_plan_counts(self.handle, c))
+        keys = ["diag_S", "offdiag_S", "root_S", "diag_D", "offdiag_D", "peers", "recv_nodes", "recv_leaves"]
+        return dict(zip(keys, list(c)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _check(self._lib.h2_destroy(self.handle))
+            self.handle = None
+            self._keep = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,1001 @@
+// h2_api.cpp -- C ABI (include/h2.h): validation, the static execution plan, device memory,
+// the NCCL exchange, and the per-call launch sequence of the distributed H^2 matvec.
+//
+// The plan replaces the paper's per-call marshaling kernels with
+// task/block tables built once here: every output node of every phase becomes one warp task
+// whose blocks point straight at their operands (implicit heap addressing, no pointer arrays
+// rebuilt per call).  Distribution follows PAPER.md:195-206 (block rows, C-level C = log2 P,
+// replicated top tree = reading R16) and PAPER.md:445-502 (diagonal / off-diagonal split,
+// compressed node lists pid / nodes_ptr / nodes, one exchange per matvec overlapped with the
+// diagonal multiply).
+#include "../../include/h2.h"
+#include "h2_internal.h"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <numeric>
+#include <string>
+#include <vector>
+
+using namespace h2;
+
+namespace {
+
+thread_local std::string g_err = "no error";
+
+int fail(int code, const std::string &msg)
+{
+    g_err = msg;
+    return code;
+}
+
+// ------------------------------------------------------------------ NCCL (loaded lazily)
+struct NcclApi {
+    bool loaded = false;
+    void *lib = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+};
+NcclApi g_nccl;
+
+#ifndef H2_NCCL_DEFAULT
+#define H2_NCCL_DEFAULT "libnccl.so.2"
+#endif
+
+bool load_nccl()
+{
+    if (g_nccl.loaded) return true;
+    const char *cands[3] = {getenv("H2_NCCL_LIB"), "libnccl.so.2", H2_NCCL_DEFAULT};
+    for (const char *c : cands) {
+        if (!c) continue;
+        g_nccl.lib = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+        if (g_nccl.lib) break;
+    }
+    if (!g_nccl.lib) return false;
+#define H2_SYM(field, name) \
+    g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(g_nccl.lib, name)); \
+    if (!g_nccl.field) return false;
+    H2_SYM(CommInitRank, "ncclCommInitRank")
+    H2_SYM(CommDestroy, "ncclCommDestroy")
+    H2_SYM(Send, "ncclSend")
+    H2_SYM(Recv, "ncclRecv")
+    H2_SYM(AllGather, "ncclAllGather")
+    H2_SYM(GroupStart, "ncclGroupStart")
+    H2_SYM(GroupEnd, "ncclGroupEnd")
+    H2_SYM(GetErrorString, "ncclGetErrorString")
+    H2_SYM(GetUniqueId, "ncclGetUniqueId")
+#undef H2_SYM
+    g_nccl.loaded = true;
+    return true;
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------ host-side plan
+struct Layout {
+    int q = 0, m = 0, p = 0, P = 1, C = 0;
+    std::vector<int> k;
+    int64_t held(int l) const { return l < C ? (int64_t)1 << l : (int64_t)1 << (l - C); }
+    int64_t g0(int l) const { return l < C ? 0 : (int64_t)p << (l - C); }
+    int owner(int l, int64_t g) const { return l < C ? -1 : (int)(g >> (l - C)); }
+};
+
+// Remote (level, global node) -> key for ordered maps
+inline int64_t node_key(int l, int64_t g) { return ((int64_t)l << 40) | g; }
+inline int key_level(int64_t key) { return (int)(key >> 40); }
+inline int64_t key_node(int64_t key) { return key & (((int64_t)1 << 40) - 1); }
+
+// Validation of the description (H2_ERR_* codes, message in g_err).
+int validate(const h2_desc *d, int nv_max, Layout &L)
+{
+    if (!d) return fail(H2_ERR_ARG, "desc is NULL");
+    if (d->dtype != H2_F64 && d->dtype != H2_F32) return fail(H2_ERR_ARG, "unknown dtype");
+    if (d->mem != H2_MEM_HOST && d->mem != H2_MEM_DEVICE) return fail(H2_ERR_ARG, "unknown mem kind");
+    if (nv_max < 1 || nv_max > 64) return fail(H2_ERR_SHAPE, "nv_max must be in [1, 64]");
+    if (d->depth < 0 || d->depth > 30) return fail(H2_ERR_STRUCT, "depth out of range [0, 30]");
+    if (d->leaf_size < 1 || d->leaf_size > KMAX) return fail(H2_ERR_SHAPE, "leaf_size must be in [1, 64]");
+    if (d->nranks < 1 || (d->nranks & (d->nranks - 1)))
+        return fail(H2_ERR_STRUCT, "nranks must be a power of two");
+    if (d->rank < 0 || d->rank >= d->nranks) return fail(H2_ERR_ARG, "rank out of range");
+    int C = 0;
+    while ((1 << C) < d->nranks) ++C;
+    if (C > d->depth) return fail(H2_ERR_STRUCT, "P too large for depth (P > 2^q)");
+    if (!d->level_rank || !d->leaf_ptr || !d->U_leaf || !d->V_leaf || !d->S_rowptr || !d->S_col ||
+        !d->S || !d->D_rowptr || (d->depth > 0 && (!d->E || !d->F)))
+        return fail(H2_ERR_ARG, "NULL array in desc");
+    L.q = d->depth; L.m = d->leaf_size; L.p = d->rank; L.P = d->nranks; L.C = C;
+    L.k.resize(L.q + 1);
+    for (int l = 0; l <= L.q; ++l) {
+        int k = d->level_rank[l];
+        if (k < 1 || k > KMAX) return fail(H2_ERR_SHAPE, "level rank k^l must be in [1, 64]");
+        L.k[l] = k;
+    }
+    const int64_t nleaf = L.held(L.q);
+    const int64_t *lp = d->leaf_ptr;
+    if (lp[0] != 0) return fail(H2_ERR_STRUCT, "leaf_ptr[0] must be 0");
+    for (int64_t i = 0; i < nleaf; ++i) {
+        int64_t sz = lp[i + 1] - lp[i];
+        if (sz < 1 || sz > L.m) return fail(H2_ERR_STRUCT, "leaf sizes must be in [1, m]");
+    }
+    if (lp[nleaf] != d->n_local) return fail(H2_ERR_STRUCT, "leaf_ptr[end] != n_local");
+    for (int l = 0; l <= L.q; ++l) {
+        const int64_t *rp = d->S_rowptr[l];
+        const int32_t *col = d->S_col[l];
+        const int64_t rows = L.held(l);
+        if (!rp) return fail(H2_ERR_ARG, "S_rowptr[l] is NULL");
+        if (rp[0] != 0) return fail(H2_ERR_STRUCT, "S_rowptr[l][0] must be 0");
+        for (int64_t i = 0; i < rows; ++i) {
+            if (rp[i + 1] < rp[i]) return fail(H2_ERR_STRUCT, "S_rowptr not monotone");
+            for (int64_t b = rp[i]; b < rp[i + 1]; ++b) {
+                if (col[b] < 0 || col[b] >= ((int64_t)1 << l))
+                    return fail(H2_ERR_STRUCT, "S_col out of range");
+                if (b > rp[i] && col[b] <= col[b - 1])
+                    return fail(H2_ERR_STRUCT, "S_col not strictly ascending within a row (duplicate block?)");
+                if (l < C) {
+                    // top-tree rows are replicated; nothing else to check
+                }
+            }
+        }
+        if (rp[rows] > 0 && !d->S[l]) return fail(H2_ERR_ARG, "S[l] is NULL but level has blocks");
+        if (l >= 1 && (!d->E[l] || !d->F[l])) return fail(H2_ERR_ARG, "E[l] / F[l] is NULL");
+    }
+    {
+        const int64_t *rp = d->D_rowptr;
+        if (rp[0] != 0) return fail(H2_ERR_STRUCT, "D_rowptr[0] must be 0");
+        for (int64_t i = 0; i < nleaf; ++i) {
+            if (rp[i + 1] < rp[i]) return fail(H2_ERR_STRUCT, "D_rowptr not monotone");
+            for (int64_t b = rp[i]; b < rp[i + 1]; ++b) {
+                if (d->D_col[b] < 0 || d->D_col[b] >= ((int64_t)1 << L.q))
+                    return fail(H2_ERR_STRUCT, "D_col out of range");
+                if (b > rp[i] && d->D_col[b] <= d->D_col[b - 1])
+                    return fail(H2_ERR_STRUCT, "D_col not strictly ascending within a row");
+            }
+        }
+        if (rp[nleaf] > 0 && !d->D) return fail(H2_ERR_ARG, "D is NULL but there are dense blocks");
+    }
+    return H2_OK;
+}
+
+struct Phase {
+    int64_t t0 = 0;
+    int n = 0;
+    int rpl = 1;
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ the handle
+struct h2_ctx {
+    Layout L;
+    int dtype = H2_F64;
+    size_t esz = 8;
+    int nv_max = 1;
+    int64_t n_local = 0, nleaf = 0;
+    bool sticky = false;
+    bool has_top = false;            // P > 1 and the top tree (levels < C) holds couplings
+    cudaStream_t stream = nullptr;   // caller's stream (default legacy)
+    cudaStream_t s_comm = nullptr;
+    cudaEvent_t ev_packed = nullptr, ev_recv = nullptr;
+    std::vector<void *> owned;       // device allocations to free
+    // operator (device)
+    const void *U = nullptr, *Vt = nullptr, *D = nullptr;
+    std::vector<const void *> E, Ft, S;
+    const void *FtC_all = nullptr;   // P > 1 && has_top: all ranks' F_C^T (allgathered)
+    // workspaces (device): plane layout, element (j, n) of a region at off + j + n * plane
+    void *xh = nullptr, *yh = nullptr;
+    int64_t xh_plane = 0, yh_plane = 0;
+    std::vector<int64_t> xh_base, yh_base;
+    int64_t xgather = -1;            // level-C all-rank roots region (has_top)
+    void *xsend = nullptr, *xrecv = nullptr, *hsend = nullptr, *hrecv = nullptr;
+    // plan (device)
+    Task *d_tasks = nullptr;
+    Blk *d_blks = nullptr;
+    PackSeg *d_segs = nullptr;
+    Phase up_leaf, coup_off[2], leaf;
+    std::vector<Phase> up_lv, top_up_lv, coup_diag, down_lv;
+    std::vector<int> up_lv_level, top_up_level, down_level;
+    int64_t nseg_x = 0, nseg_h = 0, seg_x0 = 0, seg_h0 = 0;
+    struct Peer {
+        int rank;
+        int64_t xs_off = 0, xs_cnt = 0, xr_off = 0, xr_cnt = 0;   // elements per vector
+        int64_t hs_off = 0, hs_cnt = 0, hr_off = 0, hr_cnt = 0;   // rows per vector
+    };
+    std::vector<Peer> peers;
+    int64_t xsend_tot = 0, xrecv_tot = 0, hsend_tot = 0, hrecv_tot = 0;
+    ncclComm_t comm = nullptr;
+    // e2e staging
+    void *dX = nullptr, *dY = nullptr;
+    // stats
+    double ops_local = 0;            // stored operator scalars held by this rank
+    int64_t counts[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int launches_per_call = 0;
+};
+
+namespace {
+
+int cuda_fail(h2_ctx *h, cudaError_t e, const char *what)
+{
+    if (h) h->sticky = true;
+    return fail(e == cudaErrorMemoryAllocation ? H2_ERR_OOM : H2_ERR_CUDA,
+                std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define H2_CUDA(h, call)                                       \
+    do {                                                       \
+        cudaError_t e_ = (call);                               \
+        if (e_ != cudaSuccess) return cuda_fail(h, e_, #call); \
+    } while (0)
+
+#define H2_NCCL(h, call)                                                             \
+    do {                                                                             \
+        ncclResult_t r_ = (call);                                                    \
+        if (r_ != ncclSuccess) {                                                     \
+            if (h) h->sticky = true;                                                 \
+            return fail(H2_ERR_NCCL, std::string(#call) + ": " + g_nccl.GetErrorString(r_)); \
+        }                                                                            \
+    } while (0)
+
+void *dalloc(h2_ctx *h, size_t bytes, cudaError_t &err)
+{
+    void *p = nullptr;
+    if (bytes == 0) bytes = 16;
+    err = cudaMalloc(&p, bytes);
+    if (err != cudaSuccess) return nullptr;
+    h->owned.push_back(p);
+    return p;
+}
+
+ncclDataType_t nccl_type(int dtype) { return dtype == H2_F64 ? ncclDouble : ncclFloat; }
+
+int release(h2_ctx *h)
+{
+    if (!h) return H2_OK;
+    if (h->comm && g_nccl.loaded) g_nccl.CommDestroy(h->comm);
+    for (void *p : h->owned) cudaFree(p);
+    if (h->s_comm) cudaStreamDestroy(h->s_comm);
+    if (h->ev_packed) cudaEventDestroy(h->ev_packed);
+    if (h->ev_recv) cudaEventDestroy(h->ev_recv);
+    delete h;
+    return H2_OK;
+}
+
+// Copy (HOST) or adopt (DEVICE) a floating array of `n` elements.
+int put_array(h2_ctx *h, int mem, const void *src, int64_t n, const void **out)
+{
+    if (n == 0) { *out = nullptr; return H2_OK; }
+    if (mem == H2_MEM_DEVICE) { *out = src; return H2_OK; }
+    cudaError_t err;
+    void *p = dalloc(h, (size_t)n * h->esz, err);
+    if (!p) return cuda_fail(h, err, "cudaMalloc(operator)");
+    H2_CUDA(h, cudaMemcpy(p, src, (size_t)n * h->esz, cudaMemcpyHostToDevice));
+    *out = p;
+    return H2_OK;
+}
+
+// Transposed device copy of a batch of r x c column-major matrices (-> c x r column-major).
+int put_transposed(h2_ctx *h, int mem, const void *src, int64_t batch, int r, int c, const void **out)
+{
+    int64_t n = batch * r * c;
+    if (n == 0) { *out = nullptr; return H2_OK; }
+    cudaError_t err;
+    void *dst = dalloc(h, (size_t)n * h->esz, err);
+    if (!dst) return cuda_fail(h, err, "cudaMalloc(transposed)");
+    const void *dsrc = src;
+    void *tmp = nullptr;
+    if (mem == H2_MEM_HOST) {
+        H2_CUDA(h, cudaMalloc(&tmp, (size_t)n * h->esz));
+        cudaError_t e = cudaMemcpy(tmp, src, (size_t)n * h->esz, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) { cudaFree(tmp); return cuda_fail(h, e, "cudaMemcpy(transposed)"); }
+        dsrc = tmp;
+    }
+    cudaError_t e = h->dtype == H2_F64
+                        ? launch_transpose<double>((const double *)dsrc, (double *)dst, batch, r, c, 0)
+                        : launch_transpose<float>((const float *)dsrc, (float *)dst, batch, r, c, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (tmp) cudaFree(tmp);
+    if (e != cudaSuccess) return cuda_fail(h, e, "transpose");
+    *out = dst;
+    return H2_OK;
+}
+
+template <typename T>
+int run_matvec(h2_ctx *h, T alpha, const T *X, int64_t ldx, T beta, T *Y, int64_t ldy, int nv);
+
+}  // namespace
+
+// ======================================================================== create
+static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id, h2_handle *out)
+{
+    if (!out) return fail(H2_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    Layout L;
+    int rc = validate(d, nv_max, L);
+    if (rc != H2_OK) return rc;
+    if (L.P > 1 && !nccl_unique_id) return fail(H2_ERR_ARG, "nccl_unique_id required when nranks > 1");
+
+    h2_ctx *h = new (std::nothrow) h2_ctx();
+    if (!h) return fail(H2_ERR_OOM, "host allocation failed");
+    h->L = L;
+    h->dtype = d->dtype;
+    h->esz = d->dtype == H2_F64 ? 8 : 4;
+    h->nv_max = nv_max;
+    h->n_local = d->n_local;
+    h->nleaf = L.held(L.q);
+    const int q = L.q, m = L.m, p = L.p, P = L.P, C = L.C;
+    const std::vector<int> &k = L.k;
+    const int64_t nleaf = h->nleaf;
+
+#define H2_TRY(expr)                      \
+    do {                                  \
+        int rc_ = (expr);                 \
+        if (rc_ != H2_OK) {               \
+            std::string msg_ = g_err;     \
+            release(h);                   \
+            g_err = msg_;                 \
+            return rc_;                   \
+        }                                 \
+    } while (0)
+#define H2_TRYC(call)                                                 \
+    do {                                                              \
+        cudaError_t e_ = (call);                                      \
+        if (e_ != cudaSuccess) H2_TRY(cuda_fail(h, e_, #call));       \
+    } while (0)
+
+    // ---- top-tree couplings?
+    int64_t n_top = 0;
+    for (int l = 0; l < C; ++l) n_top += d->S_rowptr[l][L.held(l)];
+    h->has_top = (P > 1 && n_top > 0);
+
+    // ---- NCCL communicator
+    if (P > 1) {
+        if (!load_nccl()) { release(h); return fail(H2_ERR_NCCL, "cannot load libnccl.so.2 (set H2_NCCL_LIB)"); }
+        ncclUniqueId id;
+        memcpy(&id, nccl_unique_id, sizeof(id));
+        ncclResult_t r = g_nccl.CommInitRank(&h->comm, P, id, p);
+        if (r != ncclSuccess) {
+            std::string msg = std::string("ncclCommInitRank: ") + g_nccl.GetErrorString(r);
+            release(h);
+            return fail(H2_ERR_NCCL, msg);
+        }
+        H2_TRYC(cudaStreamCreateWithFlags(&h->s_comm, cudaStreamNonBlocking));
+        H2_TRYC(cudaEventCreateWithFlags(&h->ev_packed, cudaEventDisableTiming));
+        H2_TRYC(cudaEventCreateWithFlags(&h->ev_recv, cudaEventDisableTiming));
+    }
+
+    // ---- operator arrays on the device; V and F re-laid out as V^T, F^T (operand order)
+    const int kq = k[q];
+    H2_TRY(put_array(h, d->mem, d->U_leaf, nleaf * m * kq, &h->U));
+    H2_TRY(put_transposed(h, d->mem, d->V_leaf, nleaf, m, kq, &h->Vt));
+    h->E.assign(q + 1, nullptr);
+    h->Ft.assign(q + 1, nullptr);
+    h->S.assign(q + 1, nullptr);
+    double ops = 2.0 * nleaf * m * kq;
+    for (int l = 1; l <= q; ++l) {
+        H2_TRY(put_array(h, d->mem, d->E[l], L.held(l) * k[l] * k[l - 1], &h->E[l]));
+        H2_TRY(put_transposed(h, d->mem, d->F[l], L.held(l), k[l], k[l - 1], &h->Ft[l]));
+        ops += 2.0 * L.held(l) * k[l] * k[l - 1];
+    }
+    for (int l = 0; l <= q; ++l) {
+        int64_t nb = d->S_rowptr[l][L.held(l)];
+        H2_TRY(put_array(h, d->mem, d->S[l], nb * k[l] * k[l], &h->S[l]));
+        ops += (double)nb * k[l] * k[l];
+    }
+    const int64_t nD = d->D_rowptr[nleaf];
+    H2_TRY(put_array(h, d->mem, d->D, nD * m * m, &h->D));
+    ops += (double)nD * m * m;
+    h->ops_local = ops;
+
+    // ---- remote needs (compressed off-diagonal node lists)
+    std::map<int, std::vector<int64_t>> need_x;   // peer -> sorted unique node keys
+    std::map<int, std::vector<int64_t>> need_h;   // peer -> sorted unique global leaves
+    int64_t n_diag = 0, n_off = 0, n_root = 0, nd_diag = 0, nd_off = 0;
+    for (int l = 0; l <= q; ++l) {
+        const int64_t *rp = d->S_rowptr[l];
+        for (int64_t i = 0; i < L.held(l); ++i)
+            for (int64_t b = rp[i]; b < rp[i + 1]; ++b) {
+                int64_t s = d->S_col[l][b];
+                int o = L.owner(l, s);
+                if (o < 0) ++n_root;
+                else if (o == p) ++n_diag;
+                else { ++n_off; need_x[o].push_back(node_key(l, s)); }
+            }
+    }
+    for (int64_t t = 0; t < nleaf; ++t)
+        for (int64_t b = d->D_rowptr[t]; b < d->D_rowptr[t + 1]; ++b) {
+            int64_t s = d->D_col[b];
+            int o = L.owner(q, s);
+            if (o < 0 || o == p) ++nd_diag;
+            else { ++nd_off; need_h[o].push_back(s); }
+        }
+    for (auto &kv : need_x) {
+        auto &v = kv.second;
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+    }
+    for (auto &kv : need_h) {
+        auto &v = kv.second;
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+    }
+
+    // ---- workspaces
+    h->xh_base.assign(q + 1, 0);
+    h->yh_base.assign(q + 1, 0);
+    int64_t xo = 0, yo = 0;
+    for (int l = 0; l <= q; ++l) {
+        h->xh_base[l] = xo; xo += L.held(l) * k[l];
+        h->yh_base[l] = yo; yo += L.held(l) * k[l];
+    }
+    if (h->has_top) { h->xgather = xo; xo += (int64_t)P * k[C]; }
+    h->xh_plane = xo;
+    h->yh_plane = yo;
+    {
+        cudaError_t err;
+        h->xh = dalloc(h, (size_t)xo * nv_max * h->esz, err);
+        if (!h->xh) H2_TRY(cuda_fail(h, err, "cudaMalloc(x^ workspace)"));
+        h->yh = dalloc(h, (size_t)yo * nv_max * h->esz, err);
+        if (!h->yh) H2_TRY(cuda_fail(h, err, "cudaMalloc(y^ workspace)"));
+        H2_TRYC(cudaMemset(h->xh, 0, (size_t)xo * nv_max * h->esz));
+        H2_TRYC(cudaMemset(h->yh, 0, (size_t)yo * nv_max * h->esz));
+    }
+
+    // ---- distributed setup: leaf sizes of every rank, send lists, F_C of every rank
+    std::vector<int64_t> gleaf_size;        // global leaf sizes (P > 1)
+    std::map<int, std::vector<int64_t>> give_x, give_h;   // what each peer needs from me
+    if (P > 1) {
+        cudaError_t err;
+        // leaf sizes (allgather)
+        std::vector<int64_t> mine(nleaf);
+        for (int64_t i = 0; i < nleaf; ++i) mine[i] = d->leaf_ptr[i + 1] - d->leaf_ptr[i];
+        int64_t *dm = (int64_t *)dalloc(h, nleaf * 8, err);
+        int64_t *dall = (int64_t *)dalloc(h, nleaf * P * 8, err);
+        if (!dm || !dall) H2_TRY(cuda_fail(h, err, "cudaMalloc(setup)"));
+        H2_TRYC(cudaMemcpy(dm, mine.data(), nleaf * 8, cudaMemcpyHostToDevice));
+        H2_TRY([&]() -> int { H2_NCCL(h, g_nccl.AllGather(dm, dall, nleaf, ncclInt64, h->comm, h->s_comm)); return H2_OK; }());
+        H2_TRYC(cudaStreamSynchronize(h->s_comm));
+        gleaf_size.resize(nleaf * P);
+        H2_TRYC(cudaMemcpy(gleaf_size.data(), dall, nleaf * P * 8, cudaMemcpyDeviceToHost));
+        // request counts: cnt[2*o + 0/1] = #x^ nodes / #leaves I need from o
+        std::vector<int64_t> cnt(2 * P, 0), allcnt(2 * P * P, 0);
+        for (auto &kv : need_x) cnt[2 * kv.first] = (int64_t)kv.second.size();
+        for (auto &kv : need_h) cnt[2 * kv.first + 1] = (int64_t)kv.second.size();
+        int64_t *dc = (int64_t *)dalloc(h, 2 * P * 8, err);
+        int64_t *dac = (int64_t *)dalloc(h, 2 * P * P * 8, err);
+        if (!dc || !dac) H2_TRY(cuda_fail(h, err, "cudaMalloc(setup)"));
+        H2_TRYC(cudaMemcpy(dc, cnt.data(), 2 * P * 8, cudaMemcpyHostToDevice));
+        H2_TRY([&]() -> int { H2_NCCL(h, g_nccl.AllGather(dc, dac, 2 * P, ncclInt64, h->comm, h->s_comm)); return H2_OK; }());
+        H2_TRYC(cudaStreamSynchronize(h->s_comm));
+        H2_TRYC(cudaMemcpy(allcnt.data(), dac, 2 * P * P * 8, cudaMemcpyDeviceToHost));
+        // exchange the request lists (setup-time, "communicated among GPUs during
+        // the setup phase")
+        std::map<int, int64_t *> dreq_out, dreq_in;
+        std::map<int, std::vector<int64_t>> req_out;
+        for (int o = 0; o < P; ++o) {
+            if (o == p) continue;
+            std::vector<int64_t> v;
+            if (need_x.count(o)) v.insert(v.end(), need_x[o].begin(), need_x[o].end());
+            if (need_h.count(o)) v.insert(v.end(), need_h[o].begin(), need_h[o].end());
+            int64_t nin = allcnt[2 * P * o + 2 * p] + allcnt[2 * P * o + 2 * p + 1];
+            if (!v.empty()) {
+                dreq_out[o] = (int64_t *)dalloc(h, v.size() * 8, err);
+                if (!dreq_out[o]) H2_TRY(cuda_fail(h, err, "cudaMalloc(setup)"));
+                H2_TRYC(cudaMemcpy(dreq_out[o], v.data(), v.size() * 8, cudaMemcpyHostToDevice));
+                req_out[o] = v;
+            }
+            if (nin) {
+                dreq_in[o] = (int64_t *)dalloc(h, nin * 8, err);
+                if (!dreq_in[o]) H2_TRY(cuda_fail(h, err, "cudaMalloc(setup)"));
+            }
+        }
+        H2_TRY([&]() -> int {
+            H2_NCCL(h, g_nccl.GroupStart());
+            for (auto &kv : req_out)
+                H2_NCCL(h, g_nccl.Send(dreq_out[kv.first], kv.second.size(), ncclInt64, kv.first, h->comm, h->s_comm));
+            for (auto &kv : dreq_in) {
+                int o = kv.first;
+                int64_t nin = allcnt[2 * P * o + 2 * p] + allcnt[2 * P * o + 2 * p + 1];
+                H2_NCCL(h, g_nccl.Recv(kv.second, nin, ncclInt64, o, h->comm, h->s_comm));
+            }
+            H2_NCCL(h, g_nccl.GroupEnd());
+            return H2_OK;
+        }());
+        H2_TRYC(cudaStreamSynchronize(h->s_comm));
+        for (auto &kv : dreq_in) {
+            int o = kv.first;
+            int64_t nx = allcnt[2 * P * o + 2 * p], nh = allcnt[2 * P * o + 2 * p + 1];
+            std::vector<int64_t> v(nx + nh);
+            H2_TRYC(cudaMemcpy(v.data(), kv.second, (nx + nh) * 8, cudaMemcpyDeviceToHost));
+            for (int64_t i = 0; i < nx; ++i) {
+                int l = key_level(v[i]);
+                int64_t g = key_node(v[i]);
+                if (l > q || L.owner(l, g) != p) H2_TRY(fail(H2_ERR_STRUCT, "peer requested a node this rank does not own"));
+                give_x[o].push_back(v[i]);
+            }
+            for (int64_t i = nx; i < nx + nh; ++i) {
+                if (L.owner(q, v[i]) != p) H2_TRY(fail(H2_ERR_STRUCT, "peer requested a leaf this rank does not own"));
+                give_h[o].push_back(v[i]);
+            }
+        }
+        // F_C^T of every rank for the replicated top upsweep (branch-root transfers
+        // duplicated at the leaf level of the root branch)
+        if (h->has_top) {
+            int64_t per = (int64_t)k[C] * k[C - 1];
+            void *all = dalloc(h, (size_t)per * P * h->esz, err);
+            if (!all) H2_TRY(cuda_fail(h, err, "cudaMalloc(F_C)"));
+            H2_TRY([&]() -> int { H2_NCCL(h, g_nccl.AllGather(h->Ft[C], all, per, nccl_type(h->dtype), h->comm, h->s_comm)); return H2_OK; }());
+            H2_TRYC(cudaStreamSynchronize(h->s_comm));
+            h->FtC_all = all;
+        }
+    }
+
+    // ---- peers and exchange buffers (per-peer chunks of nv_max x cnt, nv-independent offsets)
+    std::map<int64_t, std::pair<int64_t, int64_t>> xrecv_pos;   // key -> (elem offset, ld)
+    std::map<int64_t, std::pair<int64_t, int64_t>> hrecv_pos;   // leaf -> (row offset, ld)
+    std::vector<PackSeg> segs_x, segs_h;
+    for (int o = 0; o < P; ++o) {
+        if (o == p) continue;
+        bool any = need_x.count(o) || need_h.count(o) || give_x.count(o) || give_h.count(o);
+        if (!any) continue;
+        h2_ctx::Peer pr;
+        pr.rank = o;
+        if (need_x.count(o))
+            for (int64_t key : need_x[o]) pr.xr_cnt += k[key_level(key)];
+        if (give_x.count(o))
+            for (int64_t key : give_x[o]) pr.xs_cnt += k[key_level(key)];
+        if (need_h.count(o))
+            for (int64_t g : need_h[o]) pr.hr_cnt += gleaf_size[g];
+        if (give_h.count(o))
+            for (int64_t g : give_h[o]) pr.hs_cnt += gleaf_size[g];
+        pr.xr_off = h->xrecv_tot; h->xrecv_tot += pr.xr_cnt * nv_max;
+        pr.xs_off = h->xsend_tot; h->xsend_tot += pr.xs_cnt * nv_max;
+        pr.hr_off = h->hrecv_tot; h->hrecv_tot += pr.hr_cnt * nv_max;
+        pr.hs_off = h->hsend_tot; h->hsend_tot += pr.hs_cnt * nv_max;
+        int64_t pos = 0;
+        if (need_x.count(o))
+            for (int64_t key : need_x[o]) { xrecv_pos[key] = {pr.xr_off + pos, pr.xr_cnt}; pos += k[key_level(key)]; }
+        pos = 0;
+        if (give_x.count(o))
+            for (int64_t key : give_x[o]) {
+                int l = key_level(key);
+                int64_t slot = key_node(key) - L.g0(l);
+                segs_x.push_back({h->xh_base[l] + slot * k[l], pr.xs_off + pos, k[l], (int32_t)pr.xs_cnt});
+                pos += k[l];
+            }
+        pos = 0;
+        if (need_h.count(o))
+            for (int64_t g : need_h[o]) { hrecv_pos[g] = {pr.hr_off + pos, pr.hr_cnt}; pos += gleaf_size[g]; }
+        pos = 0;
+        if (give_h.count(o))
+            for (int64_t g : give_h[o]) {
+                int64_t slot = g - L.g0(q);
+                int32_t len = (int32_t)(d->leaf_ptr[slot + 1] - d->leaf_ptr[slot]);
+                segs_h.push_back({d->leaf_ptr[slot], pr.hs_off + pos, len, (int32_t)pr.hs_cnt});
+                pos += len;
+            }
+        h->peers.push_back(pr);
+    }
+    if (P > 1) {
+        cudaError_t err;
+        h->xsend = dalloc(h, (size_t)h->xsend_tot * h->esz, err);
+        h->xrecv = dalloc(h, (size_t)h->xrecv_tot * h->esz, err);
+        h->hsend = dalloc(h, (size_t)h->hsend_tot * h->esz, err);
+        h->hrecv = dalloc(h, (size_t)h->hrecv_tot * h->esz, err);
+        if (!h->xsend || !h->xrecv || !h->hsend || !h->hrecv) H2_TRY(cuda_fail(h, err, "cudaMalloc(exchange buffers)"));
+    }
+
+    // ---- the task / block tables
+    std::vector<Task> tasks;
+    std::vector<Blk> blks;
+    auto esz = h->esz;
+    auto at = [esz](const void *base, int64_t elems) -> const void * {
+        return static_cast<const char *>(base) + (size_t)elems * esz;
+    };
+    auto rpl_of = [](int r) { return r > 32 ? 2 : 1; };
+
+    // (1) upsweep leaves: x^_s = V_s^T x_s
+    h->up_leaf.t0 = tasks.size();
+    for (int64_t s = 0; s < nleaf; ++s) {
+        Task t{h->xh_base[q] + s * kq, (int64_t)blks.size(), 1, (uint8_t)kq, (uint8_t)m,
+               (uint8_t)(d->leaf_ptr[s + 1] - d->leaf_ptr[s]), 0};
+        blks.push_back({at(h->Vt, s * kq * m), d->leaf_ptr[s], (int32_t)t.rows, 0});
+        tasks.push_back(t);
+    }
+    h->up_leaf.n = (int)nleaf;
+    h->up_leaf.rpl = rpl_of(kq);
+    // (2) local upsweep transfers, parents at levels q-1 .. C
+    for (int l = q; l >= C + 1; --l) {
+        Phase ph;
+        ph.t0 = tasks.size();
+        ph.rpl = rpl_of(k[l - 1]);
+        for (int64_t i = 0; i < L.held(l - 1); ++i) {
+            Task t{h->xh_base[l - 1] + i * k[l - 1], (int64_t)blks.size(), 2, (uint8_t)k[l - 1],
+                   (uint8_t)k[l], 0, 0};
+            for (int64_t c = 2 * i; c <= 2 * i + 1; ++c)
+                blks.push_back({at(h->Ft[l], c * k[l] * k[l - 1]), h->xh_base[l] + c * k[l], k[l], 0});
+            tasks.push_back(t);
+        }
+        ph.n = (int)L.held(l - 1);
+        h->up_lv.push_back(ph);
+        h->up_lv_level.push_back(l);
+    }
+    // (3) replicated top upsweep (P > 1 with top couplings): parents at levels C-1 .. 0
+    if (h->has_top) {
+        for (int l = C; l >= 1; --l) {
+            Phase ph;
+            ph.t0 = tasks.size();
+            ph.rpl = rpl_of(k[l - 1]);
+            for (int64_t i = 0; i < ((int64_t)1 << (l - 1)); ++i) {
+                Task t{h->xh_base[l - 1] + i * k[l - 1], (int64_t)blks.size(), 2, (uint8_t)k[l - 1],
+                       (uint8_t)k[l], 0, 0};
+                for (int64_t c = 2 * i; c <= 2 * i + 1; ++c) {
+                    if (l == C)
+                        blks.push_back({at(h->FtC_all, c * k[l] * k[l - 1]), h->xgather + c * k[l], k[l], 0});
+                    else
+                        blks.push_back({at(h->Ft[l], c * k[l] * k[l - 1]), h->xh_base[l] + c * k[l], k[l], 0});
+                }
+                tasks.push_back(t);
+            }
+            ph.n = 1 << (l - 1);
+            h->top_up_lv.push_back(ph);
+            h->top_up_level.push_back(l);
+        }
+    }
+    // (4) coupling multiply, diagonal part, all levels in one launch per rpl class
+    //     (PAPER.md:328-331, 496); every held row gets a task (empty rows write 0)
+    std::vector<Task> offd_tasks[2];
+    std::vector<Blk> offd_blks[2];
+    {
+        std::vector<Task> cls[2];
+        std::vector<std::vector<Blk>> cls_blk[2];
+        for (int l = 0; l <= q; ++l) {
+            if (l < C && !h->has_top) {
+                // top levels without couplings: y^ stays zero (workspace zeroed once), no tasks
+                continue;
+            }
+            const int64_t *rp = d->S_rowptr[l];
+            int ci = rpl_of(k[l]) - 1;
+            for (int64_t i = 0; i < L.held(l); ++i) {
+                std::vector<Blk> bl, offb;
+                for (int64_t b = rp[i]; b < rp[i + 1]; ++b) {
+                    int64_t s = d->S_col[l][b];
+                    int o = L.owner(l, s);
+                    const void *A = at(h->S[l], b * k[l] * k[l]);
+                    if (o < 0 || o == p)
+                        bl.push_back({A, h->xh_base[l] + (s - L.g0(l)) * k[l], k[l], 0});
+                    else {
+                        auto pos = xrecv_pos.at(node_key(l, s));
+                        offb.push_back({A, pos.first, k[l], (int32_t)pos.second});
+                    }
+                }
+                Task t{h->yh_base[l] + i * k[l], 0, (int32_t)bl.size(), (uint8_t)k[l], (uint8_t)k[l], 0, 0};
+                cls[ci].push_back(t);
+                cls_blk[ci].push_back(bl);
+                if (!offb.empty()) {
+                    Task to = t;
+                    to.nblk = (int32_t)offb.size();
+                    to.blk0 = (int64_t)offd_blks[ci].size();
+                    offd_tasks[ci].push_back(to);
+                    offd_blks[ci].insert(offd_blks[ci].end(), offb.begin(), offb.end());
+                }
+            }
+        }
+        for (int ci = 0; ci < 2; ++ci) {
+            // longest rows first (better tail balance)
+            std::vector<size_t> ord(cls[ci].size());
+            std::iota(ord.begin(), ord.end(), 0);
+            std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+                return cls[ci][a].nblk > cls[ci][b].nblk;
+            });
+            Phase ph;
+            ph.t0 = tasks.size();
+            ph.rpl = ci + 1;
+            ph.n = (int)ord.size();
+            for (size_t o : ord) {
+                Task t = cls[ci][o];
+                t.blk0 = (int64_t)blks.size();
+                blks.insert(blks.end(), cls_blk[ci][o].begin(), cls_blk[ci][o].end());
+                tasks.push_back(t);
+            }
+            if (ph.n) h->coup_diag.push_back(ph);
+        }
+        for (int ci = 0; ci < 2; ++ci) {
+            h->coup_off[ci].t0 = tasks.size();
+            h->coup_off[ci].rpl = ci + 1;
+            h->coup_off[ci].n = (int)offd_tasks[ci].size();
+            int64_t b0 = (int64_t)blks.size();
+            for (Task t : offd_tasks[ci]) { t.blk0 += b0; tasks.push_back(t); }
+            blks.insert(blks.end(), offd_blks[ci].begin(), offd_blks[ci].end());
+        }
+    }
+    // (5) downsweep transfers y^_c += E_c y^_parent, levels 1 .. q-1;
+    //     top levels only when the top tree has couplings (else they are all zero)
+    for (int l = 1; l <= q - 1; ++l) {
+        if (l <= C && !h->has_top) continue;
+        Phase ph;
+        ph.t0 = tasks.size();
+        ph.rpl = rpl_of(k[l]);
+        for (int64_t c = 0; c < L.held(l); ++c) {
+            int64_t g = L.g0(l) + c, gp = g >> 1;
+            int64_t pslot = gp - L.g0(l - 1);
+            Task t{h->yh_base[l] + c * k[l], (int64_t)blks.size(), 1, (uint8_t)k[l], (uint8_t)k[l - 1], 0, 0};
+            blks.push_back({at(h->E[l], c * k[l] * k[l - 1]), h->yh_base[l - 1] + pslot * k[l - 1], k[l - 1], 0});
+            tasks.push_back(t);
+        }
+        ph.n = (int)L.held(l);
+        h->down_lv.push_back(ph);
+        h->down_level.push_back(l);
+    }
+    // (6) leaves: last transfer, U expansion, dense near field, epilogue
+    {
+        const bool hasE = q >= 1 && (q > C || h->has_top);
+        h->leaf.t0 = tasks.size();
+        h->leaf.n = (int)nleaf;
+        h->leaf.rpl = rpl_of(m);
+        for (int64_t t = 0; t < nleaf; ++t) {
+            int64_t rows = d->leaf_ptr[t + 1] - d->leaf_ptr[t];
+            Task tk{d->leaf_ptr[t], (int64_t)blks.size(), 0, (uint8_t)m, (uint8_t)m, (uint8_t)rows,
+                    (uint8_t)(hasE ? 1 : 0)};
+            if (hasE) {
+                int64_t g = L.g0(q) + t, gp = g >> 1;
+                int64_t pslot = gp - L.g0(q - 1);
+                blks.push_back({at(h->E[q], t * kq * k[q - 1]), h->yh_base[q - 1] + pslot * k[q - 1], k[q - 1], 0});
+            }
+            blks.push_back({at(h->U, t * m * kq), h->yh_base[q] + t * kq, kq, 0});
+            for (int64_t b = d->D_rowptr[t]; b < d->D_rowptr[t + 1]; ++b) {
+                int64_t s = d->D_col[b];
+                int o = L.owner(q, s);
+                const void *A = at(h->D, b * m * m);
+                if (o == p) {
+                    int64_t slot = s - L.g0(q);
+                    blks.push_back({A, d->leaf_ptr[slot], (int32_t)(d->leaf_ptr[slot + 1] - d->leaf_ptr[slot]), 0});
+                } else {
+                    auto pos = hrecv_pos.at(s);
+                    blks.push_back({A, -1 - pos.first, (int32_t)gleaf_size[s], (int32_t)pos.second});
+                }
+            }
+            tk.nblk = (int32_t)(blks.size() - tk.blk0);
+            tasks.push_back(tk);
+        }
+    }
+    // ---- upload the plan
+    {
+        cudaError_t err;
+        h->d_tasks = (Task *)dalloc(h, tasks.size() * sizeof(Task), err);
+        h->d_blks = (Blk *)dalloc(h, blks.size() * sizeof(Blk), err);
+        std::vector<PackSeg> segs = segs_x;
+        h->seg_x0 = 0; h->nseg_x = (int64_t)segs_x.size();
+        h->seg_h0 = (int64_t)segs.size(); h->nseg_h = (int64_t)segs_h.size();
+        segs.insert(segs.end(), segs_h.begin(), segs_h.end());
+        h->d_segs = (PackSeg *)dalloc(h, segs.size() * sizeof(PackSeg), err);
+        if (!h->d_tasks || !h->d_blks || !h->d_segs) H2_TRY(cuda_fail(h, err, "cudaMalloc(plan)"));
+        H2_TRYC(cudaMemcpy(h->d_tasks, tasks.data(), tasks.size() * sizeof(Task), cudaMemcpyHostToDevice));
+        H2_TRYC(cudaMemcpy(h->d_blks, blks.data(), blks.size() * sizeof(Blk), cudaMemcpyHostToDevice));
+        if (!segs.empty())
+            H2_TRYC(cudaMemcpy(h->d_segs, segs.data(), segs.size() * sizeof(PackSeg), cudaMemcpyHostToDevice));
+        H2_TRYC(cudaDeviceSynchronize());
+    }
+    int64_t peers_n = (int64_t)h->peers.size(), xr = 0, hr = 0;
+    for (auto &kv : need_x) xr += (int64_t)kv.second.size();
+    for (auto &kv : need_h) hr += (int64_t)kv.second.size();
+    int64_t c8[8] = {n_diag, n_off, n_root, nd_diag, nd_off, peers_n, xr, hr};
+    memcpy(h->counts, c8, sizeof(c8));
+    int launches = 1 + (int)h->up_lv.size() + (int)h->coup_diag.size() + (int)h->down_lv.size() + 1;
+    if (P > 1) {
+        launches += 2;   // pack x^, pack halo
+        for (int ci = 0; ci < 2; ++ci) launches += h->coup_off[ci].n ? 1 : 0;
+        if (h->has_top) launches += (int)h->top_up_lv.size();
+    }
+    h->launches_per_call = launches;
+    *out = h;
+    return H2_OK;
+#undef H2_TRY
+#undef H2_TRYC
+}
+
+extern "C" int h2_create(const h2_desc *d, int nv_max, const void *nccl_unique_id, h2_handle *out)
+{
+    try {
+        return create_impl(d, nv_max, nccl_unique_id, out);
+    } catch (const std::exception &e) {
+        if (out) *out = nullptr;
+        return fail(H2_ERR_OOM, std::string("h2_create: ") + e.what());
+    }
+}
+
+// ======================================================================== matvec
+namespace {
+
+template <typename T>
+int run_matvec(h2_ctx *h, T alpha, const T *X, int64_t ldx, T beta, T *Y, int64_t ldy, int nv)
+{
+    const Layout &L = h->L;
+    const int q = L.q, C = L.C;
+    cudaStream_t st = h->stream;
+    T *xh = (T *)h->xh, *yh = (T *)h->yh;
+    if (alpha == T(0)) {
+        H2_CUDA(h, launch_scale<T>(Y, ldy, h->n_local, nv, beta, st));
+        return H2_OK;
+    }
+    auto T0 = [&](const Phase &ph) { return h->d_tasks + ph.t0; };
+    // 1. upsweep of the local branch (PAPER.md:281 / alg:upsweep2)
+    H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, X, ldx, xh, h->xh_plane, nv,
+                                 h->up_leaf.rpl, st));
+    for (const Phase &ph : h->up_lv)
+        H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, xh, h->xh_plane,
+                                  nv, ph.rpl, st));
+    // 2. exchange (P > 1): pack my x^ nodes and x leaves that peers need, one NCCL group on the
+    //    comm stream, overlapped with the diagonal multiply (alg:optimized_dist_mult)
+    if (L.P > 1) {
+        H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_x0, h->nseg_x, xh, h->xh_plane, (T *)h->xsend, nv, st));
+        H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_h0, h->nseg_h, X, ldx, (T *)h->hsend, nv, st));
+        H2_CUDA(h, cudaEventRecord(h->ev_packed, st));
+        H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_packed, 0));
+        ncclDataType_t ty = nccl_type(h->dtype);
+        H2_NCCL(h, g_nccl.GroupStart());
+        for (const auto &pr : h->peers) {
+            if (pr.xs_cnt) H2_NCCL(h, g_nccl.Send((T *)h->xsend + pr.xs_off, pr.xs_cnt * nv, ty, pr.rank, h->comm, h->s_comm));
+            if (pr.xr_cnt) H2_NCCL(h, g_nccl.Recv((T *)h->xrecv + pr.xr_off, pr.xr_cnt * nv, ty, pr.rank, h->comm, h->s_comm));
+            if (pr.hs_cnt) H2_NCCL(h, g_nccl.Send((T *)h->hsend + pr.hs_off, pr.hs_cnt * nv, ty, pr.rank, h->comm, h->s_comm));
+            if (pr.hr_cnt) H2_NCCL(h, g_nccl.Recv((T *)h->hrecv + pr.hr_off, pr.hr_cnt * nv, ty, pr.rank, h->comm, h->s_comm));
+        }
+        H2_NCCL(h, g_nccl.GroupEnd());
+        H2_CUDA(h, cudaEventRecord(h->ev_recv, h->s_comm));
+        // replicated top tree: gather the branch roots, upsweep the top
+        if (h->has_top) {
+            const int kC = L.k[C];
+            // own root -> gather slot p, then allgather in place over the P slots of every plane
+            for (int n = 0; n < nv; ++n) {
+                T *g = xh + h->xgather + (int64_t)n * h->xh_plane;
+                H2_CUDA(h, cudaMemcpyAsync(g + (int64_t)L.p * kC, xh + h->xh_base[C] + (int64_t)n * h->xh_plane,
+                                           kC * sizeof(T), cudaMemcpyDeviceToDevice, st));
+                H2_NCCL(h, g_nccl.AllGather(g + (int64_t)L.p * kC, g, kC, ty, h->comm, st));
+            }
+            for (const Phase &ph : h->top_up_lv)
+                H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, xh,
+                                          h->xh_plane, nv, ph.rpl, st));
+        }
+    }
+    // 3. coupling multiply, diagonal part (all levels) (alg:mult)
+    for (const Phase &ph : h->coup_diag)
+        H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
+                                  nv, ph.rpl, st));
+    // 4. off-diagonal part after the exchange (waitAll, alg:optimized_dist_mult line 11-12)
+    if (L.P > 1) {
+        H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_recv, 0));
+        for (int ci = 0; ci < 2; ++ci) {
+            const Phase &ph = h->coup_off[ci];
+            H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(ph), ph.n, h->d_blks, (const T *)h->xrecv, 0, yh,
+                                      h->yh_plane, nv, ph.rpl, st));
+        }
+    }
+    // 5. downsweep transfers (alg:downsweep)
+    for (const Phase &ph : h->down_lv)
+        H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(ph), ph.n, h->d_blks, yh, h->yh_plane, yh, h->yh_plane,
+                                  nv, ph.rpl, st));
+    // 6. leaves: last transfer + U expansion + dense + epilogue
+    const int kq = L.k[q], kp = q >= 1 ? L.k[q - 1] : 1;
+    H2_CUDA(h, launch_leaf<T>(T0(h->leaf), h->leaf.n, h->d_blks, yh, h->yh_plane, X, ldx,
+                              (const T *)h->hrecv, 0, Y, ldy, alpha, beta, nv, kq, kp,
+                              kq > 32 ? 2 : 1, h->leaf.rpl, st));
+    return H2_OK;
+}
+
+int check_call(h2_ctx *h, int nv)
+{
+    if (!h) return fail(H2_ERR_ARG, "handle is NULL");
+    if (h->sticky) return fail(H2_ERR_STATE, "handle unusable after an earlier CUDA/NCCL error");
+    if (nv < 1 || nv > h->nv_max) return fail(H2_ERR_ARG, "nv must be in [1, nv_max]");
+    return H2_OK;
+}
+
+}  // namespace
+
+extern "C" int h2_matvec_ld(h2_handle h, double alpha, const void *X, int64_t ldx, double beta,
+                            void *Y, int64_t ldy, int nv)
+{
+    int rc = check_call(h, nv);
+    if (rc != H2_OK) return rc;
+    if (!X || !Y) return fail(H2_ERR_ARG, "X or Y is NULL");
+    if (ldx < h->n_local || ldy < h->n_local) return fail(H2_ERR_SHAPE, "ld < n_local");
+    if (h->dtype == H2_F64)
+        return run_matvec<double>(h, alpha, (const double *)X, ldx, beta, (double *)Y, ldy, nv);
+    return run_matvec<float>(h, (float)alpha, (const float *)X, ldx, (float)beta, (float *)Y, ldy, nv);
+}
+
+extern "C" int h2_matvec(h2_handle h, double alpha, const void *X, double beta, void *Y, int nv)
+{
+    if (!h) return fail(H2_ERR_ARG, "handle is NULL");
+    return h2_matvec_ld(h, alpha, X, h->n_local, beta, Y, h->n_local, nv);
+}
+
+extern "C" int h2_matvec_host(h2_handle h, double alpha, const void *X, double beta, void *Y, int nv)
+{
+    int rc = check_call(h, nv);
+    if (rc != H2_OK) return rc;
+    if (!X || !Y) return fail(H2_ERR_ARG, "X or Y is NULL");
+    size_t bytes = (size_t)h->n_local * nv * h->esz;
+    if (!h->dX) {
+        cudaError_t err;
+        h->dX = dalloc(h, (size_t)h->n_local * h->nv_max * h->esz, err);
+        h->dY = dalloc(h, (size_t)h->n_local * h->nv_max * h->esz, err);
+        if (!h->dX || !h->dY) return cuda_fail(h, err, "cudaMalloc(e2e staging)");
+    }
+    H2_CUDA(h, cudaMemcpyAsync(h->dX, X, bytes, cudaMemcpyHostToDevice, h->stream));
+    if (beta != 0.0) H2_CUDA(h, cudaMemcpyAsync(h->dY, Y, bytes, cudaMemcpyHostToDevice, h->stream));
+    rc = h2_matvec_ld(h, alpha, h->dX, h->n_local, beta, h->dY, h->n_local, nv);
+    if (rc != H2_OK) return rc;
+    H2_CUDA(h, cudaMemcpyAsync(Y, h->dY, bytes, cudaMemcpyDeviceToHost, h->stream));
+    H2_CUDA(h, cudaStreamSynchronize(h->stream));
+    return H2_OK;
+}
+
+extern "C" int h2_set_stream(h2_handle h, void *stream)
+{
+    if (!h) return fail(H2_ERR_ARG, "handle is NULL");
+    h->stream = (cudaStream_t)stream;
+    return H2_OK;
+}
+
+extern "C" int h2_stats(h2_handle h, int nv, double *flops, double *bytes, double *xchg_bytes,
+                        int *launches)
+{
+    if (!h) return fail(H2_ERR_ARG, "handle is NULL");
+    if (nv < 1) return fail(H2_ERR_ARG, "nv < 1");
+    const Layout &L = h->L;
+    double tree = 0;
+    for (int l = 0; l <= L.q; ++l) tree += (double)L.held(l) * L.k[l];
+    if (flops) *flops = 2.0 * nv * h->ops_local;
+    // operator once + X read + Y write + x^, y^ trees written and read once each
+    if (bytes) *bytes = (double)h->esz * (h->ops_local + nv * (2.0 * h->n_local + 4.0 * tree));
+    if (xchg_bytes) {
+        double x = 0;
+        for (const auto &pr : h->peers) x += (double)(pr.xr_cnt + pr.hr_cnt) * nv * h->esz;
+        *xchg_bytes = x;
+    }
+    if (launches) *launches = h->launches_per_call;
+    return H2_OK;
+}
+
+extern "C" int h2_plan_counts(h2_handle h, int64_t counts[8])
+{
+    if (!h || !counts) return fail(H2_ERR_ARG, "NULL argument");
+    memcpy(counts, h->counts, sizeof(h->counts));
+    return H2_OK;
+}
+
+extern "C" int h2_destroy(h2_handle h)
+{
+    if (!h) return H2_OK;
+    cudaDeviceSynchronize();
+    return release(h);
+}
+
+extern "C" int h2_nccl_unique_id(void *out128)
+{
+    if (!out128) return fail(H2_ERR_ARG, "out is NULL");
+    if (!load_nccl()) return fail(H2_ERR_NCCL, "cannot load libnccl.so.2 (set H2_NCCL_LIB)");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId id;
+    ncclResult_t r = g_nccl.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(H2_ERR_NCCL, std::string("ncclGetUniqueId: ") + g_nccl.GetErrorString(r));
+    memcpy(out128, &id, sizeof(id));
+    return H2_OK;
+}
+
+extern "C" const char *h2_last_error(void) { return g_err.c_str(); }
+
+extern "C" const char *h2_version(void) { return "h2-b200 0.1 (sm_100a)"; }

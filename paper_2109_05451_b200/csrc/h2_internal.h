@@ -1,0 +1,69 @@
+// h2_internal.h -- shared between the host plan (h2_api.cpp) and the kernels (h2_kernels.cu).
+// Not part of the public ABI (include/h2.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace h2 {
+
+constexpr int KMAX = 64;   // max rank k^l and leaf size m supported by the kernels
+constexpr int XLD = 64;    // leading dimension of a staged x operand in shared memory
+constexpr int WPB = 8;     // warps per CTA of the row kernels
+
+// One block of a row task: y_rows += A (r x c, column-major) * x (c x nv)
+//   A     : device pointer to the block (already in the operand order the kernel wants)
+//   x     : element offset of the x operand's first row in its source (plane layout:
+//           element (j, n) at x + j + n * ld); for dense blocks x < 0 encodes a halo row
+//           offset (-x - 1) into the received-leaf buffer
+//   xrows : rows of x that are real (rows >= xrows are treated as 0: ragged leaves)
+//   xld   : leading dimension (between vectors) of this block's x source; 0 = the launch's
+//           default (per-peer receive chunks carry their own)
+struct Blk {
+    const void *A;
+    int64_t x;
+    int32_t xrows;
+    int32_t xld;
+};
+
+// One warp task: an output node / leaf and its list of blocks [blk0, blk0 + nblk).
+struct Task {
+    int64_t out;     // element offset of the output's first row (plane layout)
+    int64_t blk0;
+    int32_t nblk;
+    uint8_t r;       // output rows (rank k, or leaf size m for the leaf kernel)
+    uint8_t c;       // columns of every block in this task (k of the source level, or m)
+    uint8_t rows;    // leaf kernel: real rows of this leaf (<= m)
+    uint8_t flags;   // leaf kernel: bit0 = first block is the parent transfer E_t
+};
+
+// One contiguous run copied by the pack kernel: len rows of every vector.
+struct PackSeg {
+    int64_t src;     // element offset in the source (x^ workspace or X)
+    int64_t dst;     // element offset in the send buffer
+    int32_t len;
+    int32_t dst_ld;  // distance between vectors in the destination (per-peer chunk)
+};
+
+// Kernel launchers (h2_kernels.cu).  T = double or float.  Each returns cudaGetLastError().
+template <typename T>
+cudaError_t launch_up_leaf(const Task *t, int ntask, const Blk *b, const T *X, int64_t ldx,
+                           T *xh, int64_t xh_ld, int nv, int rpl, cudaStream_t s);
+template <typename T>
+cudaError_t launch_rows(int mode, const Task *t, int ntask, const Blk *b, const T *src,
+                        int64_t src_ld, T *dst, int64_t dst_ld, int nv, int rpl, cudaStream_t s);
+template <typename T>
+cudaError_t launch_leaf(const Task *t, int ntask, const Blk *b, const T *yh, int64_t yh_ld,
+                        const T *X, int64_t ldx, const T *halo, int64_t halo_ld, T *Y,
+                        int64_t ldy, T alpha, T beta, int nv, int k, int kp, int rplk, int rplm,
+                        cudaStream_t s);
+template <typename T>
+cudaError_t launch_scale(T *Y, int64_t ldy, int64_t n, int nv, T beta, cudaStream_t s);
+template <typename T>
+cudaError_t launch_transpose(const T *src, T *dst, int64_t batch, int r, int c, cudaStream_t s);
+template <typename T>
+cudaError_t launch_pack(const PackSeg *segs, int64_t nseg, const T *src, int64_t src_ld, T *dst,
+                        int nv, cudaStream_t s);
+
+enum { MODE_WRITE = 0, MODE_ACCUM = 1 };
+
+}  // namespace h2

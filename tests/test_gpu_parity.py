@@ -1,0 +1,153 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle, element by element on the
+same seeded inputs.  Tolerances (north_star): relative 2-norm <= 1e-12 per
+column in FP64; <= 1e-5 in FP32 against the FP64 oracle run on the FP32-rounded inputs."""
+import numpy as np
+import pytest
+
+import oracle
+from h2gen import build_config, make_xy
+from tests.gpu_util import colmax_rel, random_case, gpu_matvec
+
+pytestmark = pytest.mark.gpu
+
+TOL64, TOL32 = 1e-12, 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2109_05451_b200 import load_library
+    load_library()
+
+
+def _op(h, **kw):
+    from paper_2109_05451_b200 import operator_from_h2data
+    return operator_from_h2data(h, **kw)
+
+
+def test_cfg1_parity():
+    h = build_config("cfg1")
+    op = _op(h, nv_max=1)
+    X = make_xy(h.perm, 1, 1, -1.0, 1.0)
+    Y0 = make_xy(h.perm, 1, 2, -1.0, 1.0, stream=1)
+    ref = oracle.matvec(h, X, -0.7, 0.3, Y0)
+    out = gpu_matvec(op, X, -0.7, 0.3, Y0)
+    assert colmax_rel(out, ref) <= TOL64
+
+
+@pytest.mark.parametrize("N,m,kfn,nv,seed", [
+    (700, 16, lambda l: 5 + (l * 3) % 9, 1, 1),           # ragged leaves, varying small ranks
+    (2000, 32, lambda l: 16, 3, 2),
+    (3000, 64, lambda l: 25, 17, 3),                      # k = 25, nv = 17 (two vector chunks)
+    (3000, 64, lambda l: 36, 16, 4),
+    (2500, 64, lambda l: 64, 2, 5),                       # k = 64 (two rows per lane)
+    (1500, 32, lambda l: 40 if l % 2 else 20, 64, 6),     # k alternating across 32, nv = 64
+    (1000, 64, lambda l: 33, 5, 7),
+])
+def test_random_structures(N, m, kfn, nv, seed):
+    h = random_case(N, m, kfn, seed)
+    op = _op(h, nv_max=nv)
+    X = make_xy(h.perm, nv, seed, -1.0, 1.0)
+    Y0 = make_xy(h.perm, nv, seed, -1.0, 1.0, stream=1)
+    ref = oracle.matvec(h, X, 1.3, -0.4, Y0)
+    out = gpu_matvec(op, X, 1.3, -0.4, Y0)
+    assert colmax_rel(out, ref) <= TOL64
+
+
+def test_beta_zero_nan_and_alpha_zero():
+    h = random_case(900, 32, lambda l: 12, 11)
+    op = _op(h, nv_max=2)
+    X = make_xy(h.perm, 2, 1, -1.0, 1.0)
+    Ynan = np.full((2, h.N), np.nan)
+    out = gpu_matvec(op, X, 0.9, 0.0, Ynan)
+    assert np.all(np.isfinite(out))
+    assert colmax_rel(out, oracle.matvec(h, X, 0.9)) <= TOL64
+    Y0 = make_xy(h.perm, 2, 3, stream=1)
+    out = gpu_matvec(op, X, 0.0, 0.5, Y0)
+    assert np.array_equal(out, 0.5 * Y0)
+
+
+def test_nv_smaller_than_nv_max_and_repeat_calls():
+    h = random_case(1200, 32, lambda l: 16, 12)
+    op = _op(h, nv_max=16)
+    for nv in (1, 5, 16):
+        X = make_xy(h.perm, nv, nv, -1.0, 1.0)
+        ref = oracle.matvec(h, X)
+        for _ in range(2):
+            out = gpu_matvec(op, X, 1.0, 0.0, np.zeros_like(X))
+            assert colmax_rel(out, ref) <= TOL64
+
+
+def test_device_adopted_equals_host_copied():
+    h = random_case(1500, 32, lambda l: 16, 13)
+    X = make_xy(h.perm, 4, 1, -1.0, 1.0)
+    a = gpu_matvec(_op(h, nv_max=4), X, 1.0, 0.0, np.zeros_like(X))
+    b = gpu_matvec(_op(h, nv_max=4, device=True), X, 1.0, 0.0, np.zeros_like(X))
+    assert np.array_equal(a, b)
+
+
+def test_fp32_path():
+    h = random_case(2000, 64, lambda l: 25, 14)
+    h32 = h.astype(np.float32)
+    op = _op(h32, nv_max=16, dtype="f32")
+    X = make_xy(h.perm, 16, 1, -1.0, 1.0).astype(np.float32)
+    Y0 = make_xy(h.perm, 16, 2, -1.0, 1.0, stream=1).astype(np.float32)
+    ref = oracle.matvec(h32.astype(np.float64), X.astype(np.float64), 1.1, 0.25, Y0.astype(np.float64))
+    out = gpu_matvec(op, X, 1.1, 0.25, Y0, dtype="f32")
+    assert colmax_rel(out, ref) <= TOL32
+
+
+def test_e2e_host_buffers_equal_device():
+    h = random_case(1500, 32, lambda l: 16, 15)
+    op = _op(h, nv_max=3)
+    X = make_xy(h.perm, 3, 1, -1.0, 1.0)
+    Y0 = make_xy(h.perm, 3, 2, -1.0, 1.0, stream=1)
+    dev = gpu_matvec(op, X, 0.8, 0.2, Y0)
+    Yh = Y0.copy()
+    op.matvec_host(np.ascontiguousarray(X), Yh, 0.8, 0.2)
+    assert np.array_equal(Yh, dev)
+
+
+def test_single_leaf_and_all_dense():
+    from h2gen import build_cluster_tree, dual_traversal, random_h2_data
+    from h2gen.tree import uniform_points
+    tr = build_cluster_tree(uniform_points(40, 2, 3), 64)   # q = 0: one dense block
+    st = dual_traversal(tr, 0.9)
+    h = random_h2_data(tr, st, [7], 3)
+    X = make_xy(h.perm, 2, 1, -1.0, 1.0)
+    assert colmax_rel(gpu_matvec(_op(h, nv_max=2), X, 1.0, 0.0, np.zeros_like(X)),
+                      oracle.matvec(h, X)) <= TOL64
+    tr = build_cluster_tree(uniform_points(800, 2, 4), 32)
+    st = dual_traversal(tr, 0.9, all_dense=True)
+    h = random_h2_data(tr, st, [9] * (tr.q + 1), 4)
+    X = make_xy(h.perm, 2, 1, -1.0, 1.0)
+    assert colmax_rel(gpu_matvec(_op(h, nv_max=2), X, 1.0, 0.0, np.zeros_like(X)),
+                      oracle.matvec(h, X)) <= TOL64
+
+
+def test_per_phase_trees_cfg1():
+    """Y of a pure-low-rank operator (dense blocks zeroed) isolates upsweep + coupling + downsweep."""
+    h = build_config("cfg1")
+    h.D = np.zeros_like(h.D)
+    X = make_xy(h.perm, 2, 5, -1.0, 1.0)
+    ref = oracle.matvec(h, X)
+    out = gpu_matvec(_op(h, nv_max=2), X, 1.0, 0.0, np.zeros_like(X))
+    assert colmax_rel(out, ref) <= TOL64
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("nv", [1, 16])
+def test_cfg2_full_size_sampled(nv):
+    """The bench workload at its full size and launch configuration: sampled-row oracle on 2% of
+    the leaves (exact arithmetic of those rows), alpha=1, beta=0."""
+    h = build_config("cfg2")
+    op = _op(h, nv_max=16)
+    X = make_xy(h.perm, nv, 3, 0.0, 1.0)
+    out = gpu_matvec(op, X, 1.0, 0.0, np.zeros_like(X))
+    mask = np.zeros(1 << h.q, dtype=bool)
+    mask[np.random.default_rng(0).choice(mask.size, mask.size // 50, replace=False)] = True
+    mask[[0, -1]] = True
+    ref = oracle.matvec(h, X, 1.0, 0.0, None, leaf_mask=mask)
+    rows = np.concatenate([np.arange(h.leaf_ptr[i], h.leaf_ptr[i + 1]) for i in np.flatnonzero(mask)])
+    assert colmax_rel(out[:, rows], ref[:, rows]) <= TOL64
