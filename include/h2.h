@@ -118,6 +118,18 @@ int h2_set_stream(h2_handle h, void *stream);
 int h2_stats(h2_handle h, int nv, double *flops, double *bytes, double *xchg_bytes,
              int *launches);
 
+/* Phase profiling.  Phases: 0 upsweep leaves, 1 upsweep transfers,
+ * 2 exchange pack + replicated top tree, 3 coupling (diagonal), 4 coupling (off-diagonal,
+ * after the exchange wait), 5 downsweep transfers, 6 leaves (last transfer + U expansion + dense
+ * + epilogue).  h2_set_profiling(h, 1) records CUDA events on the handle's stream between phases
+ * of every following h2_matvec; h2_phase_times synchronizes, returns the mean milliseconds per
+ * phase per call since the last read (ms[0..6], ms[7] = whole call) and the call count, and
+ * resets.  h2_phase_stats returns the algorithmic bytes and flops of each phase for nv vectors
+ * (beta == 0), ms-indexed the same way (index 7 = total). */
+int h2_set_profiling(h2_handle h, int on);
+int h2_phase_times(h2_handle h, double ms[8], int64_t *ncalls);
+int h2_phase_stats(h2_handle h, int nv, double bytes[8], double flops[8]);
+
 /* Plan facts for tests: counts[0..7] = {diag coupling blocks, offdiag coupling blocks,
  * root (top-tree) coupling blocks, diag dense blocks, offdiag dense blocks, peers,
  * remote x^ nodes received, remote leaves received}. */

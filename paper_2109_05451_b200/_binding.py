@@ -15,7 +15,10 @@ H2_F64, H2_F32 = 0, 1
 H2_MEM_HOST, H2_MEM_DEVICE = 0, 1
 
 EXPORTS = ["h2_create", "h2_matvec", "h2_matvec_ld", "h2_matvec_host", "h2_set_stream", "h2_stats",
+           "h2_set_profiling", "h2_phase_times", "h2_phase_stats",
            "h2_plan_counts", "h2_destroy", "h2_nccl_unique_id", "h2_last_error", "h2_version"]
+PHASES = ["up_leaf", "up_transfer", "exchange_top", "coupling_diag", "coupling_offdiag",
+          "down_transfer", "leaf_dense"]
 
 
 class H2Error(RuntimeError):
@@ -58,6 +61,9 @@ def load_library(path=None):
         "h2_set_stream": ([vp, vp], i32),
         "h2_stats": ([vp, i32, C.POINTER(d), C.POINTER(d), C.POINTER(d), C.POINTER(i32)], i32),
         "h2_plan_counts": ([vp, C.POINTER(C.c_int64)], i32),
+        "h2_set_profiling": ([vp, i32], i32),
+        "h2_phase_times": ([vp, C.POINTER(d), C.POINTER(C.c_int64)], i32),
+        "h2_phase_stats": ([vp, i32, C.POINTER(d), C.POINTER(d)], i32),
         "h2_destroy": ([vp], i32),
         "h2_nccl_unique_id": ([vp], i32),
         "h2_last_error": ([], C.c_char_p),
@@ -184,6 +190,21 @@ class H2Operator:
         f, b, x, n = C.c_double(), C.c_double(), C.c_double(), C.c_int()
         _check(self._lib.h2_stats(self.handle, int(nv), C.byref(f), C.byref(b), C.byref(x), C.byref(n)))
         return {"flops": f.value, "bytes": b.value, "xchg_bytes": x.value, "launches": n.value}
+
+    def set_profiling(self, on=True):
+        _check(self._lib.h2_set_profiling(self.handle, 1 if on else 0))
+
+    def phase_times(self):
+        """Mean ms per phase per call since the last read (dict incl. 'total'), and the call count."""
+        ms, n = (C.c_double * 8)(), C.c_int64()
+        _check(self._lib.h2_phase_times(self.handle, ms, C.byref(n)))
+        out = dict(zip(PHASES + ["total"], list(ms)))
+        return out, n.value
+
+    def phase_stats(self, nv):
+        b, f = (C.c_double * 8)(), (C.c_double * 8)()
+        _check(self._lib.h2_phase_stats(self.handle, int(nv), b, f))
+        return dict(zip(PHASES + ["total"], list(b))), dict(zip(PHASES + ["total"], list(f)))
 
     def plan_counts(self):
         c = (C.c_int64 * 8)()

@@ -173,7 +173,7 @@ int validate(const h2_desc *d, int nv_max, Layout &L)
 struct Phase {
     int64_t t0 = 0;
     int n = 0;
-    int rpl = 1;
+    int r = 1;       // output rows of every task in the phase (engine selection)
 };
 
 }  // namespace
@@ -205,8 +205,10 @@ struct h2_ctx {
     Task *d_tasks = nullptr;
     Blk *d_blks = nullptr;
     PackSeg *d_segs = nullptr;
-    Phase up_leaf, coup_off[2], leaf;
+    Phase up_leaf, coup_off[3], leaf;
     std::vector<Phase> up_lv, top_up_lv, coup_diag, down_lv;
+    struct Stage { TreeStage st; int nctas; int r; };
+    std::vector<Stage> up_stages, top_stages, down_stages;
     std::vector<int> up_lv_level, top_up_level, down_level;
     int64_t nseg_x = 0, nseg_h = 0, seg_x0 = 0, seg_h0 = 0;
     struct Peer {
@@ -219,6 +221,20 @@ struct h2_ctx {
     ncclComm_t comm = nullptr;
     // e2e staging
     void *dX = nullptr, *dY = nullptr;
+    // per-call arguments (device CallArgs<T>) and the captured graphs, one per nv
+    void *dargs = nullptr;
+    bool use_graph = true;
+    cudaStream_t cap_stream = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool last_stream_set = false;
+    cudaGraphExec_t graph[65] = {};
+    bool warm[65] = {};
+    // profiling
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;   // 8 events per recorded call
+    int64_t ev_used = 0;
+    double ph_ops[7] = {0, 0, 0, 0, 0, 0, 0};   // operator scalars per phase
+    double ph_vec[7] = {0, 0, 0, 0, 0, 0, 0};   // vector elements per nv per phase
     // stats
     double ops_local = 0;            // stored operator scalars held by this rank
     int64_t counts[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -266,6 +282,10 @@ int release(h2_ctx *h)
     if (!h) return H2_OK;
     if (h->comm && g_nccl.loaded) g_nccl.CommDestroy(h->comm);
     for (void *p : h->owned) cudaFree(p);
+    for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+    for (auto &g : h->graph)
+        if (g) cudaGraphExecDestroy(g);
+    if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     if (h->s_comm) cudaStreamDestroy(h->s_comm);
     if (h->ev_packed) cudaEventDestroy(h->ev_packed);
     if (h->ev_recv) cudaEventDestroy(h->ev_recv);
@@ -376,6 +396,15 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_recv, cudaEventDisableTiming));
     }
 
+    // ---- per-call argument slot and the capture stream
+    {
+        cudaError_t err;
+        h->dargs = dalloc(h, sizeof(CallArgs<double>), err);
+        if (!h->dargs) H2_TRY(cuda_fail(h, err, "cudaMalloc(args)"));
+        H2_TRYC(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+        const char *g = getenv("H2_GRAPH");
+        h->use_graph = !(g && g[0] == '0');
+    }
     // ---- operator arrays on the device; V and F re-laid out as V^T, F^T (operand order)
     const int kq = k[q];
     H2_TRY(put_array(h, d->mem, d->U_leaf, nleaf * m * kq, &h->U));
@@ -398,6 +427,37 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     H2_TRY(put_array(h, d->mem, d->D, nD * m * m, &h->D));
     ops += (double)nD * m * m;
     h->ops_local = ops;
+    {
+        // per-phase operator scalars and vector elements (per vector), DESIGN.md "Measurement"
+        double Fops = 0, Eops_mid = 0, tree_up = 0, tree_mid = 0;
+        for (int l = C + 1; l <= q; ++l) { Fops += (double)L.held(l) * k[l] * k[l - 1]; tree_up += (double)L.held(l) * k[l] + (double)L.held(l - 1) * k[l - 1]; }
+        if (P > 1) for (int l = 1; l <= C; ++l) Fops += 0;   // top tree counted in phase 2 (replicated)
+        for (int l = 1; l <= q - 1; ++l) {
+            if (l <= C && P > 1) continue;
+            Eops_mid += (double)L.held(l) * k[l] * k[l - 1];
+            tree_mid += 2.0 * L.held(l) * k[l] + (double)L.held(l - 1) * k[l - 1];
+        }
+        double tree = 0;
+        for (int l = 0; l <= q; ++l) tree += (double)L.held(l) * k[l];
+        double Sd = 0, So = 0;
+        for (int l = 0; l <= q; ++l)
+            for (int64_t i = 0; i < L.held(l); ++i)
+                for (int64_t b = d->S_rowptr[l][i]; b < d->S_rowptr[l][i + 1]; ++b) {
+                    int o = L.owner(l, d->S_col[l][b]);
+                    if (o < 0 || o == p) Sd += (double)k[l] * k[l]; else So += (double)k[l] * k[l];
+                }
+        h->ph_ops[0] = (double)nleaf * m * kq;
+        h->ph_vec[0] = (double)d->n_local + (double)nleaf * kq;
+        h->ph_ops[1] = Fops;
+        h->ph_vec[1] = tree_up;
+        h->ph_ops[3] = Sd;
+        h->ph_vec[3] = 2.0 * tree;
+        h->ph_ops[4] = So;
+        h->ph_ops[5] = Eops_mid;
+        h->ph_vec[5] = tree_mid;
+        h->ph_ops[6] = (q >= 1 ? (double)nleaf * kq * k[q - 1] : 0.0) + (double)nleaf * m * kq + (double)nD * m * m;
+        h->ph_vec[6] = (double)nleaf * kq + (q >= 1 ? (double)L.held(q - 1) * k[q - 1] : 0.0) + 2.0 * d->n_local;
+    }
 
     // ---- remote needs (compressed off-diagonal node lists)
     std::map<int, std::vector<int64_t>> need_x;   // peer -> sorted unique node keys
@@ -604,7 +664,9 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     auto at = [esz](const void *base, int64_t elems) -> const void * {
         return static_cast<const char *>(base) + (size_t)elems * esz;
     };
-    auto rpl_of = [](int r) { return r > 32 ? 2 : 1; };
+    // engine class of a row count (Simt lanes-per-row / DMMA m-tiles): <=16, <=32, <=64
+    auto cls_of = [](int r) { return r <= 16 ? 0 : r <= 32 ? 1 : 2; };
+    const int cls_r[3] = {16, 32, 64};
 
     // (1) upsweep leaves: x^_s = V_s^T x_s
     h->up_leaf.t0 = tasks.size();
@@ -615,12 +677,12 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         tasks.push_back(t);
     }
     h->up_leaf.n = (int)nleaf;
-    h->up_leaf.rpl = rpl_of(kq);
+    h->up_leaf.r = kq;
     // (2) local upsweep transfers, parents at levels q-1 .. C
     for (int l = q; l >= C + 1; --l) {
         Phase ph;
         ph.t0 = tasks.size();
-        ph.rpl = rpl_of(k[l - 1]);
+        ph.r = k[l - 1];
         for (int64_t i = 0; i < L.held(l - 1); ++i) {
             Task t{h->xh_base[l - 1] + i * k[l - 1], (int64_t)blks.size(), 2, (uint8_t)k[l - 1],
                    (uint8_t)k[l], 0, 0};
@@ -637,7 +699,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         for (int l = C; l >= 1; --l) {
             Phase ph;
             ph.t0 = tasks.size();
-            ph.rpl = rpl_of(k[l - 1]);
+            ph.r = k[l - 1];
             for (int64_t i = 0; i < ((int64_t)1 << (l - 1)); ++i) {
                 Task t{h->xh_base[l - 1] + i * k[l - 1], (int64_t)blks.size(), 2, (uint8_t)k[l - 1],
                        (uint8_t)k[l], 0, 0};
@@ -654,20 +716,20 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             h->top_up_level.push_back(l);
         }
     }
-    // (4) coupling multiply, diagonal part, all levels in one launch per rpl class
+    // (4) coupling multiply, diagonal part, all levels in one launch per engine class
     //     (PAPER.md:328-331, 496); every held row gets a task (empty rows write 0)
-    std::vector<Task> offd_tasks[2];
-    std::vector<Blk> offd_blks[2];
+    std::vector<Task> offd_tasks[3];
+    std::vector<Blk> offd_blks[3];
     {
-        std::vector<Task> cls[2];
-        std::vector<std::vector<Blk>> cls_blk[2];
+        std::vector<Task> cls[3];
+        std::vector<std::vector<Blk>> cls_blk[3];
         for (int l = 0; l <= q; ++l) {
             if (l < C && !h->has_top) {
                 // top levels without couplings: y^ stays zero (workspace zeroed once), no tasks
                 continue;
             }
             const int64_t *rp = d->S_rowptr[l];
-            int ci = rpl_of(k[l]) - 1;
+            int ci = cls_of(k[l]);
             for (int64_t i = 0; i < L.held(l); ++i) {
                 std::vector<Blk> bl, offb;
                 for (int64_t b = rp[i]; b < rp[i + 1]; ++b) {
@@ -693,7 +755,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
                 }
             }
         }
-        for (int ci = 0; ci < 2; ++ci) {
+        for (int ci = 0; ci < 3; ++ci) {
             // longest rows first (better tail balance)
             std::vector<size_t> ord(cls[ci].size());
             std::iota(ord.begin(), ord.end(), 0);
@@ -702,7 +764,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             });
             Phase ph;
             ph.t0 = tasks.size();
-            ph.rpl = ci + 1;
+            ph.r = cls_r[ci];
             ph.n = (int)ord.size();
             for (size_t o : ord) {
                 Task t = cls[ci][o];
@@ -712,9 +774,9 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             }
             if (ph.n) h->coup_diag.push_back(ph);
         }
-        for (int ci = 0; ci < 2; ++ci) {
+        for (int ci = 0; ci < 3; ++ci) {
             h->coup_off[ci].t0 = tasks.size();
-            h->coup_off[ci].rpl = ci + 1;
+            h->coup_off[ci].r = cls_r[ci];
             h->coup_off[ci].n = (int)offd_tasks[ci].size();
             int64_t b0 = (int64_t)blks.size();
             for (Task t : offd_tasks[ci]) { t.blk0 += b0; tasks.push_back(t); }
@@ -727,7 +789,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         if (l <= C && !h->has_top) continue;
         Phase ph;
         ph.t0 = tasks.size();
-        ph.rpl = rpl_of(k[l]);
+        ph.r = k[l];
         for (int64_t c = 0; c < L.held(l); ++c) {
             int64_t g = L.g0(l) + c, gp = g >> 1;
             int64_t pslot = gp - L.g0(l - 1);
@@ -744,7 +806,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         const bool hasE = q >= 1 && (q > C || h->has_top);
         h->leaf.t0 = tasks.size();
         h->leaf.n = (int)nleaf;
-        h->leaf.rpl = rpl_of(m);
+        h->leaf.r = m;
         for (int64_t t = 0; t < nleaf; ++t) {
             int64_t rows = d->leaf_ptr[t + 1] - d->leaf_ptr[t];
             Task tk{d->leaf_ptr[t], (int64_t)blks.size(), 0, (uint8_t)m, (uint8_t)m, (uint8_t)rows,
@@ -771,6 +833,47 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             tasks.push_back(tk);
         }
     }
+    // ---- fused tree stages: consecutive transfer levels whose task counts halve (upsweep) or
+    //      double (downsweep) level to level run in one launch, one CTA per subtree
+    {
+        const int JMAX = 6;
+        auto group = [&](const std::vector<Phase> &ph, bool up, std::vector<h2_ctx::Stage> &out) {
+            size_t i = 0;
+            while (i < ph.size()) {
+                size_t j = i + 1;
+                while (j < ph.size() && (int)(j - i) < JMAX &&
+                       (up ? (int64_t)ph[j].n * 2 == ph[j - 1].n : (int64_t)ph[j].n == 2 * (int64_t)ph[j - 1].n))
+                    ++j;
+                h2_ctx::Stage s{};
+                s.st.nlev = (int)(j - i);
+                s.nctas = up ? ph[j - 1].n : ph[i].n;
+                s.r = 1;
+                for (size_t u = i; u < j; ++u) {
+                    s.st.t0[u - i] = ph[u].t0;
+                    s.st.per[u - i] = ph[u].n / s.nctas;
+                    s.r = std::max(s.r, ph[u].r);
+                }
+                out.push_back(s);
+                i = j;
+            }
+        };
+        group(h->up_lv, true, h->up_stages);
+        group(h->top_up_lv, true, h->top_stages);
+        group(h->down_lv, false, h->down_stages);
+    }
+    // ---- contiguity of every task's block run (TF_ACONTIG): A_b == A_0 + b r c
+    for (Task &t : tasks) {
+        const bool is_leaf = (&t - tasks.data()) >= h->leaf.t0 && (&t - tasks.data()) < h->leaf.t0 + h->leaf.n;
+        int64_t first = t.blk0 + (is_leaf ? ((t.flags & TF_HAS_E) ? 2 : 1) : 0);
+        int64_t last = t.blk0 + t.nblk;
+        if (first >= last) continue;
+        const size_t bsz = (size_t)t.r * (is_leaf ? t.r : t.c) * h->esz;
+        bool ok = true;
+        const char *a0 = static_cast<const char *>(blks[first].A);
+        for (int64_t b = first; b < last && ok; ++b)
+            ok = static_cast<const char *>(blks[b].A) == a0 + (size_t)(b - first) * bsz;
+        if (ok) t.flags |= TF_ACONTIG;
+    }
     // ---- upload the plan
     {
         cudaError_t err;
@@ -793,11 +896,11 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     for (auto &kv : need_h) hr += (int64_t)kv.second.size();
     int64_t c8[8] = {n_diag, n_off, n_root, nd_diag, nd_off, peers_n, xr, hr};
     memcpy(h->counts, c8, sizeof(c8));
-    int launches = 1 + (int)h->up_lv.size() + (int)h->coup_diag.size() + (int)h->down_lv.size() + 1;
+    int launches = 2 + (int)h->up_stages.size() + (int)h->coup_diag.size() + (int)h->down_stages.size() + 1;
     if (P > 1) {
         launches += 2;   // pack x^, pack halo
-        for (int ci = 0; ci < 2; ++ci) launches += h->coup_off[ci].n ? 1 : 0;
-        if (h->has_top) launches += (int)h->top_up_lv.size();
+        for (int ci = 0; ci < 3; ++ci) launches += h->coup_off[ci].n ? 1 : 0;
+        if (h->has_top) launches += (int)h->top_stages.size();
     }
     h->launches_per_call = launches;
     *out = h;
@@ -819,29 +922,46 @@ extern "C" int h2_create(const h2_desc *d, int nv_max, const void *nccl_unique_i
 // ======================================================================== matvec
 namespace {
 
+// phase marker: records event `i` (0..7) of the current call when profiling is on
+int mark(h2_ctx *h, int i, cudaStream_t st)
+{
+    if (!h->prof) return H2_OK;
+    int64_t idx = h->ev_used + i;
+    while ((int64_t)h->ev_pool.size() <= idx) {
+        cudaEvent_t e;
+        H2_CUDA(h, cudaEventCreate(&e));
+        h->ev_pool.push_back(e);
+    }
+    H2_CUDA(h, cudaEventRecord(h->ev_pool[idx], st));
+    return H2_OK;
+}
+
+// Enqueue one matvec for nv vectors on `st`; X, Y, alpha, beta come from the device CallArgs
+// (written by k_set_args before), so the same sequence can be captured once as a CUDA graph.
 template <typename T>
-int run_matvec(h2_ctx *h, T alpha, const T *X, int64_t ldx, T beta, T *Y, int64_t ldy, int nv)
+int enqueue(h2_ctx *h, int nv, cudaStream_t st)
 {
     const Layout &L = h->L;
     const int q = L.q, C = L.C;
-    cudaStream_t st = h->stream;
     T *xh = (T *)h->xh, *yh = (T *)h->yh;
-    if (alpha == T(0)) {
-        H2_CUDA(h, launch_scale<T>(Y, ldy, h->n_local, nv, beta, st));
-        return H2_OK;
-    }
+    const CallArgs<T> *args = (const CallArgs<T> *)h->dargs;
     auto T0 = [&](const Phase &ph) { return h->d_tasks + ph.t0; };
+    int rc;
+#define H2_MARK(i) if ((rc = mark(h, i, st)) != H2_OK) return rc
+    H2_MARK(0);
     // 1. upsweep of the local branch (PAPER.md:281 / alg:upsweep2)
-    H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, X, ldx, xh, h->xh_plane, nv,
-                                 h->up_leaf.rpl, st));
-    for (const Phase &ph : h->up_lv)
-        H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, xh, h->xh_plane,
-                                  nv, ph.rpl, st));
+    H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
+                                 h->up_leaf.r, st));
+    H2_MARK(1);
+    for (const auto &sg : h->up_stages)
+        H2_CUDA(h, launch_tree<T>(MODE_WRITE, sg.st, sg.nctas, h->d_tasks, h->d_blks, xh, h->xh_plane, nv,
+                                  sg.r, st));
+    H2_MARK(2);
     // 2. exchange (P > 1): pack my x^ nodes and x leaves that peers need, one NCCL group on the
     //    comm stream, overlapped with the diagonal multiply (alg:optimized_dist_mult)
     if (L.P > 1) {
-        H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_x0, h->nseg_x, xh, h->xh_plane, (T *)h->xsend, nv, st));
-        H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_h0, h->nseg_h, X, ldx, (T *)h->hsend, nv, st));
+        H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_x0, h->nseg_x, xh, h->xh_plane, args, (T *)h->xsend, nv, st));
+        H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_h0, h->nseg_h, (const T *)nullptr, 0, args, (T *)h->hsend, nv, st));
         H2_CUDA(h, cudaEventRecord(h->ev_packed, st));
         H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_packed, 0));
         ncclDataType_t ty = nccl_type(h->dtype);
@@ -864,33 +984,74 @@ int run_matvec(h2_ctx *h, T alpha, const T *X, int64_t ldx, T beta, T *Y, int64_
                                            kC * sizeof(T), cudaMemcpyDeviceToDevice, st));
                 H2_NCCL(h, g_nccl.AllGather(g + (int64_t)L.p * kC, g, kC, ty, h->comm, st));
             }
-            for (const Phase &ph : h->top_up_lv)
-                H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, xh,
-                                          h->xh_plane, nv, ph.rpl, st));
+            for (const auto &sg : h->top_stages)
+                H2_CUDA(h, launch_tree<T>(MODE_WRITE, sg.st, sg.nctas, h->d_tasks, h->d_blks, xh, h->xh_plane,
+                                          nv, sg.r, st));
         }
     }
+    H2_MARK(3);
     // 3. coupling multiply, diagonal part (all levels) (alg:mult)
     for (const Phase &ph : h->coup_diag)
         H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
-                                  nv, ph.rpl, st));
+                                  nv, ph.r, st));
+    H2_MARK(4);
     // 4. off-diagonal part after the exchange (waitAll, alg:optimized_dist_mult line 11-12)
     if (L.P > 1) {
         H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_recv, 0));
-        for (int ci = 0; ci < 2; ++ci) {
+        for (int ci = 0; ci < 3; ++ci) {
             const Phase &ph = h->coup_off[ci];
             H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(ph), ph.n, h->d_blks, (const T *)h->xrecv, 0, yh,
-                                      h->yh_plane, nv, ph.rpl, st));
+                                      h->yh_plane, nv, ph.r, st));
         }
     }
+    H2_MARK(5);
     // 5. downsweep transfers (alg:downsweep)
-    for (const Phase &ph : h->down_lv)
-        H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(ph), ph.n, h->d_blks, yh, h->yh_plane, yh, h->yh_plane,
-                                  nv, ph.rpl, st));
+    for (const auto &sg : h->down_stages)
+        H2_CUDA(h, launch_tree<T>(MODE_ACCUM, sg.st, sg.nctas, h->d_tasks, h->d_blks, yh, h->yh_plane, nv,
+                                  sg.r, st));
+    H2_MARK(6);
     // 6. leaves: last transfer + U expansion + dense + epilogue
     const int kq = L.k[q], kp = q >= 1 ? L.k[q - 1] : 1;
-    H2_CUDA(h, launch_leaf<T>(T0(h->leaf), h->leaf.n, h->d_blks, yh, h->yh_plane, X, ldx,
-                              (const T *)h->hrecv, 0, Y, ldy, alpha, beta, nv, kq, kp,
-                              kq > 32 ? 2 : 1, h->leaf.rpl, st));
+    H2_CUDA(h, launch_leaf<T>(T0(h->leaf), h->leaf.n, h->d_blks, yh, h->yh_plane, args,
+                              (const T *)h->hrecv, nv, kq, kp, h->leaf.r, st));
+    H2_MARK(7);
+    if (h->prof) h->ev_used += 8;
+#undef H2_MARK
+    return H2_OK;
+}
+
+template <typename T>
+int run_matvec(h2_ctx *h, T alpha, const T *X, int64_t ldx, T beta, T *Y, int64_t ldy, int nv)
+{
+    cudaStream_t st = h->stream;
+    if (h->last_stream_set && h->last_stream != st)       // the args slot is stream-ordered
+        H2_CUDA(h, cudaStreamSynchronize(h->last_stream));
+    h->last_stream = st;
+    h->last_stream_set = true;
+    if (alpha == T(0)) {
+        H2_CUDA(h, launch_scale<T>(Y, ldy, h->n_local, nv, beta, st));
+        return H2_OK;
+    }
+    H2_CUDA(h, launch_set_args<T>((CallArgs<T> *)h->dargs, X, ldx, Y, ldy, alpha, beta, st));
+    if (h->prof || !h->use_graph || !h->warm[nv]) {
+        h->warm[nv] = true;            // first call per nv runs eagerly (sets kernel attributes)
+        return enqueue<T>(h, nv, st);
+    }
+    cudaGraphExec_t &ex = h->graph[nv];
+    if (!ex) {
+        // capture the whole matvec once per nv on a private stream (PAPER.md:298's "fast static
+        // scheduler" becomes one graph launch per call)
+        cudaGraph_t g = nullptr;
+        H2_CUDA(h, cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue<T>(h, nv, h->cap_stream);
+        cudaError_t e = cudaStreamEndCapture(h->cap_stream, &g);
+        if (rc != H2_OK) { if (g) cudaGraphDestroy(g); return rc; }
+        if (e != cudaSuccess) return cuda_fail(h, e, "cudaStreamEndCapture");
+        e = cudaGraphInstantiate(&ex, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) { ex = nullptr; return cuda_fail(h, e, "cudaGraphInstantiate"); }
+    }
+    H2_CUDA(h, cudaGraphLaunch(ex, st));
     return H2_OK;
 }
 
@@ -967,6 +1128,54 @@ extern "C" int h2_stats(h2_handle h, int nv, double *flops, double *bytes, doubl
         *xchg_bytes = x;
     }
     if (launches) *launches = h->launches_per_call;
+    return H2_OK;
+}
+
+extern "C" int h2_set_profiling(h2_handle h, int on)
+{
+    if (!h) return fail(H2_ERR_ARG, "handle is NULL");
+    h->prof = on != 0;
+    return H2_OK;
+}
+
+extern "C" int h2_phase_times(h2_handle h, double ms[8], int64_t *ncalls)
+{
+    if (!h || !ms) return fail(H2_ERR_ARG, "NULL argument");
+    for (int i = 0; i < 8; ++i) ms[i] = 0;
+    int64_t calls = h->ev_used / 8;
+    if (calls) {
+        H2_CUDA(h, cudaEventSynchronize(h->ev_pool[h->ev_used - 1]));
+        for (int64_t c = 0; c < calls; ++c) {
+            cudaEvent_t *e = &h->ev_pool[c * 8];
+            for (int i = 0; i < 7; ++i) {
+                float t = 0;
+                H2_CUDA(h, cudaEventElapsedTime(&t, e[i], e[i + 1]));
+                ms[i] += t;
+            }
+            float t = 0;
+            H2_CUDA(h, cudaEventElapsedTime(&t, e[0], e[7]));
+            ms[7] += t;
+        }
+        for (int i = 0; i < 8; ++i) ms[i] /= (double)calls;
+    }
+    if (ncalls) *ncalls = calls;
+    h->ev_used = 0;
+    return H2_OK;
+}
+
+extern "C" int h2_phase_stats(h2_handle h, int nv, double bytes[8], double flops[8])
+{
+    if (!h || nv < 1) return fail(H2_ERR_ARG, "bad argument");
+    double tb = 0, tf = 0;
+    for (int i = 0; i < 7; ++i) {
+        double b = (double)h->esz * (h->ph_ops[i] + nv * h->ph_vec[i]);
+        double f = 2.0 * nv * h->ph_ops[i];
+        if (bytes) bytes[i] = b;
+        if (flops) flops[i] = f;
+        tb += b; tf += f;
+    }
+    if (bytes) bytes[7] = tb;
+    if (flops) flops[7] = tf;
     return H2_OK;
 }
 

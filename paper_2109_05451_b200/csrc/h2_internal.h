@@ -25,6 +25,11 @@ struct Blk {
     int32_t xld;
 };
 
+// Task flags
+constexpr uint8_t TF_HAS_E = 1;     // leaf kernel: first block is the parent transfer E_t
+constexpr uint8_t TF_ACONTIG = 2;   // the task's (dense, for leaves) blocks are contiguous in
+                                    // memory: A_b = A_0 + b * r * c  (streamed as one GEMM)
+
 // One warp task: an output node / leaf and its list of blocks [blk0, blk0 + nblk).
 struct Task {
     int64_t out;     // element offset of the output's first row (plane layout)
@@ -45,25 +50,51 @@ struct PackSeg {
 };
 
 // Kernel launchers (h2_kernels.cu).  T = double or float.  Each returns cudaGetLastError().
+// Per-call arguments read by the kernels from device memory, so one captured CUDA graph per nv
+// serves every call (k_set_args writes them, stream-ordered, before each graph launch).
 template <typename T>
-cudaError_t launch_up_leaf(const Task *t, int ntask, const Blk *b, const T *X, int64_t ldx,
-                           T *xh, int64_t xh_ld, int nv, int rpl, cudaStream_t s);
+struct CallArgs {
+    const T *X;
+    T *Y;
+    int64_t ldx, ldy;
+    T alpha, beta;
+};
+
+template <typename T>
+cudaError_t launch_set_args(CallArgs<T> *a, const T *X, int64_t ldx, T *Y, int64_t ldy, T alpha, T beta,
+                            cudaStream_t s);
+// r = output rows of the phase's tasks (selects lanes-per-row / DMMA m-tiles)
+template <typename T>
+cudaError_t launch_up_leaf(const Task *t, int ntask, const Blk *b, const CallArgs<T> *args,
+                           T *xh, int64_t xh_ld, int nv, int r, cudaStream_t s);
 template <typename T>
 cudaError_t launch_rows(int mode, const Task *t, int ntask, const Blk *b, const T *src,
-                        int64_t src_ld, T *dst, int64_t dst_ld, int nv, int rpl, cudaStream_t s);
+                        int64_t src_ld, T *dst, int64_t dst_ld, int nv, int r, cudaStream_t s);
 template <typename T>
 cudaError_t launch_leaf(const Task *t, int ntask, const Blk *b, const T *yh, int64_t yh_ld,
-                        const T *X, int64_t ldx, const T *halo, int64_t halo_ld, T *Y,
-                        int64_t ldy, T alpha, T beta, int nv, int k, int kp, int rplk, int rplm,
+                        const CallArgs<T> *args, const T *halo, int nv, int k, int kp, int m,
                         cudaStream_t s);
 template <typename T>
 cudaError_t launch_scale(T *Y, int64_t ldy, int64_t n, int nv, T beta, cudaStream_t s);
 template <typename T>
 cudaError_t launch_transpose(const T *src, T *dst, int64_t batch, int r, int c, cudaStream_t s);
+// src == nullptr: read the caller's X from args (halo pack)
 template <typename T>
-cudaError_t launch_pack(const PackSeg *segs, int64_t nseg, const T *src, int64_t src_ld, T *dst,
-                        int nv, cudaStream_t s);
+cudaError_t launch_pack(const PackSeg *segs, int64_t nseg, const T *src, int64_t src_ld,
+                        const CallArgs<T> *args, T *dst, int nv, cudaStream_t s);
 
 enum { MODE_WRITE = 0, MODE_ACCUM = 1 };
+
+// A fused run of consecutive tree levels (see k_tree): per level, the first task of the phase
+// and the number of tasks each CTA owns.
+constexpr int TREE_MAXLEV = 8;
+struct TreeStage {
+    int64_t t0[TREE_MAXLEV];
+    int32_t per[TREE_MAXLEV];
+    int32_t nlev;
+};
+template <typename T>
+cudaError_t launch_tree(int mode, const TreeStage &st, int nctas, const Task *t, const Blk *b, T *buf,
+                        int64_t ld, int nv, int r, cudaStream_t s);
 
 }  // namespace h2

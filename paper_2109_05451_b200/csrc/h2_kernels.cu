@@ -3,9 +3,16 @@
 // Every phase is a set of warp tasks over a static plan built once by h2_create (the paper's
 // per-level marshaling, done at setup instead of per call).  A task owns one
 // output node (row-owner computes: no atomics, no conflict batches) and
-// accumulates   y_rows (r x nv) += sum_b A_b (r x c) x_b (c x nv)   with lanes <-> output rows
-// (RPL rows per lane), A streamed once from HBM with coalesced column loads (evict-first),
-// and the x operand staged per block in warp-private shared memory (broadcast reads).
+// accumulates   y (r x nv) += sum_b A_b (r x c) x_b (c x nv),   A_b streamed once from HBM.
+//
+// Two warp engines compute the block products:
+//   Simt  (any T, nv chunks of 1..16): lanes <-> output rows (RPL rows per lane); each A column
+//         is one coalesced warp load (evict-first); the x operand is held distributed in
+//         registers (lane j holds rows j, j+32) and broadcast with shuffles.
+//   Mma   (double, nv chunks of 8 / 16): FP64 tensor-core tiles mma.sync.m8n8k4.f64 (SASS DMMA);
+//         A fragments straight from global memory (each element loaded once), B fragments from
+//         the x^ / X source (L2) or from shared memory, accumulators in registers across all
+//         blocks of the task.
 //
 //   up_leaf   x^_s = V_s^T x_s                         PAPER.md:239, 262 (alg:upsweep2 line 3)
 //   rows/W    x^_p = F_{c1}^T x^_{c1} + F_{c2}^T x^_{c2} PAPER.md:241-253, 267-268
@@ -17,102 +24,351 @@
 
 namespace h2 {
 
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int XCAP_BYTES = 4096;   // per-warp staging of the stacked x in the Simt stream
+constexpr int ZLD = KMAX + 4;   // smem leading dimension of the z hand-over (2 wavefronts per
+                                // DMMA B-fragment load: no extra bank conflicts)
+
 template <typename T>
 __device__ __forceinline__ T ld_stream(const T *p) { return __ldcs(p); }
 
-// x operand (c x NVB) of one block into warp smem xs[n * XLD + j]; rows >= xrows and vectors
-// >= nvc are zero (ragged leaves / partial vector chunk).
+// =========================================================================== Simt engine
+template <typename T, int RPL, int NVB>
+struct SimtAcc {
+    T v[RPL][NVB];
+    template <typename F>
+    __device__ __forceinline__ void each(int lane, F f) {
+#pragma unroll
+        for (int ri = 0; ri < RPL; ++ri)
+#pragma unroll
+            for (int n = 0; n < NVB; ++n) f(lane + 32 * ri, n, v[ri][n]);
+    }
+};
+
+// x operand rows lane / lane+32 of vectors [0, nvc); rows >= xrows -> 0
 template <typename T, int NVB>
-__device__ __forceinline__ void stage_x(T *xs, const T *__restrict__ src, int64_t ld, int xrows,
-                                        int c, int nvc, int lane)
+__device__ __forceinline__ void simt_load_x(T (&x0)[NVB], T (&x1)[NVB], const T *__restrict__ src,
+                                            int64_t ld, int xrows, int nvc, int lane)
 {
 #pragma unroll
     for (int n = 0; n < NVB; ++n) {
-        for (int j = lane; j < c; j += 32)
-            xs[n * XLD + j] = (n < nvc && j < xrows) ? src[j + n * ld] : T(0);
+        x0[n] = (n < nvc && lane < xrows) ? src[lane + n * ld] : T(0);
+        x1[n] = (n < nvc && lane + 32 < xrows) ? src[lane + 32 + n * ld] : T(0);
     }
 }
 
-// acc[ri][n] += sum_j A[(j) * r + lane + 32 ri] * xs[n * XLD + j]
-template <typename T, int RPL, int NVB>
-__device__ __forceinline__ void acc_block(T (&acc)[RPL][NVB], const T *__restrict__ A, int r,
-                                          int c, const T *xs, int lane)
+template <typename T, int RPL, int NVB, int U>
+__device__ __forceinline__ void simt_cols(SimtAcc<T, RPL, NVB> &acc, const T *__restrict__ A, int r,
+                                          int j, const T (&x0)[NVB], const T (&x1)[NVB], int lane)
 {
-    int j = 0;
-    for (; j + 8 <= c; j += 8) {
-        T a[8][RPL];
+    T a[U][RPL];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-#pragma unroll
-            for (int ri = 0; ri < RPL; ++ri) {
-                int i = lane + 32 * ri;
-                a[u][ri] = (i < r) ? ld_stream(A + (int64_t)(j + u) * r + i) : T(0);
-            }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-#pragma unroll
-            for (int n = 0; n < NVB; ++n) {
-                T xv = xs[n * XLD + j + u];
-#pragma unroll
-                for (int ri = 0; ri < RPL; ++ri) acc[ri][n] = fma(a[u][ri], xv, acc[ri][n]);
-            }
-    }
-    for (; j < c; ++j) {
-        T a[RPL];
+    for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int ri = 0; ri < RPL; ++ri) {
             int i = lane + 32 * ri;
-            a[ri] = (i < r) ? ld_stream(A + (int64_t)j * r + i) : T(0);
+            a[u][ri] = (i < r) ? ld_stream(A + (int64_t)(j + u) * r + i) : T(0);
         }
 #pragma unroll
-        for (int n = 0; n < NVB; ++n) {
-            T xv = xs[n * XLD + j];
+    for (int u = 0; u < U; ++u) {
+        const int jj = j + u;                       // warp-uniform
 #pragma unroll
-            for (int ri = 0; ri < RPL; ++ri) acc[ri][n] = fma(a[ri], xv, acc[ri][n]);
+        for (int n = 0; n < NVB; ++n) {
+            T xv = __shfl_sync(FULL, jj < 32 ? x0[n] : x1[n], jj & 31);
+#pragma unroll
+            for (int ri = 0; ri < RPL; ++ri) acc.v[ri][n] = fma(a[u][ri], xv, acc.v[ri][n]);
         }
     }
 }
 
+// acc += A (r x c, col-major) * x (c x nvc) with x in registers (x0/x1)
 template <typename T, int RPL, int NVB>
-__device__ __forceinline__ void zero_acc(T (&acc)[RPL][NVB])
+__device__ __forceinline__ void simt_block_regs(SimtAcc<T, RPL, NVB> &acc, const T *__restrict__ A,
+                                                int r, int c, const T (&x0)[NVB], const T (&x1)[NVB],
+                                                int lane)
 {
-#pragma unroll
-    for (int ri = 0; ri < RPL; ++ri)
-#pragma unroll
-        for (int n = 0; n < NVB; ++n) acc[ri][n] = T(0);
+    int j = 0;
+    for (; j + 16 <= c; j += 16) simt_cols<T, RPL, NVB, 16>(acc, A, r, j, x0, x1, lane);
+    if (j + 8 <= c) { simt_cols<T, RPL, NVB, 8>(acc, A, r, j, x0, x1, lane); j += 8; }
+    if (j + 4 <= c) { simt_cols<T, RPL, NVB, 4>(acc, A, r, j, x0, x1, lane); j += 4; }
+    for (; j < c; ++j) simt_cols<T, RPL, NVB, 1>(acc, A, r, j, x0, x1, lane);
 }
+
+template <typename T, int RPL, int NVB>
+__device__ __forceinline__ void simt_block(SimtAcc<T, RPL, NVB> &acc, const T *__restrict__ A, int r,
+                                           int c, const T *__restrict__ src, int64_t ld, int xrows,
+                                           int nvc, int lane)
+{
+    T x0[NVB], x1[NVB];
+    simt_load_x<T, NVB>(x0, x1, src, ld, xrows, nvc, lane);
+    simt_block_regs<T, RPL, NVB>(acc, A, r, c, x0, x1, lane);
+}
+
+// =========================================================================== Mma engine
+template <int MT, int NT>
+struct MmaAcc {
+    double v[MT][NT][2];
+    template <typename F>
+    __device__ __forceinline__ void each(int lane, F f) {
+        const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) f(mt * 8 + g, nt * 8 + 2 * t + i, v[mt][nt][i]);
+    }
+};
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+// acc += A (r x c, col-major, global) * B (c x nvc; element (j, n) at src[j + n*ld], global or
+// shared).  Fragments (PTX m8n8k4 .f64): A row = 8mt + lane/4, col = 4ks + lane%4;
+// B row = 4ks + lane%4, col = 8nt + lane/4; rows >= xrows / cols >= nvc read as 0.
+template <int MT, int NT, bool A_STREAM>
+__device__ __forceinline__ void mma_block(MmaAcc<MT, NT> &acc, const double *__restrict__ A, int r,
+                                          int c, const double *src, int64_t ld, int xrows, int nvc,
+                                          int lane)
+{
+    const int g = lane >> 2, t = lane & 3;
+    const int ksn = (c + 3) >> 2;
+#pragma unroll 2
+    for (int ks = 0; ks < ksn; ++ks) {
+        const int col = ks * 4 + t;
+        double a[MT], b[NT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            const int row = mt * 8 + g;
+            const double *p = A + (int64_t)col * r + row;
+            a[mt] = (row < r && col < c) ? (A_STREAM ? ld_stream(p) : *p) : 0.0;
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const int n = nt * 8 + g;
+            b[nt] = (col < xrows && n < nvc) ? src[col + n * ld] : 0.0;
+        }
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a[mt], b[nt]);
+    }
+}
+
+// =========================================================================== streaming rows
+// A task whose blocks A_b are CONTIGUOUS (flag TF_ACONTIG: A_b = A_0 + b r c, e.g. the CSR run
+// of a coupling row, the dense row of a leaf, the two child transfers of a parent) is one
+// GEMM  y (r x nv) += [A_1 .. A_n] (r x n c) [x_1; ..; x_n] (n c x nv):  its A columns are
+// streamed back to back with no per-block dependent descriptor loads, and the stacked x is
+// gathered per block from its own source (x^ slots, X leaf rows or the halo buffer).
+template <typename T>
+struct Src {
+    const T *pos;     // x >= 0: pos + x, leading dimension pos_ld (or the block's xld)
+    int64_t pos_ld;
+    const T *neg;     // x < 0: neg + (-x - 1), leading dimension xld (halo buffer)
+    int n0;           // first vector of the current chunk
+};
+
+template <typename T>
+__device__ __forceinline__ const T *resolve(const Src<T> &s, int64_t x, int32_t xld, int64_t &ld)
+{
+    if (x >= 0) { ld = xld ? (int64_t)xld : s.pos_ld; return s.pos + x + s.n0 * ld; }
+    ld = xld;
+    return s.neg + (-x - 1) + s.n0 * ld;
+}
+
+// acc += A (r x K, col-major, contiguous) * xs (K x nvc in shared memory, ld xld)
+template <typename T, int RPL, int NVB, int U>
+__device__ __forceinline__ void simt_cols_smem(SimtAcc<T, RPL, NVB> &acc, const T *__restrict__ A,
+                                               int r, int j, const T *xs, int xld, int lane)
+{
+    T a[U][RPL];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int ri = 0; ri < RPL; ++ri) {
+            int i = lane + 32 * ri;
+            a[u][ri] = (i < r) ? ld_stream(A + (int64_t)(j + u) * r + i) : T(0);
+        }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int n = 0; n < NVB; ++n) {
+            T xv = xs[j + u + n * xld];
+#pragma unroll
+            for (int ri = 0; ri < RPL; ++ri) acc.v[ri][n] = fma(a[u][ri], xv, acc.v[ri][n]);
+        }
+}
+
+template <typename T, int RPL, int NVB>
+__device__ __forceinline__ void simt_stream(SimtAcc<T, RPL, NVB> &acc, const T *__restrict__ A0, int r,
+                                            int c, int nblk, const Blk *__restrict__ blks,
+                                            const Src<T> &src, int nvc, int lane, T *xs, int xcap)
+{
+    int per = xcap / (c * NVB);
+    per = per < 1 ? 1 : (per > 32 ? 32 : per);
+    for (int b0 = 0; b0 < nblk; b0 += per) {
+        const int nb = min(per, nblk - b0);
+        const int K = nb * c;
+        int64_t xo = 0;
+        int xr = 0, xl = 0;
+        if (lane < nb) {
+            const Blk b = blks[b0 + lane];
+            xo = b.x; xr = b.xrows; xl = b.xld;
+        }
+        __syncwarp();
+        for (int e0 = 0; e0 < K; e0 += 32) {           // gather the stacked x of the chunk
+            const int e = e0 + lane;
+            const int bb = min(e / c, nb - 1), j = e - bb * c;
+            const int64_t bxo = __shfl_sync(FULL, xo, bb);
+            const int bxr = __shfl_sync(FULL, xr, bb), bxl = __shfl_sync(FULL, xl, bb);
+            if (e < K) {
+                int64_t ld;
+                const T *p = resolve(src, bxo, bxl, ld);
+#pragma unroll
+                for (int n = 0; n < NVB; ++n) xs[e + n * K] = (j < bxr && n < nvc) ? p[j + n * ld] : T(0);
+            }
+        }
+        __syncwarp();
+        const T *A = A0 + (int64_t)b0 * r * c;
+        int j = 0;
+        for (; j + 16 <= K; j += 16) simt_cols_smem<T, RPL, NVB, 16>(acc, A, r, j, xs, K, lane);
+        if (j + 8 <= K) { simt_cols_smem<T, RPL, NVB, 8>(acc, A, r, j, xs, K, lane); j += 8; }
+        if (j + 4 <= K) { simt_cols_smem<T, RPL, NVB, 4>(acc, A, r, j, xs, K, lane); j += 4; }
+        for (; j < K; ++j) simt_cols_smem<T, RPL, NVB, 1>(acc, A, r, j, xs, K, lane);
+        __syncwarp();
+    }
+}
+
+struct MmaDesc {
+    const double *p;
+    int64_t ld;
+    int32_t xrows;
+    int32_t pad;
+};
+
+template <int MT, int NT>
+__device__ __forceinline__ void mma_stream(MmaAcc<MT, NT> &acc, const double *__restrict__ A0, int r,
+                                           int c, int nblk, const Blk *__restrict__ blks,
+                                           const Src<double> &src, int nvc, int lane, MmaDesc *ds)
+{
+    const int g = lane >> 2, t = lane & 3;
+    for (int b0 = 0; b0 < nblk; b0 += 32) {
+        const int nb = min(32, nblk - b0);
+        const int K = nb * c;
+        __syncwarp();
+        if (lane < nb) {
+            const Blk b = blks[b0 + lane];
+            int64_t ld;
+            const double *p = resolve(src, b.x, b.xld, ld);
+            ds[lane] = MmaDesc{p, ld, b.xrows, 0};
+        }
+        __syncwarp();
+        const double *A = A0 + (int64_t)b0 * r * c;
+        int bb = 0, j = t;
+        while (j >= c) { j -= c; ++bb; }
+        MmaDesc d = ds[min(bb, nb - 1)];
+        const int ksn = (K + 3) >> 2;
+#pragma unroll 2
+        for (int ks = 0; ks < ksn; ++ks) {
+            const int col = ks * 4 + t;
+            double a[MT], b[NT];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                const int row = mt * 8 + g;
+                a[mt] = (row < r && col < K) ? ld_stream(A + (int64_t)col * r + row) : 0.0;
+            }
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                const int n = nt * 8 + g;
+                b[nt] = (col < K && j < d.xrows && n < nvc) ? d.p[j + n * d.ld] : 0.0;
+            }
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a[mt], b[nt]);
+            j += 4;
+            if (j >= c) {
+                do { j -= c; ++bb; } while (j >= c);
+                d = ds[min(bb, nb - 1)];
+            }
+        }
+    }
+}
+
+// =========================================================================== common helpers
+template <typename Acc>
+__device__ __forceinline__ void acc_zero(Acc &acc, int lane)
+{
+    acc.each(lane, [](int, int, auto &v) { v = 0; });
+}
+
+template <typename Acc, typename T>
+__device__ __forceinline__ void acc_load(Acc &acc, const T *base, int64_t ld, int r, int nvc, int lane)
+{
+    acc.each(lane, [&](int row, int n, auto &v) { v = (row < r && n < nvc) ? base[row + n * ld] : T(0); });
+}
+
+template <typename Acc, typename T>
+__device__ __forceinline__ void acc_store(Acc &acc, T *base, int64_t ld, int r, int nvc, int lane)
+{
+    acc.each(lane, [&](int row, int n, auto &v) {
+        if (row < r && n < nvc) base[row + n * ld] = v;
+    });
+}
+
+// Engine selector: Simt<T, RPL, NVB> or Mma<MT, NT> behind one interface
+template <typename T, int RPL, int NVB>
+struct Simt {
+    using Acc = SimtAcc<T, RPL, NVB>;
+    static constexpr int NV = NVB;
+    static constexpr int SCRATCH = XCAP_BYTES;      // per-warp smem for the stream staging
+    __device__ static void block(Acc &acc, const T *A, int r, int c, const T *src, int64_t ld, int xrows,
+                                 int nvc, int lane)
+    { simt_block<T, RPL, NVB>(acc, A, r, c, src, ld, xrows, nvc, lane); }
+    __device__ static void stream(Acc &acc, const T *A0, int r, int c, int nblk, const Blk *blks,
+                                  const Src<T> &src, int nvc, int lane, void *scratch)
+    { simt_stream<T, RPL, NVB>(acc, A0, r, c, nblk, blks, src, nvc, lane, (T *)scratch, XCAP_BYTES / (int)sizeof(T)); }
+};
+
+template <int MT, int NT>
+struct Mma {
+    using Acc = MmaAcc<MT, NT>;
+    static constexpr int NV = 8 * NT;
+    static constexpr int SCRATCH = 32 * sizeof(MmaDesc);
+    __device__ static void block(Acc &acc, const double *A, int r, int c, const double *src, int64_t ld,
+                                 int xrows, int nvc, int lane)
+    { mma_block<MT, NT, true>(acc, A, r, c, src, ld, xrows, nvc, lane); }
+    __device__ static void stream(Acc &acc, const double *A0, int r, int c, int nblk, const Blk *blks,
+                                  const Src<double> &src, int nvc, int lane, void *scratch)
+    { mma_stream<MT, NT>(acc, A0, r, c, nblk, blks, src, nvc, lane, (MmaDesc *)scratch); }
+};
 
 // ---------------------------------------------------------------------------------------
 // Upsweep leaves: x^_s (k x nv) = Vt_s (k x m) x_s (m x nv), Vt = V^T re-laid out at create.
-template <typename T, int RPL, int NVB>
-__global__ void __launch_bounds__(WPB * 32)
+template <typename T, typename Eng>
+__global__ void __launch_bounds__(WPB * 32, 2)
 k_up_leaf(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
-          const T *__restrict__ X, int64_t ldx, T *__restrict__ xh, int64_t xh_ld, int nv)
+          const CallArgs<T> *__restrict__ args, T *__restrict__ xh, int64_t xh_ld, int nv)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int task = blockIdx.x * WPB + wid;
+    const int lane = threadIdx.x & 31;
+    const int task = blockIdx.x * WPB + (threadIdx.x >> 5);
     if (task >= ntask) return;
-    T *xs = reinterpret_cast<T *>(smem_raw) + wid * NVB * XLD;
+    const T *__restrict__ X = args->X;
+    const int64_t ldx = args->ldx;
     const Task tk = tasks[task];
     const Blk b = blks[tk.blk0];
-    const T *A = static_cast<const T *>(b.A);
-    for (int n0 = 0; n0 < nv; n0 += NVB) {
-        const int nvc = min(NVB, nv - n0);
-        T acc[RPL][NVB];
-        zero_acc(acc);
-        __syncwarp();
-        stage_x<T, NVB>(xs, X + b.x + n0 * ldx, ldx, b.xrows, tk.c, nvc, lane);
-        __syncwarp();
-        acc_block<T, RPL, NVB>(acc, A, tk.r, tk.c, xs, lane);
-#pragma unroll
-        for (int ri = 0; ri < RPL; ++ri) {
-            int i = lane + 32 * ri;
-            if (i < tk.r)
-#pragma unroll
-                for (int n = 0; n < NVB; ++n)
-                    if (n < nvc) xh[tk.out + i + (int64_t)(n0 + n) * xh_ld] = acc[ri][n];
-        }
+    for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
+        const int nvc = min(Eng::NV, nv - n0);
+        typename Eng::Acc acc;
+        acc_zero(acc, lane);
+        Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.c, X + b.x + (int64_t)n0 * ldx, ldx,
+                   b.xrows, nvc, lane);
+        acc_store(acc, xh + tk.out + (int64_t)n0 * xh_ld, xh_ld, tk.r, nvc, lane);
     }
 }
 
@@ -120,8 +376,8 @@ k_up_leaf(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blk
 // Generic row tasks whose x operands and output live in the x^/y^ workspaces:
 //   MODE_WRITE  out  = sum_b A_b x_b    (upsweep transfers, coupling multiply)
 //   MODE_ACCUM  out += sum_b A_b x_b    (downsweep transfers, off-diagonal coupling pass)
-template <typename T, int RPL, int NVB, int MODE>
-__global__ void __launch_bounds__(WPB * 32)
+template <typename T, typename Eng, int MODE>
+__global__ void __launch_bounds__(WPB * 32, 2)
 k_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
        const T *__restrict__ src, int64_t src_ld, T *__restrict__ dst, int64_t dst_ld, int nv)
 {
@@ -129,117 +385,148 @@ k_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int task = blockIdx.x * WPB + wid;
     if (task >= ntask) return;
-    T *xs = reinterpret_cast<T *>(smem_raw) + wid * NVB * XLD;
+    void *scratch = smem_raw + wid * Eng::SCRATCH;
     const Task tk = tasks[task];
-    for (int n0 = 0; n0 < nv; n0 += NVB) {
-        const int nvc = min(NVB, nv - n0);
-        T acc[RPL][NVB];
-        if (MODE == MODE_ACCUM) {
-#pragma unroll
-            for (int ri = 0; ri < RPL; ++ri) {
-                int i = lane + 32 * ri;
-#pragma unroll
-                for (int n = 0; n < NVB; ++n)
-                    acc[ri][n] = (i < tk.r && n < nvc)
-                                     ? dst[tk.out + i + (int64_t)(n0 + n) * dst_ld] : T(0);
-            }
-        } else {
-            zero_acc(acc);
+    for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
+        const int nvc = min(Eng::NV, nv - n0);
+        typename Eng::Acc acc;
+        if (MODE == MODE_ACCUM) acc_load(acc, dst + tk.out + (int64_t)n0 * dst_ld, dst_ld, tk.r, nvc, lane);
+        else acc_zero(acc, lane);
+        if ((tk.flags & TF_ACONTIG) && tk.nblk > 0) {
+            const Blk b0 = blks[tk.blk0];
+            const Src<T> sr{src, src_ld, nullptr, n0};
+            Eng::stream(acc, static_cast<const T *>(b0.A), tk.r, tk.c, tk.nblk, blks + tk.blk0, sr, nvc,
+                        lane, scratch);
+            acc_store(acc, dst + tk.out + (int64_t)n0 * dst_ld, dst_ld, tk.r, nvc, lane);
+            continue;
         }
         for (int bi = 0; bi < tk.nblk; ++bi) {
             const Blk b = blks[tk.blk0 + bi];
             const int64_t ld = b.xld ? (int64_t)b.xld : src_ld;
-            __syncwarp();
-            stage_x<T, NVB>(xs, src + b.x + (int64_t)n0 * ld, ld, b.xrows, tk.c, nvc, lane);
-            __syncwarp();
-            acc_block<T, RPL, NVB>(acc, static_cast<const T *>(b.A), tk.r, tk.c, xs, lane);
+            Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.c, src + b.x + (int64_t)n0 * ld, ld,
+                       b.xrows, nvc, lane);
         }
-#pragma unroll
-        for (int ri = 0; ri < RPL; ++ri) {
-            int i = lane + 32 * ri;
-            if (i < tk.r)
-#pragma unroll
-                for (int n = 0; n < NVB; ++n)
-                    if (n < nvc) dst[tk.out + i + (int64_t)(n0 + n) * dst_ld] = acc[ri][n];
+        acc_store(acc, dst + tk.out + (int64_t)n0 * dst_ld, dst_ld, tk.r, nvc, lane);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Fused tree stage: one CTA owns a subtree and runs `nlev` consecutive transfer levels of it,
+// level by level, with a CTA barrier between levels (the upsweep levels q-1 .. 0 or the
+// downsweep levels 1 .. q-1 in a few launches instead of one launch per level, PAPER.md:263,
+// 408).  Level i's tasks of CTA c are [t0[i] + c * per[i], t0[i] + (c + 1) * per[i]).
+template <typename T, typename Eng, int MODE>
+__global__ void __launch_bounds__(WPB * 32, 2)
+k_tree(TreeStage st, const Task *__restrict__ tasks, const Blk *__restrict__ blks, T *__restrict__ buf,
+       int64_t ld, int nv)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    void *scratch = smem_raw + wid * Eng::SCRATCH;
+    for (int lv = 0; lv < st.nlev; ++lv) {
+        const int per = st.per[lv];
+        const int64_t base = st.t0[lv] + (int64_t)blockIdx.x * per;
+        for (int ti = wid; ti < per; ti += WPB) {
+            const Task tk = tasks[base + ti];
+            for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
+                const int nvc = min(Eng::NV, nv - n0);
+                typename Eng::Acc acc;
+                if (MODE == MODE_ACCUM) acc_load(acc, buf + tk.out + (int64_t)n0 * ld, ld, tk.r, nvc, lane);
+                else acc_zero(acc, lane);
+                if (tk.flags & TF_ACONTIG) {
+                    const Src<T> sr{buf, ld, nullptr, n0};
+                    Eng::stream(acc, static_cast<const T *>(blks[tk.blk0].A), tk.r, tk.c, tk.nblk,
+                                blks + tk.blk0, sr, nvc, lane, scratch);
+                } else {
+                    for (int bi = 0; bi < tk.nblk; ++bi) {
+                        const Blk b = blks[tk.blk0 + bi];
+                        Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.c, buf + b.x + (int64_t)n0 * ld,
+                                   ld, b.xrows, nvc, lane);
+                    }
+                }
+                acc_store(acc, buf + tk.out + (int64_t)n0 * ld, ld, tk.r, nvc, lane);
+            }
         }
+        __syncthreads();   // level lv complete (global writes visible to the CTA) before lv + 1
     }
 }
 
 // ---------------------------------------------------------------------------------------
 // Leaf kernel: last downsweep transfer + leaf expansion + dense near field + epilogue.
 // blocks: [E_t (if flags&1), x = parent y^ offset] [U_t, x = own y^ offset] [D_ts ...]
-template <typename T, int RPLK, int RPLM, int NVB>
-__global__ void __launch_bounds__(WPB * 32)
+// EngK computes z (rows k), EngM the leaf rows (m); z is handed over through warp smem.
+template <typename T, typename EngK, typename EngM>
+__global__ void __launch_bounds__(WPB * 32, 2)
 k_leaf(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
-       const T *__restrict__ yh, int64_t yh_ld, const T *__restrict__ X, int64_t ldx,
-       const T *__restrict__ halo, int64_t halo_ld, T *__restrict__ Y, int64_t ldy, T alpha,
-       T beta, int nv, int k, int kp)
+       const T *__restrict__ yh, int64_t yh_ld, const CallArgs<T> *__restrict__ args,
+       const T *__restrict__ halo, int nv, int k, int kp)
 {
+    const T *__restrict__ X = args->X;
+    T *__restrict__ Y = args->Y;
+    const int64_t ldx = args->ldx, ldy = args->ldy;
+    const T alpha = args->alpha, beta = args->beta;
+    static_assert(EngK::NV == EngM::NV, "engines must agree on the vector chunk");
+    constexpr int NV = EngM::NV;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int task = blockIdx.x * WPB + wid;
     if (task >= ntask) return;
-    T *xs = reinterpret_cast<T *>(smem_raw) + wid * NVB * XLD;
+    T *zs = reinterpret_cast<T *>(smem_raw) + wid * NV * ZLD;
+    void *scratch = smem_raw + (size_t)WPB * NV * ZLD * sizeof(T) + wid * EngM::SCRATCH;
     const Task tk = tasks[task];
     const bool hasE = tk.flags & 1;
     const Blk bU = blks[tk.blk0 + (hasE ? 1 : 0)];
-    for (int n0 = 0; n0 < nv; n0 += NVB) {
-        const int nvc = min(NVB, nv - n0);
-        // z_t = y^_t + E_t y^_parent   (lanes <-> rank rows)
-        T z[RPLK][NVB];
-#pragma unroll
-        for (int ri = 0; ri < RPLK; ++ri) {
-            int i = lane + 32 * ri;
-#pragma unroll
-            for (int n = 0; n < NVB; ++n)
-                z[ri][n] = (i < k && n < nvc) ? yh[bU.x + i + (int64_t)(n0 + n) * yh_ld] : T(0);
-        }
+    for (int n0 = 0; n0 < nv; n0 += NV) {
+        const int nvc = min(NV, nv - n0);
+        // z_t = y^_t + E_t y^_parent
+        typename EngK::Acc z;
+        acc_load(z, yh + bU.x + (int64_t)n0 * yh_ld, yh_ld, k, nvc, lane);
         if (hasE) {
             const Blk bE = blks[tk.blk0];
-            __syncwarp();
-            stage_x<T, NVB>(xs, yh + bE.x + (int64_t)n0 * yh_ld, yh_ld, bE.xrows, kp, nvc, lane);
-            __syncwarp();
-            acc_block<T, RPLK, NVB>(z, static_cast<const T *>(bE.A), k, kp, xs, lane);
+            EngK::block(z, static_cast<const T *>(bE.A), k, kp, yh + bE.x + (int64_t)n0 * yh_ld, yh_ld,
+                        bE.xrows, nvc, lane);
         }
         __syncwarp();
-#pragma unroll
-        for (int ri = 0; ri < RPLK; ++ri) {
-            int i = lane + 32 * ri;
-            if (i < k)
-#pragma unroll
-                for (int n = 0; n < NVB; ++n) xs[n * XLD + i] = z[ri][n];
-        }
+        acc_store(z, zs, (int64_t)ZLD, k, nvc, lane);
         __syncwarp();
-        // y_t = U_t z_t  (lanes <-> leaf rows)
-        T acc[RPLM][NVB];
-        zero_acc(acc);
-        acc_block<T, RPLM, NVB>(acc, static_cast<const T *>(bU.A), tk.r, k, xs, lane);
+        // y_t = U_t z_t
+        typename EngM::Acc acc;
+        acc_zero(acc, lane);
+        EngM::block(acc, static_cast<const T *>(bU.A), tk.r, k, zs, (int64_t)ZLD, k, nvc, lane);
         // dense near field y_t += sum_s D_ts x_s
-        const int64_t d0 = tk.blk0 + (hasE ? 2 : 1), d1 = tk.blk0 + tk.nblk;
-        for (int64_t bi = d0; bi < d1; ++bi) {
-            const Blk b = blks[bi];
+        const int dfirst = hasE ? 2 : 1;
+        if ((tk.flags & TF_ACONTIG) && tk.nblk > dfirst) {
+            const Blk b0 = blks[tk.blk0 + dfirst];
+            const Src<T> sr{X, ldx, halo, n0};
+            EngM::stream(acc, static_cast<const T *>(b0.A), tk.r, tk.r, tk.nblk - dfirst,
+                         blks + tk.blk0 + dfirst, sr, nvc, lane, scratch);
+        } else
+        for (int bi = dfirst; bi < tk.nblk; ++bi) {
+            const Blk b = blks[tk.blk0 + bi];
             const T *src;
             int64_t ld;
             if (b.x >= 0) { src = X + b.x; ld = ldx; }
-            else          { src = halo + (-b.x - 1); ld = b.xld ? (int64_t)b.xld : halo_ld; }
-            __syncwarp();
-            stage_x<T, NVB>(xs, src + (int64_t)n0 * ld, ld, b.xrows, tk.r, nvc, lane);
-            __syncwarp();
-            acc_block<T, RPLM, NVB>(acc, static_cast<const T *>(b.A), tk.r, tk.r, xs, lane);
+            else          { src = halo + (-b.x - 1); ld = b.xld; }
+            EngM::block(acc, static_cast<const T *>(b.A), tk.r, tk.r, src + (int64_t)n0 * ld, ld,
+                        b.xrows, nvc, lane);
         }
         // epilogue Y = alpha y + beta Y (beta == 0: Y not read)
-#pragma unroll
-        for (int ri = 0; ri < RPLM; ++ri) {
-            int i = lane + 32 * ri;
-            if (i < tk.rows)
-#pragma unroll
-                for (int n = 0; n < NVB; ++n)
-                    if (n < nvc) {
-                        T *p = Y + tk.out + i + (int64_t)(n0 + n) * ldy;
-                        *p = (beta == T(0)) ? alpha * acc[ri][n] : fma(alpha, acc[ri][n], beta * *p);
-                    }
-        }
+        T *Yb = Y + tk.out + (int64_t)n0 * ldy;
+        const int rows = tk.rows;
+        acc.each(lane, [&](int row, int n, auto &v) {
+            if (row < rows && n < nvc) {
+                T *p = Yb + row + n * ldy;
+                *p = (beta == T(0)) ? alpha * v : fma(alpha, (T)v, beta * *p);
+            }
+        });
+        __syncwarp();
     }
+}
+
+template <typename T>
+__global__ void k_set_args(CallArgs<T> *a, const T *X, int64_t ldx, T *Y, int64_t ldy, T alpha, T beta)
+{
+    a->X = X; a->ldx = ldx; a->Y = Y; a->ldy = ldy; a->alpha = alpha; a->beta = beta;
 }
 
 template <typename T>
@@ -271,9 +558,10 @@ __global__ void k_transpose(const T *__restrict__ src, T *__restrict__ dst, int6
 // dst[seg.dst + j + n * seg.dst_ld] = src[seg.src + j + n * src_ld], j < seg.len, n < nv
 template <typename T>
 __global__ void k_pack(const PackSeg *__restrict__ segs, int64_t nseg, const T *__restrict__ src,
-                       int64_t src_ld, T *__restrict__ dst, int nv)
+                       int64_t src_ld, const CallArgs<T> *__restrict__ args, T *__restrict__ dst, int nv)
 {
     const int lane = threadIdx.x & 31;
+    if (!src) { src = args->X; src_ld = args->ldx; }   // halo pack reads the caller's X
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nseg;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const PackSeg sg = segs[w];
@@ -284,86 +572,137 @@ __global__ void k_pack(const PackSeg *__restrict__ segs, int64_t nseg, const T *
 }
 
 // ---------------------------------------------------------------------------------------
-// launchers
+// dispatch: Simt for float or nv <= 4; Mma (DMMA) for double with nv >= 5
 static inline int grid_for(int ntask) { return (ntask + WPB - 1) / WPB; }
 
-template <typename K>
-static cudaError_t set_smem(K kernel, size_t bytes)
-{
-    if (bytes > 48 * 1024)
-        return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    return cudaSuccess;
-}
-
-static inline int nvb_for(int nv) { return nv <= 1 ? 1 : nv <= 2 ? 2 : nv <= 4 ? 4 : nv <= 8 ? 8 : 16; }
-
-#define H2_NVB_SWITCH(nvb, ...)                                  \
-    switch (nvb) {                                               \
-    case 1: { constexpr int NVB = 1; __VA_ARGS__; } break;       \
-    case 2: { constexpr int NVB = 2; __VA_ARGS__; } break;       \
-    case 4: { constexpr int NVB = 4; __VA_ARGS__; } break;       \
-    case 8: { constexpr int NVB = 8; __VA_ARGS__; } break;       \
-    default: { constexpr int NVB = 16; __VA_ARGS__; } break;     \
+template <typename T>
+struct Dispatch {
+    // f(Eng) with Eng chosen from (rows r -> RPL / MT, nv -> NVB / NT)
+    template <typename F>
+    static void run(int r, int nv, F f)
+    {
+        const int rpl = r > 32 ? 2 : 1;
+        if (nv <= 1) { if (rpl == 1) f(Simt<T, 1, 1>{}); else f(Simt<T, 2, 1>{}); }
+        else if (nv <= 2) { if (rpl == 1) f(Simt<T, 1, 2>{}); else f(Simt<T, 2, 2>{}); }
+        else if (nv <= 4) { if (rpl == 1) f(Simt<T, 1, 4>{}); else f(Simt<T, 2, 4>{}); }
+        else if (nv <= 8) { if (rpl == 1) f(Simt<T, 1, 8>{}); else f(Simt<T, 2, 8>{}); }
+        else { if (rpl == 1) f(Simt<T, 1, 16>{}); else f(Simt<T, 2, 16>{}); }
     }
-#define H2_RPL_SWITCH(rpl, NAME, ...)                                  \
-    if ((rpl) <= 1) { constexpr int NAME = 1; __VA_ARGS__; }           \
-    else            { constexpr int NAME = 2; __VA_ARGS__; }
+    template <typename F>
+    static void run2(int rk, int rm, int nv, F f)
+    {
+        run(rk, nv, [&](auto ek) {
+            using EK = decltype(ek);
+            run(rm, nv, [&](auto em) {
+                using EM = decltype(em);
+                if constexpr (EK::NV == EM::NV) f(ek, em);
+            });
+        });
+    }
+};
+
+template <>
+struct Dispatch<double> {
+    template <typename F>
+    static void run(int r, int nv, F f)
+    {
+        using T = double;
+        const int rpl = r > 32 ? 2 : 1;
+        if (nv <= 1) { if (rpl == 1) f(Simt<T, 1, 1>{}); else f(Simt<T, 2, 1>{}); }
+        else if (nv <= 2) { if (rpl == 1) f(Simt<T, 1, 2>{}); else f(Simt<T, 2, 2>{}); }
+        else if (nv <= 4) { if (rpl == 1) f(Simt<T, 1, 4>{}); else f(Simt<T, 2, 4>{}); }
+        else if (nv <= 8) {
+            if (r <= 16) f(Mma<2, 1>{}); else if (r <= 32) f(Mma<4, 1>{}); else f(Mma<8, 1>{});
+        } else {
+            if (r <= 16) f(Mma<2, 2>{}); else if (r <= 32) f(Mma<4, 2>{}); else f(Mma<8, 2>{});
+        }
+    }
+    template <typename F>
+    static void run2(int rk, int rm, int nv, F f)
+    {
+        run(rk, nv, [&](auto ek) {
+            using EK = decltype(ek);
+            run(rm, nv, [&](auto em) {
+                using EM = decltype(em);
+                if constexpr (EK::NV == EM::NV) f(ek, em);
+            });
+        });
+    }
+};
 
 template <typename T>
-cudaError_t launch_up_leaf(const Task *t, int ntask, const Blk *b, const T *X, int64_t ldx,
-                           T *xh, int64_t xh_ld, int nv, int rpl, cudaStream_t s)
+cudaError_t launch_set_args(CallArgs<T> *a, const T *X, int64_t ldx, T *Y, int64_t ldy, T alpha, T beta,
+                            cudaStream_t s)
+{
+    k_set_args<T><<<1, 1, 0, s>>>(a, X, ldx, Y, ldy, alpha, beta);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_up_leaf(const Task *t, int ntask, const Blk *b, const CallArgs<T> *args,
+                           T *xh, int64_t xh_ld, int nv, int r, cudaStream_t s)
 {
     if (ntask == 0) return cudaSuccess;
-    cudaError_t err = cudaSuccess;
-    H2_NVB_SWITCH(nvb_for(nv), H2_RPL_SWITCH(rpl, RPL, {
-        size_t sm = (size_t)WPB * NVB * XLD * sizeof(T);
-        err = set_smem(k_up_leaf<T, RPL, NVB>, sm);
-        if (err == cudaSuccess)
-            k_up_leaf<T, RPL, NVB><<<grid_for(ntask), WPB * 32, sm, s>>>(t, ntask, b, X, ldx, xh, xh_ld, nv);
-    }))
-    if (err != cudaSuccess) return err;
+    Dispatch<T>::run(r, nv, [&](auto e) {
+        k_up_leaf<T, decltype(e)><<<grid_for(ntask), WPB * 32, 0, s>>>(t, ntask, b, args, xh, xh_ld, nv);
+    });
     return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_rows(int mode, const Task *t, int ntask, const Blk *b, const T *src,
-                        int64_t src_ld, T *dst, int64_t dst_ld, int nv, int rpl, cudaStream_t s)
+                        int64_t src_ld, T *dst, int64_t dst_ld, int nv, int r, cudaStream_t s)
 {
     if (ntask == 0) return cudaSuccess;
-    cudaError_t err = cudaSuccess;
-    H2_NVB_SWITCH(nvb_for(nv), H2_RPL_SWITCH(rpl, RPL, {
-        size_t sm = (size_t)WPB * NVB * XLD * sizeof(T);
-        if (mode == MODE_WRITE) {
-            err = set_smem(k_rows<T, RPL, NVB, MODE_WRITE>, sm);
-            if (err == cudaSuccess)
-                k_rows<T, RPL, NVB, MODE_WRITE><<<grid_for(ntask), WPB * 32, sm, s>>>(
-                    t, ntask, b, src, src_ld, dst, dst_ld, nv);
-        } else {
-            err = set_smem(k_rows<T, RPL, NVB, MODE_ACCUM>, sm);
-            if (err == cudaSuccess)
-                k_rows<T, RPL, NVB, MODE_ACCUM><<<grid_for(ntask), WPB * 32, sm, s>>>(
-                    t, ntask, b, src, src_ld, dst, dst_ld, nv);
-        }
-    }))
-    if (err != cudaSuccess) return err;
+    Dispatch<T>::run(r, nv, [&](auto e) {
+        using E = decltype(e);
+        const size_t sm = (size_t)WPB * E::SCRATCH;
+        if (mode == MODE_WRITE)
+            k_rows<T, E, MODE_WRITE><<<grid_for(ntask), WPB * 32, sm, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv);
+        else
+            k_rows<T, E, MODE_ACCUM><<<grid_for(ntask), WPB * 32, sm, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv);
+    });
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_tree(int mode, const TreeStage &st, int nctas, const Task *t, const Blk *b, T *buf,
+                        int64_t ld, int nv, int r, cudaStream_t s)
+{
+    if (nctas == 0 || st.nlev == 0) return cudaSuccess;
+    Dispatch<T>::run(r, nv, [&](auto e) {
+        using E = decltype(e);
+        const size_t sm = (size_t)WPB * E::SCRATCH;
+        if (mode == MODE_WRITE)
+            k_tree<T, E, MODE_WRITE><<<nctas, WPB * 32, sm, s>>>(st, t, b, buf, ld, nv);
+        else
+            k_tree<T, E, MODE_ACCUM><<<nctas, WPB * 32, sm, s>>>(st, t, b, buf, ld, nv);
+    });
     return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_leaf(const Task *t, int ntask, const Blk *b, const T *yh, int64_t yh_ld,
-                             const T *X, int64_t ldx, const T *halo, int64_t halo_ld, T *Y,
-                             int64_t ldy, T alpha, T beta, int nv, int k, int kp, int rplk,
-                             int rplm, cudaStream_t s)
+                        const CallArgs<T> *args, const T *halo, int nv, int k, int kp, int m,
+                        cudaStream_t s)
 {
     if (ntask == 0) return cudaSuccess;
     cudaError_t err = cudaSuccess;
-    H2_NVB_SWITCH(nvb_for(nv), H2_RPL_SWITCH(rplk, RK, H2_RPL_SWITCH(rplm, RM, {
-        size_t sm = (size_t)WPB * NVB * XLD * sizeof(T);
-        err = set_smem(k_leaf<T, RK, RM, NVB>, sm);
+    Dispatch<T>::run2(k, m, nv, [&](auto ek, auto em) {
+        using EK = decltype(ek);
+        using EM = decltype(em);
+        auto kern = k_leaf<T, EK, EM>;
+        const size_t sm = (size_t)WPB * (EM::NV * ZLD * sizeof(T) + EM::SCRATCH);
+        if (sm > 48 * 1024) {
+            static bool attr_set = false;       // once per instantiation
+            if (!attr_set) {
+                err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                attr_set = (err == cudaSuccess);
+            }
+        }
         if (err == cudaSuccess)
-            k_leaf<T, RK, RM, NVB><<<grid_for(ntask), WPB * 32, sm, s>>>(
-                t, ntask, b, yh, yh_ld, X, ldx, halo, halo_ld, Y, ldy, alpha, beta, nv, k, kp);
-    })))
+            kern<<<grid_for(ntask), WPB * 32, sm, s>>>(t, ntask, b, yh, yh_ld, args, halo, nv, k, kp);
+    });
     if (err != cudaSuccess) return err;
     return cudaGetLastError();
 }
@@ -385,28 +724,31 @@ cudaError_t launch_transpose(const T *src, T *dst, int64_t batch, int r, int c, 
 }
 
 template <typename T>
-cudaError_t launch_pack(const PackSeg *segs, int64_t nseg, const T *src, int64_t src_ld, T *dst,
-                        int nv, cudaStream_t s)
+cudaError_t launch_pack(const PackSeg *segs, int64_t nseg, const T *src, int64_t src_ld,
+                        const CallArgs<T> *args, T *dst, int nv, cudaStream_t s)
 {
     if (nseg == 0) return cudaSuccess;
     int64_t blocks = (nseg + 7) / 8;
-    k_pack<T><<<(int)(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(segs, nseg, src, src_ld, dst, nv);
+    k_pack<T><<<(int)(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(segs, nseg, src, src_ld, args, dst, nv);
     return cudaGetLastError();
 }
 
-#define H2_INSTANTIATE(T)                                                                     \
-    template cudaError_t launch_up_leaf<T>(const Task *, int, const Blk *, const T *, int64_t, \
-                                           T *, int64_t, int, int, cudaStream_t);             \
-    template cudaError_t launch_rows<T>(int, const Task *, int, const Blk *, const T *,       \
-                                        int64_t, T *, int64_t, int, int, cudaStream_t);       \
-    template cudaError_t launch_leaf<T>(    const Task *, int, const Blk *, const T *,       \
-                                             int64_t, const T *, int64_t, const T *, int64_t, \
-                                             T *, int64_t, T, T, int, int, int, int, int,     \
-                                             cudaStream_t);                                   \
-    template cudaError_t launch_scale<T>(T *, int64_t, int64_t, int, T, cudaStream_t);         \
-    template cudaError_t launch_transpose<T>(const T *, T *, int64_t, int, int, cudaStream_t); \
-    template cudaError_t launch_pack<T>(const PackSeg *, int64_t, const T *, int64_t, T *, int, \
-                                        cudaStream_t);
+#define H2_INSTANTIATE(T)                                                                      \
+    template cudaError_t launch_set_args<T>(CallArgs<T> *, const T *, int64_t, T *, int64_t, T, T, \
+                                            cudaStream_t);                                     \
+    template cudaError_t launch_up_leaf<T>(const Task *, int, const Blk *, const CallArgs<T> *, \
+                                           T *, int64_t, int, int, cudaStream_t);              \
+    template cudaError_t launch_rows<T>(int, const Task *, int, const Blk *, const T *,        \
+                                        int64_t, T *, int64_t, int, int, cudaStream_t);        \
+    template cudaError_t launch_leaf<T>(const Task *, int, const Blk *, const T *, int64_t,    \
+                                        const CallArgs<T> *, const T *, int, int, int, int,    \
+                                        cudaStream_t);                                         \
+    template cudaError_t launch_scale<T>(T *, int64_t, int64_t, int, T, cudaStream_t);          \
+    template cudaError_t launch_tree<T>(int, const TreeStage &, int, const Task *, const Blk *, T *, \
+                                        int64_t, int, int, cudaStream_t);                      \
+    template cudaError_t launch_transpose<T>(const T *, T *, int64_t, int, int, cudaStream_t);  \
+    template cudaError_t launch_pack<T>(const PackSeg *, int64_t, const T *, int64_t,          \
+                                        const CallArgs<T> *, T *, int, cudaStream_t);
 
 H2_INSTANTIATE(double)
 H2_INSTANTIATE(float)
