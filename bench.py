@@ -203,11 +203,8 @@ def main():
     t_gen = time.perf_counter() - t_gen
     nccl_id = None
     if P > 1:
-        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rk == 0:
-            idt.copy_(torch.frombuffer(bytearray(pkg.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.cpu().numpy().tolist())
+        from paper_2109_05451_b200.operator import broadcast_nccl_id
+        nccl_id = broadcast_nccl_id(dev)
     nv_max = max(wl["nvs"])
     op = pkg.H2Operator(dtype=wl["dtype"], nv_max=nv_max, nccl_id=nccl_id, **kw)
     n_local = int(kw["n_local"])
@@ -314,10 +311,7 @@ def main():
             traffic = tr["phases"][dom]
     except Exception:
         pass
-    roofline = {"bound": "hbm", "kernel": {"up_leaf": "k_up_leaf", "up_transfer": "k_rows<WRITE>",
-                                           "coupling_diag": "k_rows<WRITE>", "coupling_offdiag": "k_rows<ACCUM>",
-                                           "down_transfer": "k_rows<ACCUM>", "leaf_dense": "k_leaf",
-                                           "exchange_top": "k_pack"}.get(dom, dom),
+    roofline = {"bound": "hbm", "kernel": pkg._binding.KERNEL_OF_PHASE.get(dom, dom),
                 "phase": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": traffic, "peak_source": hbm_src,
                 "algorithmic_bytes_per_step": bytes_dom, "ms_per_step": ms_dom}

@@ -119,21 +119,34 @@ int h2_stats(h2_handle h, int nv, double *flops, double *bytes, double *xchg_byt
              int *launches);
 
 /* Phase profiling.  Phases: 0 upsweep leaves, 1 upsweep transfers,
- * 2 exchange pack + replicated top tree, 3 coupling (diagonal), 4 coupling (off-diagonal,
- * after the exchange wait), 5 downsweep transfers, 6 leaves (last transfer + U expansion + dense
- * + epilogue).  h2_set_profiling(h, 1) records CUDA events on the handle's stream between phases
- * of every following h2_matvec; h2_phase_times synchronizes, returns the mean milliseconds per
- * phase per call since the last read (ms[0..6], ms[7] = whole call) and the call count, and
- * resets.  h2_phase_stats returns the algorithmic bytes and flops of each phase for nv vectors
- * (beta == 0), ms-indexed the same way (index 7 = total). */
+ * 2 exchange pack + replicated top tree, 3 coupling (diagonal, levels above the leaves),
+ * 4 coupling (off-diagonal, after the exchange wait), 5 downsweep transfers, 6 leaves (last
+ * transfer + U expansion), 7 dense near field + epilogue (own concurrent stream), 8 coupling at
+ * the leaf level (diagonal; own concurrent stream).  h2_set_profiling(h, 1) records
+ * CUDA events between phases of every following h2_matvec (eager launches, no graph);
+ * h2_phase_times synchronizes, returns the mean milliseconds per phase per call since the last
+ * read (ms[0..8]; ms[9] = whole call on the main stream) and the call count, and resets.
+ * h2_phase_stats returns the algorithmic bytes and flops of each phase for nv vectors
+ * (beta == 0), indexed the same way (index 9 = total). */
+#define H2_NPHASE 9
 int h2_set_profiling(h2_handle h, int on);
-int h2_phase_times(h2_handle h, double ms[8], int64_t *ncalls);
-int h2_phase_stats(h2_handle h, int nv, double bytes[8], double flops[8]);
+int h2_phase_times(h2_handle h, double ms[H2_NPHASE + 1], int64_t *ncalls);
+int h2_phase_stats(h2_handle h, int nv, double bytes[H2_NPHASE + 1], double flops[H2_NPHASE + 1]);
 
 /* Plan facts for tests: counts[0..7] = {diag coupling blocks, offdiag coupling blocks,
  * root (top-tree) coupling blocks, diag dense blocks, offdiag dense blocks, peers,
  * remote x^ nodes received, remote leaves received}. */
 int h2_plan_counts(h2_handle h, int64_t counts[8]);
+
+/* Host-only plan census (no device, no communication): the compressed off-diagonal node lists of
+ * this rank's view in the paper's format (Fig. compressed_vnodes): for coupling
+ * level `level` (0..q) -- or the dense halo leaves when level == -1 -- pid[0..npid) are the peer
+ * ranks this rank receives from (ascending), and nodes[nodes_ptr[i] .. nodes_ptr[i+1]) the
+ * ascending GLOBAL node (leaf) indices it needs from pid[i].  Call once with pid / nodes_ptr /
+ * nodes NULL to get the sizes (*npid, *nnodes), then with buffers of [npid], [npid+1], [nnodes].
+ * Validates the description like h2_create (nv_max treated as 1). */
+int h2_plan_census(const h2_desc *d, int level, int64_t *pid, int64_t *nodes_ptr, int64_t *nodes,
+                   int64_t *npid, int64_t *nnodes);
 
 /* Release device memory, the NCCL communicator and streams.  NULL is a no-op. */
 int h2_destroy(h2_handle h);

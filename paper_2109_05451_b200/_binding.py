@@ -16,9 +16,13 @@ H2_MEM_HOST, H2_MEM_DEVICE = 0, 1
 
 EXPORTS = ["h2_create", "h2_matvec", "h2_matvec_ld", "h2_matvec_host", "h2_set_stream", "h2_stats",
            "h2_set_profiling", "h2_phase_times", "h2_phase_stats",
-           "h2_plan_counts", "h2_destroy", "h2_nccl_unique_id", "h2_last_error", "h2_version"]
+           "h2_plan_counts", "h2_plan_census", "h2_destroy", "h2_nccl_unique_id", "h2_last_error", "h2_version"]
 PHASES = ["up_leaf", "up_transfer", "exchange_top", "coupling_diag", "coupling_offdiag",
-          "down_transfer", "leaf_dense"]
+          "down_transfer", "leaf_u", "dense", "coupling_leaf"]
+KERNEL_OF_PHASE = {"up_leaf": "k_up_leaf", "up_transfer": "k_tree<WRITE>", "exchange_top": "k_pack",
+                   "coupling_diag": "k_rows<WRITE>", "coupling_offdiag": "k_rows<ACCUM>",
+                   "down_transfer": "k_tree<ACCUM>", "leaf_u": "k_leaf_u", "dense": "k_dense",
+                   "coupling_leaf": "k_rows<WRITE>"}
 
 
 class H2Error(RuntimeError):
@@ -61,6 +65,7 @@ def load_library(path=None):
         "h2_set_stream": ([vp, vp], i32),
         "h2_stats": ([vp, i32, C.POINTER(d), C.POINTER(d), C.POINTER(d), C.POINTER(i32)], i32),
         "h2_plan_counts": ([vp, C.POINTER(C.c_int64)], i32),
+        "h2_plan_census": ([C.POINTER(h2_desc), i32, vp, vp, vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], i32),
         "h2_set_profiling": ([vp, i32], i32),
         "h2_phase_times": ([vp, C.POINTER(d), C.POINTER(C.c_int64)], i32),
         "h2_phase_stats": ([vp, i32, C.POINTER(d), C.POINTER(d)], i32),
@@ -92,27 +97,22 @@ def _is_torch(a):
     return type(a).__module__.startswith("torch")
 
 
-class H2Operator:
-    """One rank's H² operator on the GPU (h2_create / h2_matvec / h2_destroy).
-
-    Floating arrays: numpy arrays (HOST: copied) or CUDA torch tensors (DEVICE: adopted and
-    kept alive by this object); all of one kind.  Integer arrays: numpy.  Shapes follow
-    include/h2.h (column-major small matrices)."""
+class _Desc:
+    """Marshals one rank's arrays into an h2_desc (keeps the buffers alive)."""
 
     def __init__(self, *, depth, leaf_size, level_rank, leaf_ptr, U_leaf, V_leaf, E, F, S_rowptr,
-                 S_col, S, D_rowptr, D_col, D, n_local, rank=0, nranks=1, dtype="f64", nv_max=16,
-                 nccl_id=None):
-        lib = load_library()
-        self._lib = lib
+                 S_col, S, D_rowptr, D_col, D, n_local, rank=0, nranks=1, dtype="f64"):
         self.dtype = {"f64": H2_F64, "f32": H2_F32}[dtype]
         self.np_dtype = np.float64 if self.dtype == H2_F64 else np.float32
-        self.n_local, self.nv_max, self.rank, self.nranks = int(n_local), int(nv_max), rank, nranks
         fl = [U_leaf, V_leaf, D] + [a for a in list(E) + list(F) + list(S) if a is not None]
-        device = any(_is_torch(a) and a.is_cuda for a in fl)
-        self._keep = []
+        self.device = device = any(_is_torch(a) and a.is_cuda for a in fl)
+        self.keep = []
+
+        def size(a):
+            return 0 if a is None else (a.numel() if _is_torch(a) else a.size)
 
         def fptr(a):
-            if a is None:
+            if a is None or size(a) == 0:
                 return None
             if device:
                 if not (_is_torch(a) and a.is_cuda and a.is_contiguous()):
@@ -120,46 +120,80 @@ class H2Operator:
                 want = "torch.float64" if self.dtype == H2_F64 else "torch.float32"
                 if str(a.dtype) != want:
                     raise ValueError(f"float arrays must be {want}")
-                self._keep.append(a)
+                self.keep.append(a)
                 return a.data_ptr()
             a = np.ascontiguousarray(a, dtype=self.np_dtype)
-            self._keep.append(a)
+            self.keep.append(a)
             return a.ctypes.data
 
         def iptr(a, dt):
             a = np.ascontiguousarray(a, dtype=dt)
-            self._keep.append(a)
+            self.keep.append(a)
             return a.ctypes.data
 
         q = int(depth)
         arr = lambda vals: (C.c_void_p * (q + 1))(*vals)
-        self._E = arr([fptr(e) if e is not None else None for e in E])
-        self._F = arr([fptr(f) if f is not None else None for f in F])
-        self._Srp = arr([iptr(r, np.int64) for r in S_rowptr])
-        self._Scol = arr([iptr(c, np.int32) for c in S_col])
-        self._S = arr([fptr(s) if (s is not None and s.size if not _is_torch(s) else s.numel()) else None
-                       for s in S])
+        self.E = arr([fptr(e) for e in E])
+        self.F = arr([fptr(f) for f in F])
+        self.Srp = arr([iptr(r, np.int64) for r in S_rowptr])
+        self.Scol = arr([iptr(c, np.int32) for c in S_col])
+        self.S = arr([fptr(s) for s in S])
         d = h2_desc()
         d.dtype, d.mem, d.depth, d.leaf_size = self.dtype, H2_MEM_DEVICE if device else H2_MEM_HOST, q, int(leaf_size)
         d.rank, d.nranks, d.n_local = int(rank), int(nranks), int(n_local)
         d.level_rank = iptr(level_rank, np.int32)
         d.leaf_ptr = iptr(leaf_ptr, np.int64)
         d.U_leaf, d.V_leaf = fptr(U_leaf), fptr(V_leaf)
-        d.E, d.F = C.cast(self._E, C.c_void_p), C.cast(self._F, C.c_void_p)
-        d.S_rowptr, d.S_col, d.S = (C.cast(self._Srp, C.c_void_p), C.cast(self._Scol, C.c_void_p),
-                                    C.cast(self._S, C.c_void_p))
+        d.E, d.F = C.cast(self.E, C.c_void_p), C.cast(self.F, C.c_void_p)
+        d.S_rowptr, d.S_col, d.S = (C.cast(self.Srp, C.c_void_p), C.cast(self.Scol, C.c_void_p),
+                                    C.cast(self.S, C.c_void_p))
         d.D_rowptr, d.D_col = iptr(D_rowptr, np.int64), iptr(D_col, np.int32)
-        d.D = fptr(D) if (D is not None and (D.numel() if _is_torch(D) else D.size)) else None
+        d.D = fptr(D)
+        self.desc = d
+
+
+def plan_census(level, **kw):
+    """Host-only compressed off-diagonal node lists (pid, nodes_ptr, nodes) of one rank's view
+    (PAPER.md:454-468); level -1 = dense halo leaves.  No GPU needed."""
+    lib = load_library()
+    kw = dict(kw)
+    for key in ("dtype", "nv_max", "nccl_id"):
+        kw.pop(key, None)
+    ds = _Desc(**kw)
+    npid, nn = C.c_int64(), C.c_int64()
+    _check(lib.h2_plan_census(C.byref(ds.desc), int(level), None, None, None, C.byref(npid), C.byref(nn)))
+    pid = np.zeros(npid.value, dtype=np.int64)
+    ptr = np.zeros(npid.value + 1, dtype=np.int64)
+    nodes = np.zeros(nn.value, dtype=np.int64)
+    _check(lib.h2_plan_census(C.byref(ds.desc), int(level), pid.ctypes.data, ptr.ctypes.data,
+                              nodes.ctypes.data, C.byref(npid), C.byref(nn)))
+    return pid, ptr, nodes
+
+
+class H2Operator:
+    """One rank's H² operator on the GPU (h2_create / h2_matvec / h2_destroy).
+
+    Floating arrays: numpy arrays (HOST: copied) or CUDA torch tensors (DEVICE: adopted and
+    kept alive by this object); all of one kind.  Integer arrays: numpy.  Shapes follow
+    include/h2.h (column-major small matrices)."""
+
+    def __init__(self, *, dtype="f64", nv_max=16, nccl_id=None, **kw):
+        lib = load_library()
+        self._lib = lib
+        ds = _Desc(dtype=dtype, **kw)
+        self.dtype, self.np_dtype = ds.dtype, ds.np_dtype
+        self.n_local, self.nv_max = int(kw["n_local"]), int(nv_max)
+        self.rank, self.nranks = int(kw.get("rank", 0)), int(kw.get("nranks", 1))
         idbuf = None
-        if nranks > 1:
+        if self.nranks > 1:
             if nccl_id is None or len(nccl_id) != 128:
                 raise ValueError("nccl_id (128 bytes) required when nranks > 1")
             idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
         h = C.c_void_p()
-        _check(lib.h2_create(C.byref(d), int(nv_max), C.cast(idbuf, C.c_void_p) if idbuf else None, C.byref(h)))
+        _check(lib.h2_create(C.byref(ds.desc), int(nv_max), C.cast(idbuf, C.c_void_p) if idbuf else None,
+                             C.byref(h)))
         self.handle = h
-        if not device:
-            self._keep = []     # host arrays were copied by h2_create
+        self._keep = ds.keep if ds.device else []   # host arrays were copied by h2_create
 
     # -- calls
     def set_stream(self, stream_ptr):
@@ -196,13 +230,13 @@ class H2Operator:
 
     def phase_times(self):
         """Mean ms per phase per call since the last read (dict incl. 'total'), and the call count."""
-        ms, n = (C.c_double * 8)(), C.c_int64()
+        ms, n = (C.c_double * 10)(), C.c_int64()
         _check(self._lib.h2_phase_times(self.handle, ms, C.byref(n)))
         out = dict(zip(PHASES + ["total"], list(ms)))
         return out, n.value
 
     def phase_stats(self, nv):
-        b, f = (C.c_double * 8)(), (C.c_double * 8)()
+        b, f = (C.c_double * 10)(), (C.c_double * 10)()
         _check(self._lib.h2_phase_stats(self.handle, int(nv), b, f))
         return dict(zip(PHASES + ["total"], list(b))), dict(zip(PHASES + ["total"], list(f)))
 

@@ -85,6 +85,15 @@ bool load_nccl()
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// H2_DEBUG=1: trace the setup / call steps on stderr (debugging multi-rank hangs)
+bool dbg_on()
+{
+    static int on = -1;
+    if (on < 0) { const char *e = getenv("H2_DEBUG"); on = (e && e[0] == '1') ? 1 : 0; }
+    return on == 1;
+}
+#define H2_DBG(...) do { if (dbg_on()) { fprintf(stderr, "[h2] " __VA_ARGS__); fputc('\n', stderr); fflush(stderr); } } while (0)
+
 // ------------------------------------------------------------------ host-side plan
 struct Layout {
     int q = 0, m = 0, p = 0, P = 1, C = 0;
@@ -170,6 +179,45 @@ int validate(const h2_desc *d, int nv_max, Layout &L)
     return H2_OK;
 }
 
+// Which remote nodes this rank's block rows need: for every peer, the sorted
+// unique off-diagonal column nodes (level, node) of the coupling blocks and the remote leaves of
+// the dense blocks; plus the diagonal / off-diagonal / root block counts.
+struct RemoteNeeds {
+    std::map<int, std::vector<int64_t>> need_x;   // peer -> sorted unique node keys
+    std::map<int, std::vector<int64_t>> need_h;   // peer -> sorted unique global leaves
+    int64_t n_diag = 0, n_off = 0, n_root = 0, nd_diag = 0, nd_off = 0;
+};
+
+void remote_needs(const h2_desc *d, const Layout &L, RemoteNeeds &rn)
+{
+    const int q = L.q, p = L.p;
+    for (int l = 0; l <= q; ++l) {
+        const int64_t *rp = d->S_rowptr[l];
+        for (int64_t i = 0; i < L.held(l); ++i)
+            for (int64_t b = rp[i]; b < rp[i + 1]; ++b) {
+                int64_t s = d->S_col[l][b];
+                int o = L.owner(l, s);
+                if (o < 0) ++rn.n_root;
+                else if (o == p) ++rn.n_diag;
+                else { ++rn.n_off; rn.need_x[o].push_back(node_key(l, s)); }
+            }
+    }
+    const int64_t nleaf = L.held(q);
+    for (int64_t t = 0; t < nleaf; ++t)
+        for (int64_t b = d->D_rowptr[t]; b < d->D_rowptr[t + 1]; ++b) {
+            int64_t s = d->D_col[b];
+            int o = L.owner(q, s);
+            if (o < 0 || o == p) ++rn.nd_diag;
+            else { ++rn.nd_off; rn.need_h[o].push_back(s); }
+        }
+    for (auto *m : {&rn.need_x, &rn.need_h})
+        for (auto &kv : *m) {
+            auto &v = kv.second;
+            std::sort(v.begin(), v.end());
+            v.erase(std::unique(v.begin(), v.end()), v.end());
+        }
+}
+
 struct Phase {
     int64_t t0 = 0;
     int n = 0;
@@ -189,7 +237,11 @@ struct h2_ctx {
     bool has_top = false;            // P > 1 and the top tree (levels < C) holds couplings
     cudaStream_t stream = nullptr;   // caller's stream (default legacy)
     cudaStream_t s_comm = nullptr;
+    cudaStream_t s_dense = nullptr;  // low-priority stream of the dense near field
+    cudaStream_t s_leafc = nullptr;  // leaf-level coupling, concurrent with the upsweep transfers
     cudaEvent_t ev_packed = nullptr, ev_recv = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_dense = nullptr, ev_halo = nullptr;
+    cudaEvent_t ev_upleaf = nullptr, ev_leafc = nullptr;
     std::vector<void *> owned;       // device allocations to free
     // operator (device)
     const void *U = nullptr, *Vt = nullptr, *D = nullptr;
@@ -205,8 +257,8 @@ struct h2_ctx {
     Task *d_tasks = nullptr;
     Blk *d_blks = nullptr;
     PackSeg *d_segs = nullptr;
-    Phase up_leaf, coup_off[3], leaf;
-    std::vector<Phase> up_lv, top_up_lv, coup_diag, down_lv;
+    Phase up_leaf, coup_off[3], leaf, dense;
+    std::vector<Phase> up_lv, top_up_lv, coup_diag, coup_leaf, down_lv;
     struct Stage { TreeStage st; int nctas; int r; };
     std::vector<Stage> up_stages, top_stages, down_stages;
     std::vector<int> up_lv_level, top_up_level, down_level;
@@ -233,8 +285,8 @@ struct h2_ctx {
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;   // 8 events per recorded call
     int64_t ev_used = 0;
-    double ph_ops[7] = {0, 0, 0, 0, 0, 0, 0};   // operator scalars per phase
-    double ph_vec[7] = {0, 0, 0, 0, 0, 0, 0};   // vector elements per nv per phase
+    double ph_ops[H2_NPHASE] = {};   // operator scalars per phase
+    double ph_vec[H2_NPHASE] = {};   // vector elements per nv per phase
     // stats
     double ops_local = 0;            // stored operator scalars held by this rank
     int64_t counts[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -280,15 +332,19 @@ ncclDataType_t nccl_type(int dtype) { return dtype == H2_F64 ? ncclDouble : nccl
 int release(h2_ctx *h)
 {
     if (!h) return H2_OK;
+    // captured graphs hold references to the NCCL communicator's resources: destroy them first
+    for (auto &g : h->graph)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    cudaDeviceSynchronize();
     if (h->comm && g_nccl.loaded) g_nccl.CommDestroy(h->comm);
     for (void *p : h->owned) cudaFree(p);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
-    for (auto &g : h->graph)
-        if (g) cudaGraphExecDestroy(g);
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     if (h->s_comm) cudaStreamDestroy(h->s_comm);
-    if (h->ev_packed) cudaEventDestroy(h->ev_packed);
-    if (h->ev_recv) cudaEventDestroy(h->ev_recv);
+    if (h->s_dense) cudaStreamDestroy(h->s_dense);
+    if (h->s_leafc) cudaStreamDestroy(h->s_leafc);
+    for (cudaEvent_t e : {h->ev_packed, h->ev_recv, h->ev_fork, h->ev_dense, h->ev_halo, h->ev_upleaf, h->ev_leafc})
+        if (e) cudaEventDestroy(e);
     delete h;
     return H2_OK;
 }
@@ -385,7 +441,9 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         if (!load_nccl()) { release(h); return fail(H2_ERR_NCCL, "cannot load libnccl.so.2 (set H2_NCCL_LIB)"); }
         ncclUniqueId id;
         memcpy(&id, nccl_unique_id, sizeof(id));
+        H2_DBG("rank %d: ncclCommInitRank P=%d", p, P);
         ncclResult_t r = g_nccl.CommInitRank(&h->comm, P, id, p);
+        H2_DBG("rank %d: comm ready", p);
         if (r != ncclSuccess) {
             std::string msg = std::string("ncclCommInitRank: ") + g_nccl.GetErrorString(r);
             release(h);
@@ -402,6 +460,15 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         h->dargs = dalloc(h, sizeof(CallArgs<double>), err);
         if (!h->dargs) H2_TRY(cuda_fail(h, err, "cudaMalloc(args)"));
         H2_TRYC(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+        int least = 0, greatest = 0;
+        H2_TRYC(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        H2_TRYC(cudaStreamCreateWithPriority(&h->s_dense, cudaStreamNonBlocking, least));
+        H2_TRYC(cudaStreamCreateWithPriority(&h->s_leafc, cudaStreamNonBlocking, least));
+        H2_TRYC(cudaEventCreateWithFlags(&h->ev_upleaf, cudaEventDisableTiming));
+        H2_TRYC(cudaEventCreateWithFlags(&h->ev_leafc, cudaEventDisableTiming));
+        H2_TRYC(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        H2_TRYC(cudaEventCreateWithFlags(&h->ev_dense, cudaEventDisableTiming));
+        H2_TRYC(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
         const char *g = getenv("H2_GRAPH");
         h->use_graph = !(g && g[0] == '0');
     }
@@ -439,58 +506,40 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         }
         double tree = 0;
         for (int l = 0; l <= q; ++l) tree += (double)L.held(l) * k[l];
-        double Sd = 0, So = 0;
+        double Sd = 0, So = 0, Sq = 0;
         for (int l = 0; l <= q; ++l)
             for (int64_t i = 0; i < L.held(l); ++i)
                 for (int64_t b = d->S_rowptr[l][i]; b < d->S_rowptr[l][i + 1]; ++b) {
                     int o = L.owner(l, d->S_col[l][b]);
-                    if (o < 0 || o == p) Sd += (double)k[l] * k[l]; else So += (double)k[l] * k[l];
+                    double e = (double)k[l] * k[l];
+                    if (o >= 0 && o != p) So += e;
+                    else if (l == q && q > 0) Sq += e;
+                    else Sd += e;
                 }
+        h->ph_ops[8] = Sq;
+        h->ph_vec[8] = 2.0 * (double)L.held(q) * k[q];
         h->ph_ops[0] = (double)nleaf * m * kq;
         h->ph_vec[0] = (double)d->n_local + (double)nleaf * kq;
         h->ph_ops[1] = Fops;
         h->ph_vec[1] = tree_up;
         h->ph_ops[3] = Sd;
-        h->ph_vec[3] = 2.0 * tree;
+        h->ph_vec[3] = 2.0 * (tree - (q > 0 ? (double)L.held(q) * k[q] : 0.0));
         h->ph_ops[4] = So;
         h->ph_ops[5] = Eops_mid;
         h->ph_vec[5] = tree_mid;
-        h->ph_ops[6] = (q >= 1 ? (double)nleaf * kq * k[q - 1] : 0.0) + (double)nleaf * m * kq + (double)nD * m * m;
+        h->ph_ops[6] = (q >= 1 ? (double)nleaf * kq * k[q - 1] : 0.0) + (double)nleaf * m * kq;
         h->ph_vec[6] = (double)nleaf * kq + (q >= 1 ? (double)L.held(q - 1) * k[q - 1] : 0.0) + 2.0 * d->n_local;
+        h->ph_ops[7] = (double)nD * m * m;
+        h->ph_vec[7] = 2.0 * d->n_local;   // X read (once), Y write
     }
 
     // ---- remote needs (compressed off-diagonal node lists)
-    std::map<int, std::vector<int64_t>> need_x;   // peer -> sorted unique node keys
-    std::map<int, std::vector<int64_t>> need_h;   // peer -> sorted unique global leaves
-    int64_t n_diag = 0, n_off = 0, n_root = 0, nd_diag = 0, nd_off = 0;
-    for (int l = 0; l <= q; ++l) {
-        const int64_t *rp = d->S_rowptr[l];
-        for (int64_t i = 0; i < L.held(l); ++i)
-            for (int64_t b = rp[i]; b < rp[i + 1]; ++b) {
-                int64_t s = d->S_col[l][b];
-                int o = L.owner(l, s);
-                if (o < 0) ++n_root;
-                else if (o == p) ++n_diag;
-                else { ++n_off; need_x[o].push_back(node_key(l, s)); }
-            }
-    }
-    for (int64_t t = 0; t < nleaf; ++t)
-        for (int64_t b = d->D_rowptr[t]; b < d->D_rowptr[t + 1]; ++b) {
-            int64_t s = d->D_col[b];
-            int o = L.owner(q, s);
-            if (o < 0 || o == p) ++nd_diag;
-            else { ++nd_off; need_h[o].push_back(s); }
-        }
-    for (auto &kv : need_x) {
-        auto &v = kv.second;
-        std::sort(v.begin(), v.end());
-        v.erase(std::unique(v.begin(), v.end()), v.end());
-    }
-    for (auto &kv : need_h) {
-        auto &v = kv.second;
-        std::sort(v.begin(), v.end());
-        v.erase(std::unique(v.begin(), v.end()), v.end());
-    }
+    RemoteNeeds rn;
+    remote_needs(d, L, rn);
+    auto &need_x = rn.need_x;
+    auto &need_h = rn.need_h;
+    const int64_t n_diag = rn.n_diag, n_off = rn.n_off, n_root = rn.n_root, nd_diag = rn.nd_diag,
+                  nd_off = rn.nd_off;
 
     // ---- workspaces
     h->xh_base.assign(q + 1, 0);
@@ -590,6 +639,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
                 give_h[o].push_back(v[i]);
             }
         }
+        H2_DBG("rank %d: request lists exchanged (give_x peers %zu, give_h peers %zu)", p, give_x.size(), give_h.size());
         // F_C^T of every rank for the replicated top upsweep (branch-root transfers
         // duplicated at the leaf level of the root branch)
         if (h->has_top) {
@@ -721,8 +771,11 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     std::vector<Task> offd_tasks[3];
     std::vector<Blk> offd_blks[3];
     {
-        std::vector<Task> cls[3];
-        std::vector<std::vector<Blk>> cls_blk[3];
+        // classes: engine class ci (0..2) for the levels above the leaves, 3 + ci for the leaf
+        // level (its coupling only needs x^ of the leaves: it runs on its own stream right after
+        // the leaf projection, concurrent with the upsweep transfers)
+        std::vector<Task> cls[6];
+        std::vector<std::vector<Blk>> cls_blk[6];
         for (int l = 0; l <= q; ++l) {
             if (l < C && !h->has_top) {
                 // top levels without couplings: y^ stays zero (workspace zeroed once), no tasks
@@ -744,8 +797,9 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
                     }
                 }
                 Task t{h->yh_base[l] + i * k[l], 0, (int32_t)bl.size(), (uint8_t)k[l], (uint8_t)k[l], 0, 0};
-                cls[ci].push_back(t);
-                cls_blk[ci].push_back(bl);
+                const int cj = (l == q && q > 0) ? 3 + ci : ci;
+                cls[cj].push_back(t);
+                cls_blk[cj].push_back(bl);
                 if (!offb.empty()) {
                     Task to = t;
                     to.nblk = (int32_t)offb.size();
@@ -755,24 +809,24 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
                 }
             }
         }
-        for (int ci = 0; ci < 3; ++ci) {
+        for (int cj = 0; cj < 6; ++cj) {
             // longest rows first (better tail balance)
-            std::vector<size_t> ord(cls[ci].size());
+            std::vector<size_t> ord(cls[cj].size());
             std::iota(ord.begin(), ord.end(), 0);
             std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
-                return cls[ci][a].nblk > cls[ci][b].nblk;
+                return cls[cj][a].nblk > cls[cj][b].nblk;
             });
             Phase ph;
             ph.t0 = tasks.size();
-            ph.r = cls_r[ci];
+            ph.r = cls_r[cj % 3];
             ph.n = (int)ord.size();
             for (size_t o : ord) {
-                Task t = cls[ci][o];
+                Task t = cls[cj][o];
                 t.blk0 = (int64_t)blks.size();
-                blks.insert(blks.end(), cls_blk[ci][o].begin(), cls_blk[ci][o].end());
+                blks.insert(blks.end(), cls_blk[cj][o].begin(), cls_blk[cj][o].end());
                 tasks.push_back(t);
             }
-            if (ph.n) h->coup_diag.push_back(ph);
+            if (ph.n) (cj < 3 ? h->coup_diag : h->coup_leaf).push_back(ph);
         }
         for (int ci = 0; ci < 3; ++ci) {
             h->coup_off[ci].t0 = tasks.size();
@@ -801,7 +855,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         h->down_lv.push_back(ph);
         h->down_level.push_back(l);
     }
-    // (6) leaves: last transfer, U expansion, dense near field, epilogue
+    // (6) leaves: last transfer + U expansion (Y += alpha U z)
     {
         const bool hasE = q >= 1 && (q > C || h->has_top);
         h->leaf.t0 = tasks.size();
@@ -810,13 +864,25 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         for (int64_t t = 0; t < nleaf; ++t) {
             int64_t rows = d->leaf_ptr[t + 1] - d->leaf_ptr[t];
             Task tk{d->leaf_ptr[t], (int64_t)blks.size(), 0, (uint8_t)m, (uint8_t)m, (uint8_t)rows,
-                    (uint8_t)(hasE ? 1 : 0)};
+                    (uint8_t)(hasE ? TF_HAS_E : 0)};
             if (hasE) {
                 int64_t g = L.g0(q) + t, gp = g >> 1;
                 int64_t pslot = gp - L.g0(q - 1);
                 blks.push_back({at(h->E[q], t * kq * k[q - 1]), h->yh_base[q - 1] + pslot * k[q - 1], k[q - 1], 0});
             }
             blks.push_back({at(h->U, t * m * kq), h->yh_base[q] + t * kq, kq, 0});
+            tk.nblk = (int32_t)(blks.size() - tk.blk0);
+            tasks.push_back(tk);
+        }
+    }
+    // (7) dense near field + epilogue (Y = alpha A_de X + beta Y), one task per leaf
+    {
+        h->dense.t0 = tasks.size();
+        h->dense.n = (int)nleaf;
+        h->dense.r = m;
+        for (int64_t t = 0; t < nleaf; ++t) {
+            int64_t rows = d->leaf_ptr[t + 1] - d->leaf_ptr[t];
+            Task tk{d->leaf_ptr[t], (int64_t)blks.size(), 0, (uint8_t)m, (uint8_t)m, (uint8_t)rows, 0};
             for (int64_t b = d->D_rowptr[t]; b < d->D_rowptr[t + 1]; ++b) {
                 int64_t s = d->D_col[b];
                 int o = L.owner(q, s);
@@ -833,24 +899,28 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             tasks.push_back(tk);
         }
     }
-    // ---- fused tree stages: consecutive transfer levels whose task counts halve (upsweep) or
-    //      double (downsweep) level to level run in one launch, one CTA per subtree
+    // ---- tree stages: levels with many nodes run as one full-grid launch each; the small top
+    //      levels (<= 16 nodes) are fused into one launch whose CTAs each own a subtree and sweep
+    //      it level by level (k_tree), saving the per-level launch latency
     {
-        const int JMAX = 6;
+        const int SMALL = 16;
         auto group = [&](const std::vector<Phase> &ph, bool up, std::vector<h2_ctx::Stage> &out) {
             size_t i = 0;
             while (i < ph.size()) {
                 size_t j = i + 1;
-                while (j < ph.size() && (int)(j - i) < JMAX &&
-                       (up ? (int64_t)ph[j].n * 2 == ph[j - 1].n : (int64_t)ph[j].n == 2 * (int64_t)ph[j - 1].n))
-                    ++j;
+                if (ph[i].n <= SMALL)
+                    while (j < ph.size() && (int)(j - i) < TREE_MAXLEV && ph[j].n <= SMALL &&
+                           (up ? (int64_t)ph[j].n * 2 == ph[j - 1].n : (int64_t)ph[j].n == 2 * (int64_t)ph[j - 1].n))
+                        ++j;
                 h2_ctx::Stage s{};
                 s.st.nlev = (int)(j - i);
-                s.nctas = up ? ph[j - 1].n : ph[i].n;
+                if (j - i == 1) s.nctas = ph[i].n >= WPB ? ph[i].n / WPB : 1;
+                else s.nctas = up ? ph[j - 1].n : ph[i].n;
                 s.r = 1;
                 for (size_t u = i; u < j; ++u) {
                     s.st.t0[u - i] = ph[u].t0;
-                    s.st.per[u - i] = ph[u].n / s.nctas;
+                    s.st.per[u - i] = (ph[u].n + s.nctas - 1) / s.nctas;
+                    s.st.cnt[u - i] = ph[u].n;
                     s.r = std::max(s.r, ph[u].r);
                 }
                 out.push_back(s);
@@ -863,11 +933,12 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     }
     // ---- contiguity of every task's block run (TF_ACONTIG): A_b == A_0 + b r c
     for (Task &t : tasks) {
-        const bool is_leaf = (&t - tasks.data()) >= h->leaf.t0 && (&t - tasks.data()) < h->leaf.t0 + h->leaf.n;
-        int64_t first = t.blk0 + (is_leaf ? ((t.flags & TF_HAS_E) ? 2 : 1) : 0);
+        const int64_t ti = &t - tasks.data();
+        if (ti >= h->leaf.t0 && ti < h->leaf.t0 + h->leaf.n) continue;   // [E][U]: not a run
+        int64_t first = t.blk0;
         int64_t last = t.blk0 + t.nblk;
         if (first >= last) continue;
-        const size_t bsz = (size_t)t.r * (is_leaf ? t.r : t.c) * h->esz;
+        const size_t bsz = (size_t)t.r * t.c * h->esz;
         bool ok = true;
         const char *a0 = static_cast<const char *>(blks[first].A);
         for (int64_t b = first; b < last && ok; ++b)
@@ -891,12 +962,15 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             H2_TRYC(cudaMemcpy(h->d_segs, segs.data(), segs.size() * sizeof(PackSeg), cudaMemcpyHostToDevice));
         H2_TRYC(cudaDeviceSynchronize());
     }
+    H2_DBG("rank %d: plan uploaded (%zu tasks, %zu blocks, %zu peers, has_top %d)", p, tasks.size(), blks.size(),
+           h->peers.size(), (int)h->has_top);
     int64_t peers_n = (int64_t)h->peers.size(), xr = 0, hr = 0;
     for (auto &kv : need_x) xr += (int64_t)kv.second.size();
     for (auto &kv : need_h) hr += (int64_t)kv.second.size();
     int64_t c8[8] = {n_diag, n_off, n_root, nd_diag, nd_off, peers_n, xr, hr};
     memcpy(h->counts, c8, sizeof(c8));
-    int launches = 2 + (int)h->up_stages.size() + (int)h->coup_diag.size() + (int)h->down_stages.size() + 1;
+    int launches = 2 + (int)h->up_stages.size() + (int)h->coup_diag.size() + (int)h->coup_leaf.size() +
+                   (int)h->down_stages.size() + 2;
     if (P > 1) {
         launches += 2;   // pack x^, pack halo
         for (int ci = 0; ci < 3; ++ci) launches += h->coup_off[ci].n ? 1 : 0;
@@ -922,7 +996,8 @@ extern "C" int h2_create(const h2_desc *d, int nv_max, const void *nccl_unique_i
 // ======================================================================== matvec
 namespace {
 
-// phase marker: records event `i` (0..7) of the current call when profiling is on
+// phase marker: records event `i` (0..NEV-1) of the current call when profiling is on
+constexpr int NEV = 13;
 int mark(h2_ctx *h, int i, cudaStream_t st)
 {
     if (!h->prof) return H2_OK;
@@ -949,28 +1024,56 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     int rc;
 #define H2_MARK(i) if ((rc = mark(h, i, st)) != H2_OK) return rc
     H2_MARK(0);
+    ncclDataType_t ty = nccl_type(h->dtype);
+    // 0. fork: the dense near field runs on its own low-priority stream from the start, in
+    //    parallel with the tree phases; for P > 1 the x-leaf halo it needs is
+    //    exchanged first on the comm stream (X is an input, so it can start at t = 0)
+    H2_CUDA(h, cudaEventRecord(h->ev_fork, st));
+    H2_CUDA(h, cudaStreamWaitEvent(h->s_dense, h->ev_fork, 0));
+    if (L.P > 1) {
+        H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_fork, 0));
+        H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_h0, h->nseg_h, (const T *)nullptr, 0, args, (T *)h->hsend, nv, h->s_comm));
+        H2_NCCL(h, g_nccl.GroupStart());
+        for (const auto &pr : h->peers) {
+            if (pr.hs_cnt) H2_NCCL(h, g_nccl.Send((T *)h->hsend + pr.hs_off, pr.hs_cnt * nv, ty, pr.rank, h->comm, h->s_comm));
+            if (pr.hr_cnt) H2_NCCL(h, g_nccl.Recv((T *)h->hrecv + pr.hr_off, pr.hr_cnt * nv, ty, pr.rank, h->comm, h->s_comm));
+        }
+        H2_NCCL(h, g_nccl.GroupEnd());
+        H2_CUDA(h, cudaEventRecord(h->ev_halo, h->s_comm));
+        H2_CUDA(h, cudaStreamWaitEvent(h->s_dense, h->ev_halo, 0));
+    }
+    if ((rc = mark(h, 9, h->s_dense)) != H2_OK) return rc;
+    H2_CUDA(h, launch_dense<T>(T0(h->dense), h->dense.n, h->d_blks, args, (const T *)h->hrecv, nv, L.m, h->s_dense));
+    if ((rc = mark(h, 10, h->s_dense)) != H2_OK) return rc;
+    H2_CUDA(h, cudaEventRecord(h->ev_dense, h->s_dense));
     // 1. upsweep of the local branch (PAPER.md:281 / alg:upsweep2)
     H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
                                  h->up_leaf.r, st));
     H2_MARK(1);
+    // 1b. leaf-level coupling (diagonal part) as soon as x^ of the leaves exists (alg:mult's
+    //     levels are independent), on its own stream
+    H2_CUDA(h, cudaEventRecord(h->ev_upleaf, st));
+    H2_CUDA(h, cudaStreamWaitEvent(h->s_leafc, h->ev_upleaf, 0));
+    if ((rc = mark(h, 11, h->s_leafc)) != H2_OK) return rc;
+    for (const Phase &ph : h->coup_leaf)
+        H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
+                                  nv, ph.r, h->s_leafc));
+    if ((rc = mark(h, 12, h->s_leafc)) != H2_OK) return rc;
+    H2_CUDA(h, cudaEventRecord(h->ev_leafc, h->s_leafc));
     for (const auto &sg : h->up_stages)
         H2_CUDA(h, launch_tree<T>(MODE_WRITE, sg.st, sg.nctas, h->d_tasks, h->d_blks, xh, h->xh_plane, nv,
                                   sg.r, st));
     H2_MARK(2);
-    // 2. exchange (P > 1): pack my x^ nodes and x leaves that peers need, one NCCL group on the
-    //    comm stream, overlapped with the diagonal multiply (alg:optimized_dist_mult)
+    // 2. exchange (P > 1): pack my x^ nodes that peers need, one NCCL group on the comm stream,
+    //    overlapped with the diagonal multiply (alg:optimized_dist_mult)
     if (L.P > 1) {
         H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_x0, h->nseg_x, xh, h->xh_plane, args, (T *)h->xsend, nv, st));
-        H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_h0, h->nseg_h, (const T *)nullptr, 0, args, (T *)h->hsend, nv, st));
         H2_CUDA(h, cudaEventRecord(h->ev_packed, st));
         H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_packed, 0));
-        ncclDataType_t ty = nccl_type(h->dtype);
         H2_NCCL(h, g_nccl.GroupStart());
         for (const auto &pr : h->peers) {
             if (pr.xs_cnt) H2_NCCL(h, g_nccl.Send((T *)h->xsend + pr.xs_off, pr.xs_cnt * nv, ty, pr.rank, h->comm, h->s_comm));
             if (pr.xr_cnt) H2_NCCL(h, g_nccl.Recv((T *)h->xrecv + pr.xr_off, pr.xr_cnt * nv, ty, pr.rank, h->comm, h->s_comm));
-            if (pr.hs_cnt) H2_NCCL(h, g_nccl.Send((T *)h->hsend + pr.hs_off, pr.hs_cnt * nv, ty, pr.rank, h->comm, h->s_comm));
-            if (pr.hr_cnt) H2_NCCL(h, g_nccl.Recv((T *)h->hrecv + pr.hr_off, pr.hr_cnt * nv, ty, pr.rank, h->comm, h->s_comm));
         }
         H2_NCCL(h, g_nccl.GroupEnd());
         H2_CUDA(h, cudaEventRecord(h->ev_recv, h->s_comm));
@@ -995,8 +1098,10 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
         H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
                                   nv, ph.r, st));
     H2_MARK(4);
-    // 4. off-diagonal part after the exchange (waitAll, alg:optimized_dist_mult line 11-12)
+    // 4. off-diagonal part after the exchange (waitAll, alg:optimized_dist_mult line 11-12);
+    //    it accumulates into leaf-level rows too, so the leaf coupling stream joins first
     if (L.P > 1) {
+        H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_leafc, 0));
         H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_recv, 0));
         for (int ci = 0; ci < 3; ++ci) {
             const Phase &ph = h->coup_off[ci];
@@ -1010,12 +1115,16 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
         H2_CUDA(h, launch_tree<T>(MODE_ACCUM, sg.st, sg.nctas, h->d_tasks, h->d_blks, yh, h->yh_plane, nv,
                                   sg.r, st));
     H2_MARK(6);
-    // 6. leaves: last transfer + U expansion + dense + epilogue
-    const int kq = L.k[q], kp = q >= 1 ? L.k[q - 1] : 1;
-    H2_CUDA(h, launch_leaf<T>(T0(h->leaf), h->leaf.n, h->d_blks, yh, h->yh_plane, args,
-                              (const T *)h->hrecv, nv, kq, kp, h->leaf.r, st));
+    // 6. leaves: last transfer + U expansion added into Y after the dense and leaf-coupling
+    //    streams joined
+    H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_dense, 0));
+    H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_leafc, 0));
     H2_MARK(7);
-    if (h->prof) h->ev_used += 8;
+    const int kq = L.k[q], kp = q >= 1 ? L.k[q - 1] : 1;
+    H2_CUDA(h, launch_leaf_u<T>(T0(h->leaf), h->leaf.n, h->d_blks, yh, h->yh_plane, args, nv, kq, kp,
+                                h->leaf.r, st));
+    H2_MARK(8);
+    if (h->prof) h->ev_used += NEV;
 #undef H2_MARK
     return H2_OK;
 }
@@ -1032,6 +1141,7 @@ int run_matvec(h2_ctx *h, T alpha, const T *X, int64_t ldx, T beta, T *Y, int64_
         H2_CUDA(h, launch_scale<T>(Y, ldy, h->n_local, nv, beta, st));
         return H2_OK;
     }
+    H2_DBG("rank %d: matvec nv=%d warm=%d graph=%d", h->L.p, nv, (int)h->warm[nv], (int)(h->graph[nv] != nullptr));
     H2_CUDA(h, launch_set_args<T>((CallArgs<T> *)h->dargs, X, ldx, Y, ldy, alpha, beta, st));
     if (h->prof || !h->use_graph || !h->warm[nv]) {
         h->warm[nv] = true;            // first call per nv runs eagerly (sets kernel attributes)
@@ -1138,45 +1248,83 @@ extern "C" int h2_set_profiling(h2_handle h, int on)
     return H2_OK;
 }
 
-extern "C" int h2_phase_times(h2_handle h, double ms[8], int64_t *ncalls)
+extern "C" int h2_phase_times(h2_handle h, double ms[H2_NPHASE + 1], int64_t *ncalls)
 {
     if (!h || !ms) return fail(H2_ERR_ARG, "NULL argument");
-    for (int i = 0; i < 8; ++i) ms[i] = 0;
-    int64_t calls = h->ev_used / 8;
+    for (int i = 0; i <= H2_NPHASE; ++i) ms[i] = 0;
+    int64_t calls = h->ev_used / NEV;
+    // phase -> (start event, end event) of a call; see enqueue()
+    static const int span[H2_NPHASE + 1][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6},
+                                               {7, 8}, {9, 10}, {11, 12}, {0, 8}};
     if (calls) {
-        H2_CUDA(h, cudaEventSynchronize(h->ev_pool[h->ev_used - 1]));
+        H2_CUDA(h, cudaDeviceSynchronize());
         for (int64_t c = 0; c < calls; ++c) {
-            cudaEvent_t *e = &h->ev_pool[c * 8];
-            for (int i = 0; i < 7; ++i) {
+            cudaEvent_t *e = &h->ev_pool[c * NEV];
+            for (int i = 0; i <= H2_NPHASE; ++i) {
                 float t = 0;
-                H2_CUDA(h, cudaEventElapsedTime(&t, e[i], e[i + 1]));
+                H2_CUDA(h, cudaEventElapsedTime(&t, e[span[i][0]], e[span[i][1]]));
                 ms[i] += t;
             }
-            float t = 0;
-            H2_CUDA(h, cudaEventElapsedTime(&t, e[0], e[7]));
-            ms[7] += t;
         }
-        for (int i = 0; i < 8; ++i) ms[i] /= (double)calls;
+        for (int i = 0; i <= H2_NPHASE; ++i) ms[i] /= (double)calls;
     }
     if (ncalls) *ncalls = calls;
     h->ev_used = 0;
     return H2_OK;
 }
 
-extern "C" int h2_phase_stats(h2_handle h, int nv, double bytes[8], double flops[8])
+extern "C" int h2_phase_stats(h2_handle h, int nv, double bytes[H2_NPHASE + 1], double flops[H2_NPHASE + 1])
 {
     if (!h || nv < 1) return fail(H2_ERR_ARG, "bad argument");
     double tb = 0, tf = 0;
-    for (int i = 0; i < 7; ++i) {
+    for (int i = 0; i < H2_NPHASE; ++i) {
         double b = (double)h->esz * (h->ph_ops[i] + nv * h->ph_vec[i]);
         double f = 2.0 * nv * h->ph_ops[i];
         if (bytes) bytes[i] = b;
         if (flops) flops[i] = f;
         tb += b; tf += f;
     }
-    if (bytes) bytes[7] = tb;
-    if (flops) flops[7] = tf;
+    if (bytes) bytes[H2_NPHASE] = tb;
+    if (flops) flops[H2_NPHASE] = tf;
     return H2_OK;
+}
+
+extern "C" int h2_plan_census(const h2_desc *d, int level, int64_t *pid, int64_t *nodes_ptr,
+                              int64_t *nodes, int64_t *npid, int64_t *nnodes)
+{
+    try {
+        Layout L;
+        int rc = validate(d, 1, L);
+        if (rc != H2_OK) return rc;
+        if (level < -1 || level > L.q) return fail(H2_ERR_ARG, "level out of range [-1, q]");
+        if (!npid || !nnodes) return fail(H2_ERR_ARG, "npid / nnodes is NULL");
+        RemoteNeeds rn;
+        remote_needs(d, L, rn);
+        int64_t np = 0, nn = 0;
+        if (nodes_ptr) nodes_ptr[0] = 0;
+        for (int o = 0; o < L.P; ++o) {
+            std::vector<int64_t> v;
+            if (level < 0) {
+                if (rn.need_h.count(o)) v = rn.need_h[o];
+            } else if (rn.need_x.count(o)) {
+                for (int64_t key : rn.need_x[o])
+                    if (key_level(key) == level) v.push_back(key_node(key));
+            }
+            if (v.empty()) continue;
+            if (pid) pid[np] = o;
+            for (int64_t g : v) {
+                if (nodes) nodes[nn] = g;
+                ++nn;
+            }
+            ++np;
+            if (nodes_ptr) nodes_ptr[np] = nn;
+        }
+        *npid = np;
+        *nnodes = nn;
+        return H2_OK;
+    } catch (const std::exception &e) {
+        return fail(H2_ERR_OOM, std::string("h2_plan_census: ") + e.what());
+    }
 }
 
 extern "C" int h2_plan_counts(h2_handle h, int64_t counts[8])
@@ -1189,7 +1337,7 @@ extern "C" int h2_plan_counts(h2_handle h, int64_t counts[8])
 extern "C" int h2_destroy(h2_handle h)
 {
     if (!h) return H2_OK;
-    cudaDeviceSynchronize();
+    H2_DBG("rank %d: destroy", h->L.p);
     return release(h);
 }
 

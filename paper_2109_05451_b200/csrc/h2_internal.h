@@ -71,9 +71,11 @@ template <typename T>
 cudaError_t launch_rows(int mode, const Task *t, int ntask, const Blk *b, const T *src,
                         int64_t src_ld, T *dst, int64_t dst_ld, int nv, int r, cudaStream_t s);
 template <typename T>
-cudaError_t launch_leaf(const Task *t, int ntask, const Blk *b, const T *yh, int64_t yh_ld,
-                        const CallArgs<T> *args, const T *halo, int nv, int k, int kp, int m,
-                        cudaStream_t s);
+cudaError_t launch_leaf_u(const Task *t, int ntask, const Blk *b, const T *yh, int64_t yh_ld,
+                          const CallArgs<T> *args, int nv, int k, int kp, int m, cudaStream_t s);
+template <typename T>
+cudaError_t launch_dense(const Task *t, int ntask, const Blk *b, const CallArgs<T> *args, const T *halo,
+                         int nv, int m, cudaStream_t s);
 template <typename T>
 cudaError_t launch_scale(T *Y, int64_t ldy, int64_t n, int nv, T beta, cudaStream_t s);
 template <typename T>
@@ -90,7 +92,8 @@ enum { MODE_WRITE = 0, MODE_ACCUM = 1 };
 constexpr int TREE_MAXLEV = 8;
 struct TreeStage {
     int64_t t0[TREE_MAXLEV];
-    int32_t per[TREE_MAXLEV];
+    int32_t per[TREE_MAXLEV];   // tasks per CTA
+    int32_t cnt[TREE_MAXLEV];   // tasks of the level
     int32_t nlev;
 };
 template <typename T>

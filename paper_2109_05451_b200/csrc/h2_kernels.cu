@@ -425,8 +425,10 @@ k_tree(TreeStage st, const Task *__restrict__ tasks, const Blk *__restrict__ blk
     void *scratch = smem_raw + wid * Eng::SCRATCH;
     for (int lv = 0; lv < st.nlev; ++lv) {
         const int per = st.per[lv];
-        const int64_t base = st.t0[lv] + (int64_t)blockIdx.x * per;
-        for (int ti = wid; ti < per; ti += WPB) {
+        const int64_t first = (int64_t)blockIdx.x * per;
+        const int64_t base = st.t0[lv] + first;
+        const int my = (int)min((int64_t)per, (int64_t)st.cnt[lv] - first);
+        for (int ti = wid; ti < my; ti += WPB) {
             const Task tk = tasks[base + ti];
             for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
                 const int nvc = min(Eng::NV, nv - n0);
@@ -452,19 +454,20 @@ k_tree(TreeStage st, const Task *__restrict__ tasks, const Blk *__restrict__ blk
 }
 
 // ---------------------------------------------------------------------------------------
-// Leaf kernel: last downsweep transfer + leaf expansion + dense near field + epilogue.
-// blocks: [E_t (if flags&1), x = parent y^ offset] [U_t, x = own y^ offset] [D_ts ...]
+// Leaf kernel: last downsweep transfer + leaf expansion, added into Y:
+//   z_t = y^_t + E_t y^_parent ;  Y_t += alpha U_t z_t
+// blocks: [E_t (if TF_HAS_E), x = parent y^ offset] [U_t, x = own y^ offset].  k_dense has
+// already written Y = alpha A_de X + beta Y on the dense stream (reading R11).
 // EngK computes z (rows k), EngM the leaf rows (m); z is handed over through warp smem.
 template <typename T, typename EngK, typename EngM>
 __global__ void __launch_bounds__(WPB * 32, 2)
-k_leaf(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
-       const T *__restrict__ yh, int64_t yh_ld, const CallArgs<T> *__restrict__ args,
-       const T *__restrict__ halo, int nv, int k, int kp)
+k_leaf_u(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
+         const T *__restrict__ yh, int64_t yh_ld, const CallArgs<T> *__restrict__ args, int nv, int k,
+         int kp)
 {
-    const T *__restrict__ X = args->X;
     T *__restrict__ Y = args->Y;
-    const int64_t ldx = args->ldx, ldy = args->ldy;
-    const T alpha = args->alpha, beta = args->beta;
+    const int64_t ldy = args->ldy;
+    const T alpha = args->alpha;
     static_assert(EngK::NV == EngM::NV, "engines must agree on the vector chunk");
     constexpr int NV = EngM::NV;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -472,13 +475,11 @@ k_leaf(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
     const int task = blockIdx.x * WPB + wid;
     if (task >= ntask) return;
     T *zs = reinterpret_cast<T *>(smem_raw) + wid * NV * ZLD;
-    void *scratch = smem_raw + (size_t)WPB * NV * ZLD * sizeof(T) + wid * EngM::SCRATCH;
     const Task tk = tasks[task];
-    const bool hasE = tk.flags & 1;
+    const bool hasE = tk.flags & TF_HAS_E;
     const Blk bU = blks[tk.blk0 + (hasE ? 1 : 0)];
     for (int n0 = 0; n0 < nv; n0 += NV) {
         const int nvc = min(NV, nv - n0);
-        // z_t = y^_t + E_t y^_parent
         typename EngK::Acc z;
         acc_load(z, yh + bU.x + (int64_t)n0 * yh_ld, yh_ld, k, nvc, lane);
         if (hasE) {
@@ -489,28 +490,58 @@ k_leaf(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
         __syncwarp();
         acc_store(z, zs, (int64_t)ZLD, k, nvc, lane);
         __syncwarp();
-        // y_t = U_t z_t
         typename EngM::Acc acc;
         acc_zero(acc, lane);
         EngM::block(acc, static_cast<const T *>(bU.A), tk.r, k, zs, (int64_t)ZLD, k, nvc, lane);
-        // dense near field y_t += sum_s D_ts x_s
-        const int dfirst = hasE ? 2 : 1;
-        if ((tk.flags & TF_ACONTIG) && tk.nblk > dfirst) {
-            const Blk b0 = blks[tk.blk0 + dfirst];
+        T *Yb = Y + tk.out + (int64_t)n0 * ldy;
+        const int rows = tk.rows;
+        acc.each(lane, [&](int row, int n, auto &v) {
+            if (row < rows && n < nvc) {
+                T *p = Yb + row + n * ldy;
+                *p = fma(alpha, (T)v, *p);
+            }
+        });
+        __syncwarp();
+    }
+}
+
+// Dense near field + epilogue (reading R12), on its own low-priority stream
+// concurrent with the tree phases:  Y_t = alpha sum_s D_ts x_s + beta Y_t  (beta == 0: Y is
+// write-only).  Every leaf has a task (rows without dense blocks still apply beta).
+template <typename T, typename Eng>
+__global__ void __launch_bounds__(WPB * 32, 2)
+k_dense(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
+        const CallArgs<T> *__restrict__ args, const T *__restrict__ halo, int nv)
+{
+    const T *__restrict__ X = args->X;
+    T *__restrict__ Y = args->Y;
+    const int64_t ldx = args->ldx, ldy = args->ldy;
+    const T alpha = args->alpha, beta = args->beta;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int task = blockIdx.x * WPB + wid;
+    if (task >= ntask) return;
+    void *scratch = smem_raw + wid * Eng::SCRATCH;
+    const Task tk = tasks[task];
+    for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
+        const int nvc = min(Eng::NV, nv - n0);
+        typename Eng::Acc acc;
+        acc_zero(acc, lane);
+        if ((tk.flags & TF_ACONTIG) && tk.nblk > 0) {
             const Src<T> sr{X, ldx, halo, n0};
-            EngM::stream(acc, static_cast<const T *>(b0.A), tk.r, tk.r, tk.nblk - dfirst,
-                         blks + tk.blk0 + dfirst, sr, nvc, lane, scratch);
-        } else
-        for (int bi = dfirst; bi < tk.nblk; ++bi) {
-            const Blk b = blks[tk.blk0 + bi];
-            const T *src;
-            int64_t ld;
-            if (b.x >= 0) { src = X + b.x; ld = ldx; }
-            else          { src = halo + (-b.x - 1); ld = b.xld; }
-            EngM::block(acc, static_cast<const T *>(b.A), tk.r, tk.r, src + (int64_t)n0 * ld, ld,
-                        b.xrows, nvc, lane);
+            Eng::stream(acc, static_cast<const T *>(blks[tk.blk0].A), tk.r, tk.r, tk.nblk, blks + tk.blk0,
+                        sr, nvc, lane, scratch);
+        } else {
+            for (int bi = 0; bi < tk.nblk; ++bi) {
+                const Blk b = blks[tk.blk0 + bi];
+                const T *src;
+                int64_t ld;
+                if (b.x >= 0) { src = X + b.x; ld = ldx; }
+                else          { src = halo + (-b.x - 1); ld = b.xld; }
+                Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.r, src + (int64_t)n0 * ld, ld,
+                           b.xrows, nvc, lane);
+            }
         }
-        // epilogue Y = alpha y + beta Y (beta == 0: Y not read)
         T *Yb = Y + tk.out + (int64_t)n0 * ldy;
         const int rows = tk.rows;
         acc.each(lane, [&](int row, int n, auto &v) {
@@ -519,7 +550,6 @@ k_leaf(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
                 *p = (beta == T(0)) ? alpha * v : fma(alpha, (T)v, beta * *p);
             }
         });
-        __syncwarp();
     }
 }
 
@@ -682,17 +712,16 @@ cudaError_t launch_tree(int mode, const TreeStage &st, int nctas, const Task *t,
 }
 
 template <typename T>
-cudaError_t launch_leaf(const Task *t, int ntask, const Blk *b, const T *yh, int64_t yh_ld,
-                        const CallArgs<T> *args, const T *halo, int nv, int k, int kp, int m,
-                        cudaStream_t s)
+cudaError_t launch_leaf_u(const Task *t, int ntask, const Blk *b, const T *yh, int64_t yh_ld,
+                          const CallArgs<T> *args, int nv, int k, int kp, int m, cudaStream_t s)
 {
     if (ntask == 0) return cudaSuccess;
     cudaError_t err = cudaSuccess;
     Dispatch<T>::run2(k, m, nv, [&](auto ek, auto em) {
         using EK = decltype(ek);
         using EM = decltype(em);
-        auto kern = k_leaf<T, EK, EM>;
-        const size_t sm = (size_t)WPB * (EM::NV * ZLD * sizeof(T) + EM::SCRATCH);
+        auto kern = k_leaf_u<T, EK, EM>;
+        const size_t sm = (size_t)WPB * EM::NV * ZLD * sizeof(T);
         if (sm > 48 * 1024) {
             static bool attr_set = false;       // once per instantiation
             if (!attr_set) {
@@ -701,9 +730,22 @@ cudaError_t launch_leaf(const Task *t, int ntask, const Blk *b, const T *yh, int
             }
         }
         if (err == cudaSuccess)
-            kern<<<grid_for(ntask), WPB * 32, sm, s>>>(t, ntask, b, yh, yh_ld, args, halo, nv, k, kp);
+            kern<<<grid_for(ntask), WPB * 32, sm, s>>>(t, ntask, b, yh, yh_ld, args, nv, k, kp);
     });
     if (err != cudaSuccess) return err;
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_dense(const Task *t, int ntask, const Blk *b, const CallArgs<T> *args, const T *halo,
+                         int nv, int m, cudaStream_t s)
+{
+    if (ntask == 0) return cudaSuccess;
+    Dispatch<T>::run(m, nv, [&](auto e) {
+        using E = decltype(e);
+        const size_t sm = (size_t)WPB * E::SCRATCH;
+        k_dense<T, E><<<grid_for(ntask), WPB * 32, sm, s>>>(t, ntask, b, args, halo, nv);
+    });
     return cudaGetLastError();
 }
 
@@ -740,9 +782,10 @@ cudaError_t launch_pack(const PackSeg *segs, int64_t nseg, const T *src, int64_t
                                            T *, int64_t, int, int, cudaStream_t);              \
     template cudaError_t launch_rows<T>(int, const Task *, int, const Blk *, const T *,        \
                                         int64_t, T *, int64_t, int, int, cudaStream_t);        \
-    template cudaError_t launch_leaf<T>(const Task *, int, const Blk *, const T *, int64_t,    \
-                                        const CallArgs<T> *, const T *, int, int, int, int,    \
-                                        cudaStream_t);                                         \
+    template cudaError_t launch_leaf_u<T>(const Task *, int, const Blk *, const T *, int64_t,  \
+                                          const CallArgs<T> *, int, int, int, int, cudaStream_t); \
+    template cudaError_t launch_dense<T>(const Task *, int, const Blk *, const CallArgs<T> *,   \
+                                         const T *, int, int, cudaStream_t);                   \
     template cudaError_t launch_scale<T>(T *, int64_t, int64_t, int, T, cudaStream_t);          \
     template cudaError_t launch_tree<T>(int, const TreeStage &, int, const Task *, const Blk *, T *, \
                                         int64_t, int, int, cudaStream_t);                      \

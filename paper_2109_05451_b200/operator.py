@@ -57,6 +57,19 @@ def shard_arrays(h, rank=0, P=1):
     return kw, (r0, r1)
 
 
+def broadcast_nccl_id(device):
+    """A fresh NCCL unique id (each h2_create needs its own) generated on rank 0 and broadcast
+    with torch.distributed (plumbing only)."""
+    import torch
+    import torch.distributed as dist
+    from ._binding import nccl_unique_id
+    t = torch.zeros(128, dtype=torch.uint8, device=device)
+    if dist.get_rank() == 0:
+        t.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(t, 0)
+    return bytes(t.cpu().numpy().tolist())
+
+
 def operator_from_h2data(h, rank=0, nranks=1, nccl_id=None, dtype="f64", nv_max=16, device=False,
                          torch_device=None):
     """H2Operator for `rank` of `nranks`.  device=True uploads the floating arrays as CUDA torch
