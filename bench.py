@@ -133,7 +133,7 @@ def build_problem(wl, P, rank, with_global):
     return tree, st, None, kw, rows
 
 
-def run_reference(args, wl):
+def run_reference(args, wl, emit):
     """--impl reference: the CPU oracle (oracle/, plain C FP64, single thread) on the same
     workload, one full step (every nv) per timed step; rank 0 only."""
     ws, rk, _ = dist_env()
@@ -167,10 +167,15 @@ def run_reference(args, wl):
                             "sample": f"one full step ({'+'.join('nv=%d' % v for v in wl['nvs'])} matvecs) "
                                       f"of {args.config} at full size per timed step, single-threaded C oracle"},
            "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 def main():
+    # keep stdout for the single JSON line: library / NCCL chatter goes to stderr
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(os.dup(2), "w")
+    emit = lambda obj: os.write(json_fd, (json.dumps(obj) + "\n").encode())
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -184,7 +189,7 @@ def main():
     args.warmup = max(3, args.warmup)
     wl = WORKLOADS[args.config]
     if args.impl == "reference":
-        return run_reference(args, wl)
+        return run_reference(args, wl, emit)
 
     import torch
     import torch.distributed as dist
@@ -251,7 +256,8 @@ def main():
             per_nv_ms[nv] += ev[s][i][0].elapsed_time(ev[s][i][1])
     phases, ncalls = op.phase_times()
     op.set_profiling(False)
-    # per-nv phase times: one extra profiled pass per nv (same launch configuration)
+    # per-nv phase times: one extra profiled pass per nv (same kernels; side streams serialized
+    # so each phase's CUDA events bracket only its own launches)
     for nv in wl["nvs"]:
         op.set_profiling(True)
         for _ in range(3):
@@ -344,10 +350,15 @@ def main():
                                     "gflops_per_gpu": float(ft[i + 1]) / (per_nv_ms[nv] * 1e-3) / 1e9 / P,
                                     "phases_ms": {k: round(v, 5) for k, v in per_nv_ph[nv].items()}}
                           for i, nv in enumerate(wl["nvs"])},
-               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "roofline": roofline,
+               "path_bandwidth": {str(nv): {"algorithmic_bytes": op.stats(nv)["bytes"],
+                                            "GB_s": op.stats(nv)["bytes"] / (per_nv_ms[nv] * 1e-3) / 1e9,
+                                            "frac_of_hbm": op.stats(nv)["bytes"] / (per_nv_ms[nv] * 1e-3) / 1e9 / hbm}
+                                  for nv in wl["nvs"]},
+               "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": launches * len(wl["nvs"]) * args.steps,
                "clocks": clocks.summary() if not args.profile_only else None}
-        print(json.dumps(out), flush=True)
+        emit(out)
     op.close()
     if P > 1:
         dist.barrier()

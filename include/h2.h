@@ -123,7 +123,8 @@ int h2_stats(h2_handle h, int nv, double *flops, double *bytes, double *xchg_byt
  * 4 coupling (off-diagonal, after the exchange wait), 5 downsweep transfers, 6 leaves (last
  * transfer + U expansion), 7 dense near field + epilogue (own concurrent stream), 8 coupling at
  * the leaf level (diagonal; own concurrent stream).  h2_set_profiling(h, 1) records
- * CUDA events between phases of every following h2_matvec (eager launches, no graph);
+ * CUDA events between phases of every following h2_matvec (eager launches, no graph, the side
+ * streams serialized onto the handle's stream so each phase is timed alone);
  * h2_phase_times synchronizes, returns the mean milliseconds per phase per call since the last
  * read (ms[0..8]; ms[9] = whole call on the main stream) and the call count, and resets.
  * h2_phase_stats returns the algorithmic bytes and flops of each phase for nv vectors

@@ -261,6 +261,14 @@ struct h2_ctx {
     std::vector<Phase> up_lv, top_up_lv, coup_diag, coup_leaf, down_lv;
     struct Stage { TreeStage st; int nctas; int r; };
     std::vector<Stage> up_stages, top_stages, down_stages;
+    // dependency-driven single-launch sweeps (k_chain): task ranges, their deps, the flags
+    bool use_chain = true;
+    int chain_ctas = 0;
+    int64_t up_c0 = 0, dn_c0 = 0;
+    int up_cn = 0, dn_cn = 0, up_cr = 1, dn_cr = 1;
+    ChainDep *d_deps = nullptr;      // [up_cn + dn_cn]
+    int32_t *d_flags = nullptr;
+    int64_t nflags = 0;
     std::vector<int> up_lv_level, top_up_level, down_level;
     int64_t nseg_x = 0, nseg_h = 0, seg_x0 = 0, seg_h0 = 0;
     struct Peer {
@@ -276,6 +284,10 @@ struct h2_ctx {
     // per-call arguments (device CallArgs<T>) and the captured graphs, one per nv
     void *dargs = nullptr;
     bool use_graph = true;
+    int tma_mode = 0;                // H2_TMA: 0 never, 1 always, 2 for nv <= 4 only
+    int bw_ctas = 0;                 // grid cap of the side-stream bandwidth kernels (H2_BW_CTAS)
+    bool one_side = false;           // leaf-level coupling queued behind the dense kernel (H2_ONE_SIDE)
+    bool tma_on(int nv) const { return tma_mode == 1 || (tma_mode == 2 && nv <= 4); }
     cudaStream_t cap_stream = nullptr;
     cudaStream_t last_stream = nullptr;
     bool last_stream_set = false;
@@ -459,9 +471,12 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         cudaError_t err;
         h->dargs = dalloc(h, sizeof(CallArgs<double>), err);
         if (!h->dargs) H2_TRY(cuda_fail(h, err, "cudaMalloc(args)"));
-        H2_TRYC(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+        H2_TRYC(cudaMemset(h->dargs, 0, sizeof(CallArgs<double>)));
         int least = 0, greatest = 0;
         H2_TRYC(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        // the tree chain (captured on cap_stream) gets the highest priority, the bandwidth
+        // kernels on the side streams the lowest (PAPER.md:509 low-priority stream)
+        H2_TRYC(cudaStreamCreateWithPriority(&h->cap_stream, cudaStreamNonBlocking, greatest));
         H2_TRYC(cudaStreamCreateWithPriority(&h->s_dense, cudaStreamNonBlocking, least));
         H2_TRYC(cudaStreamCreateWithPriority(&h->s_leafc, cudaStreamNonBlocking, least));
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_upleaf, cudaEventDisableTiming));
@@ -471,6 +486,15 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
         const char *g = getenv("H2_GRAPH");
         h->use_graph = !(g && g[0] == '0');
+        const char *tm = getenv("H2_TMA");
+        h->tma_mode = tm ? atoi(tm) : 0;
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const char *bc = getenv("H2_BW_CTAS");      // per SM; default 0 = uncapped grid
+        h->bw_ctas = (bc ? atoi(bc) : 0) * nsm;
+        const char *os = getenv("H2_ONE_SIDE");
+        h->one_side = os && os[0] == '1';
     }
     // ---- operator arrays on the device; V and F re-laid out as V^T, F^T (operand order)
     const int kq = k[q];
@@ -931,6 +955,67 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         group(h->top_up_lv, true, h->top_stages);
         group(h->down_lv, false, h->down_stages);
     }
+    // ---- chain sweeps: flat flag index per held node; deps on children (up) / parent (down)
+    std::vector<ChainDep> cdeps;
+    {
+        std::vector<int64_t> fbase(q + 2, 0);
+        for (int l = 0; l <= q; ++l) fbase[l + 1] = fbase[l] + L.held(l);
+        if (!h->up_lv.empty()) {
+            h->up_c0 = h->up_lv.front().t0;
+            for (size_t u = 0; u < h->up_lv.size(); ++u) {
+                const Phase &ph = h->up_lv[u];
+                const int lc = h->up_lv_level[u];          // children level; parents at lc - 1
+                if (ph.t0 != h->up_c0 + h->up_cn) { h->use_chain = false; break; }
+                for (int64_t i = 0; i < ph.n; ++i) {
+                    ChainDep dp{(int32_t)(fbase[lc - 1] + i), -1, -1, 0};
+                    if (lc <= q - 1) {                     // children computed by the chain too
+                        dp.dep0 = (int32_t)(fbase[lc] + 2 * i);
+                        dp.dep1 = (int32_t)(fbase[lc] + 2 * i + 1);
+                    }
+                    cdeps.push_back(dp);
+                }
+                h->up_cn += ph.n;
+                h->up_cr = std::max(h->up_cr, ph.r);
+            }
+        }
+        if (!h->down_lv.empty()) {
+            h->dn_c0 = h->down_lv.front().t0;
+            for (size_t u = 0; u < h->down_lv.size() && h->use_chain; ++u) {
+                const Phase &ph = h->down_lv[u];
+                const int l = h->down_level[u];
+                if (ph.t0 != h->dn_c0 + h->dn_cn) { h->use_chain = false; break; }
+                const bool parent_in_chain = u > 0 && h->down_level[u - 1] == l - 1;
+                for (int64_t c = 0; c < ph.n; ++c) {
+                    ChainDep dp{(int32_t)(fbase[l] + c), -1, -1, 0};
+                    if (parent_in_chain) {
+                        const int64_t gp = (L.g0(l) + c) >> 1;
+                        dp.dep0 = (int32_t)(fbase[l - 1] + gp - L.g0(l - 1));
+                    }
+                    cdeps.push_back(dp);
+                }
+                h->dn_cn += ph.n;
+                h->dn_cr = std::max(h->dn_cr, ph.r);
+            }
+        }
+        // default: staged launches (measured faster on B200 for cfg2); H2_CHAIN=1 enables
+        const char *ce = getenv("H2_CHAIN");
+        if (!(ce && ce[0] == '1')) h->use_chain = false;
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const char *cc = getenv("H2_CHAIN_CTAS");
+        h->chain_ctas = (cc ? atoi(cc) : 2) * nsm;
+        cudaError_t err;
+        // two flag sets: x^ nodes (upsweep chain) and y^ nodes (downsweep chain)
+        h->nflags = fbase[q + 1];
+        h->d_flags = (int32_t *)dalloc(h, (size_t)2 * fbase[q + 1] * sizeof(int32_t), err);
+        if (!h->d_flags) H2_TRY(cuda_fail(h, err, "cudaMalloc(flags)"));
+        H2_TRYC(cudaMemset(h->d_flags, 0, (size_t)2 * fbase[q + 1] * sizeof(int32_t)));
+        h->d_deps = (ChainDep *)dalloc(h, (cdeps.size() + 1) * sizeof(ChainDep), err);
+        if (!h->d_deps) H2_TRY(cuda_fail(h, err, "cudaMalloc(deps)"));
+        if (!cdeps.empty())
+            H2_TRYC(cudaMemcpy(h->d_deps, cdeps.data(), cdeps.size() * sizeof(ChainDep), cudaMemcpyHostToDevice));
+    }
     // ---- contiguity of every task's block run (TF_ACONTIG): A_b == A_0 + b r c
     for (Task &t : tasks) {
         const int64_t ti = &t - tasks.data();
@@ -1023,13 +1108,16 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     auto T0 = [&](const Phase &ph) { return h->d_tasks + ph.t0; };
     int rc;
 #define H2_MARK(i) if ((rc = mark(h, i, st)) != H2_OK) return rc
-    H2_MARK(0);
     ncclDataType_t ty = nccl_type(h->dtype);
+    // profiling serializes the side streams onto the main one so every phase's events bracket
+    // only its own kernels (clean per-kernel durations for the roofline)
+    cudaStream_t s_dense = h->prof ? st : h->s_dense;
+    cudaStream_t s_leafc = h->prof ? st : (h->one_side ? h->s_dense : h->s_leafc);
     // 0. fork: the dense near field runs on its own low-priority stream from the start, in
     //    parallel with the tree phases; for P > 1 the x-leaf halo it needs is
     //    exchanged first on the comm stream (X is an input, so it can start at t = 0)
     H2_CUDA(h, cudaEventRecord(h->ev_fork, st));
-    H2_CUDA(h, cudaStreamWaitEvent(h->s_dense, h->ev_fork, 0));
+    H2_CUDA(h, cudaStreamWaitEvent(s_dense, h->ev_fork, 0));
     if (L.P > 1) {
         H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_fork, 0));
         H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_h0, h->nseg_h, (const T *)nullptr, 0, args, (T *)h->hsend, nv, h->s_comm));
@@ -1040,29 +1128,35 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
         }
         H2_NCCL(h, g_nccl.GroupEnd());
         H2_CUDA(h, cudaEventRecord(h->ev_halo, h->s_comm));
-        H2_CUDA(h, cudaStreamWaitEvent(h->s_dense, h->ev_halo, 0));
+        H2_CUDA(h, cudaStreamWaitEvent(s_dense, h->ev_halo, 0));
     }
-    if ((rc = mark(h, 9, h->s_dense)) != H2_OK) return rc;
-    H2_CUDA(h, launch_dense<T>(T0(h->dense), h->dense.n, h->d_blks, args, (const T *)h->hrecv, nv, L.m, h->s_dense));
-    if ((rc = mark(h, 10, h->s_dense)) != H2_OK) return rc;
-    H2_CUDA(h, cudaEventRecord(h->ev_dense, h->s_dense));
+    if ((rc = mark(h, 9, s_dense)) != H2_OK) return rc;
+    H2_CUDA(h, launch_dense<T>(T0(h->dense), h->dense.n, h->d_blks, args, (const T *)h->hrecv, nv, h->dense.r, h->tma_on(nv), h->bw_ctas, s_dense));
+    if ((rc = mark(h, 10, s_dense)) != H2_OK) return rc;
+    H2_CUDA(h, cudaEventRecord(h->ev_dense, s_dense));
+    H2_MARK(0);
     // 1. upsweep of the local branch (PAPER.md:281 / alg:upsweep2)
     H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
                                  h->up_leaf.r, st));
-    H2_MARK(1);
     // 1b. leaf-level coupling (diagonal part) as soon as x^ of the leaves exists (alg:mult's
     //     levels are independent), on its own stream
     H2_CUDA(h, cudaEventRecord(h->ev_upleaf, st));
-    H2_CUDA(h, cudaStreamWaitEvent(h->s_leafc, h->ev_upleaf, 0));
-    if ((rc = mark(h, 11, h->s_leafc)) != H2_OK) return rc;
+    H2_CUDA(h, cudaStreamWaitEvent(s_leafc, h->ev_upleaf, 0));
+    if ((rc = mark(h, 11, s_leafc)) != H2_OK) return rc;
     for (const Phase &ph : h->coup_leaf)
         H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
-                                  nv, ph.r, h->s_leafc));
-    if ((rc = mark(h, 12, h->s_leafc)) != H2_OK) return rc;
-    H2_CUDA(h, cudaEventRecord(h->ev_leafc, h->s_leafc));
-    for (const auto &sg : h->up_stages)
-        H2_CUDA(h, launch_tree<T>(MODE_WRITE, sg.st, sg.nctas, h->d_tasks, h->d_blks, xh, h->xh_plane, nv,
-                                  sg.r, st));
+                                  nv, ph.r, h->tma_on(nv), h->bw_ctas, s_leafc));
+    if ((rc = mark(h, 12, s_leafc)) != H2_OK) return rc;
+    H2_CUDA(h, cudaEventRecord(h->ev_leafc, s_leafc));
+    H2_MARK(1);
+    if (h->use_chain)
+        H2_CUDA(h, launch_chain<T>(MODE_WRITE, h->d_tasks + h->up_c0, h->d_deps, h->up_cn, h->d_blks, xh,
+                                   h->xh_plane, nv, h->up_cr, h->d_flags, (CallArgs<T> *)h->dargs, 0,
+                                   h->chain_ctas, st));
+    else
+        for (const auto &sg : h->up_stages)
+            H2_CUDA(h, launch_tree<T>(MODE_WRITE, sg.st, sg.nctas, h->d_tasks, h->d_blks, xh, h->xh_plane, nv,
+                                      sg.r, st));
     H2_MARK(2);
     // 2. exchange (P > 1): pack my x^ nodes that peers need, one NCCL group on the comm stream,
     //    overlapped with the diagonal multiply (alg:optimized_dist_mult)
@@ -1096,7 +1190,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     // 3. coupling multiply, diagonal part (all levels) (alg:mult)
     for (const Phase &ph : h->coup_diag)
         H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
-                                  nv, ph.r, st));
+                                  nv, ph.r, h->tma_on(nv), 0, st));
     H2_MARK(4);
     // 4. off-diagonal part after the exchange (waitAll, alg:optimized_dist_mult line 11-12);
     //    it accumulates into leaf-level rows too, so the leaf coupling stream joins first
@@ -1106,14 +1200,19 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
         for (int ci = 0; ci < 3; ++ci) {
             const Phase &ph = h->coup_off[ci];
             H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(ph), ph.n, h->d_blks, (const T *)h->xrecv, 0, yh,
-                                      h->yh_plane, nv, ph.r, st));
+                                      h->yh_plane, nv, ph.r, h->tma_on(nv), 0, st));
         }
     }
     H2_MARK(5);
     // 5. downsweep transfers (alg:downsweep)
-    for (const auto &sg : h->down_stages)
-        H2_CUDA(h, launch_tree<T>(MODE_ACCUM, sg.st, sg.nctas, h->d_tasks, h->d_blks, yh, h->yh_plane, nv,
-                                  sg.r, st));
+    if (h->use_chain)
+        H2_CUDA(h, launch_chain<T>(MODE_ACCUM, h->d_tasks + h->dn_c0, h->d_deps + h->up_cn, h->dn_cn, h->d_blks,
+                                   yh, h->yh_plane, nv, h->dn_cr, h->d_flags + h->nflags, (CallArgs<T> *)h->dargs, 1,
+                                   h->chain_ctas, st));
+    else
+        for (const auto &sg : h->down_stages)
+            H2_CUDA(h, launch_tree<T>(MODE_ACCUM, sg.st, sg.nctas, h->d_tasks, h->d_blks, yh, h->yh_plane, nv,
+                                      sg.r, st));
     H2_MARK(6);
     // 6. leaves: last transfer + U expansion added into Y after the dense and leaf-coupling
     //    streams joined
@@ -1254,8 +1353,8 @@ extern "C" int h2_phase_times(h2_handle h, double ms[H2_NPHASE + 1], int64_t *nc
     for (int i = 0; i <= H2_NPHASE; ++i) ms[i] = 0;
     int64_t calls = h->ev_used / NEV;
     // phase -> (start event, end event) of a call; see enqueue()
-    static const int span[H2_NPHASE + 1][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6},
-                                               {7, 8}, {9, 10}, {11, 12}, {0, 8}};
+    static const int span[H2_NPHASE + 1][2] = {{0, 11}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6},
+                                               {7, 8}, {9, 10}, {11, 12}, {9, 8}};
     if (calls) {
         H2_CUDA(h, cudaDeviceSynchronize());
         for (int64_t c = 0; c < calls; ++c) {

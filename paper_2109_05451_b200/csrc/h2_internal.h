@@ -58,7 +58,19 @@ struct CallArgs {
     T *Y;
     int64_t ldx, ldy;
     T alpha, beta;
+    int32_t epoch;           // call counter: completion flags of the chain kernels hold it
+    uint32_t ticket[4];      // work tickets of the chain kernels (reset every call)
 };
+
+// Dependencies of one chain task (k_chain): it may start once flags[dep0] and flags[dep1]
+// (-1 = none) equal the call's epoch; on completion it sets flags[self].
+struct ChainDep {
+    int32_t self, dep0, dep1, pad;
+};
+template <typename T>
+cudaError_t launch_chain(int mode, const Task *t, const ChainDep *deps, int ntask, const Blk *b, T *buf,
+                         int64_t ld, int nv, int r, int32_t *flags, CallArgs<T> *args, int which,
+                         int max_ctas, cudaStream_t s);
 
 template <typename T>
 cudaError_t launch_set_args(CallArgs<T> *a, const T *X, int64_t ldx, T *Y, int64_t ldy, T alpha, T beta,
@@ -67,15 +79,19 @@ cudaError_t launch_set_args(CallArgs<T> *a, const T *X, int64_t ldx, T *Y, int64
 template <typename T>
 cudaError_t launch_up_leaf(const Task *t, int ntask, const Blk *b, const CallArgs<T> *args,
                            T *xh, int64_t xh_ld, int nv, int r, cudaStream_t s);
+// tma: stream contiguous block runs through the cp.async.bulk ring (else register loads)
+// max_ctas > 0: cap the grid (tasks are grid-strided): persistent bandwidth kernels that leave
+// SM room for the latency-bound tree chain running concurrently
 template <typename T>
 cudaError_t launch_rows(int mode, const Task *t, int ntask, const Blk *b, const T *src,
-                        int64_t src_ld, T *dst, int64_t dst_ld, int nv, int r, cudaStream_t s);
+                        int64_t src_ld, T *dst, int64_t dst_ld, int nv, int r, bool tma, int max_ctas,
+                        cudaStream_t s);
 template <typename T>
 cudaError_t launch_leaf_u(const Task *t, int ntask, const Blk *b, const T *yh, int64_t yh_ld,
                           const CallArgs<T> *args, int nv, int k, int kp, int m, cudaStream_t s);
 template <typename T>
 cudaError_t launch_dense(const Task *t, int ntask, const Blk *b, const CallArgs<T> *args, const T *halo,
-                         int nv, int m, cudaStream_t s);
+                         int nv, int m, bool tma, int max_ctas, cudaStream_t s);
 template <typename T>
 cudaError_t launch_scale(T *Y, int64_t ldy, int64_t n, int nv, T beta, cudaStream_t s);
 template <typename T>

@@ -273,7 +273,8 @@ __device__ __forceinline__ void mma_stream(MmaAcc<MT, NT> &acc, const double *__
         while (j >= c) { j -= c; ++bb; }
         MmaDesc d = ds[min(bb, nb - 1)];
         const int ksn = (K + 3) >> 2;
-#pragma unroll 2
+        // deeper unroll (more loads in flight) when the accumulator leaves registers for it
+#pragma unroll (MT <= 4 ? 4 : 2)
         for (int ks = 0; ks < ksn; ++ks) {
             const int col = ks * 4 + t;
             double a[MT], b[NT];
@@ -297,6 +298,279 @@ __device__ __forceinline__ void mma_stream(MmaAcc<MT, NT> &acc, const double *__
                 d = ds[min(bb, nb - 1)];
             }
         }
+    }
+}
+
+// =========================================================================== TMA-bulk row stream
+// The contiguous A run of a task (coupling row, dense leaf row) is pulled into a warp-private
+// shared-memory ring by cp.async.bulk (SASS UBLKCP) completing on mbarriers: the loads are
+// asynchronous and independent of registers, so a few warps keep the HBM pipe full.  The ring is
+// a circular buffer of the byte stream (RING bytes, NST stages of STB bytes); element e of the
+// run sits at ring[(shift + e * esz) & (RING - 1)].  The consumer of chunk c processes every
+// column whose last byte lies in chunk c (chunk c-1 is still resident), then releases chunk c-1
+// and issues chunk c + NST - 1 into its stage.
+constexpr int TMA_STB = 4096;
+constexpr int TMA_NST = 4;
+constexpr int TMA_RING = TMA_STB * TMA_NST;
+
+struct TmaRing {
+    unsigned char *ring;     // TMA_RING bytes, 128-byte aligned
+    uint64_t *mbar;          // TMA_NST mbarriers
+    uint32_t seq;            // running chunk sequence number (warp-uniform)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async()
+{
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// one warp-private ring (called once per warp at kernel start)
+__device__ __forceinline__ TmaRing ring_init(unsigned char *base, int lane)
+{
+    TmaRing r;
+    r.ring = base;
+    r.mbar = reinterpret_cast<uint64_t *>(base + TMA_RING);
+    r.seq = 0;
+    if (lane == 0) {
+        for (int i = 0; i < TMA_NST; ++i) mbar_init(&r.mbar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        fence_proxy_async();
+    }
+    __syncwarp();
+    return r;
+}
+
+// geometry of one contiguous byte run [a0, a0 + nbytes) in the ring
+struct RunGeo {
+    const unsigned char *g0;   // a0 rounded down to 16
+    uint32_t shift;            // a0 - g0
+    int64_t bulk;              // bytes copied by bulk copies: floor16(a0 + nbytes) - g0
+    uint32_t tail;             // remaining bytes (< 16) copied by lane 0
+    int nch;                   // chunks
+};
+
+__device__ __forceinline__ RunGeo run_geo(const void *a0, int64_t nbytes)
+{
+    RunGeo gq;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(a0);
+    const uintptr_t g0 = a & ~uintptr_t(15), e = a + nbytes, eb = e & ~uintptr_t(15);
+    gq.g0 = reinterpret_cast<const unsigned char *>(g0);
+    gq.shift = (uint32_t)(a - g0);
+    gq.bulk = (int64_t)(eb - g0);
+    gq.tail = (uint32_t)(e - eb);
+    const int64_t span = (int64_t)(e - g0);
+    gq.nch = (int)((span + TMA_STB - 1) / TMA_STB);
+    return gq;
+}
+
+// lane 0: issue chunk ci of the run into stage (seq + ci) % NST
+__device__ __forceinline__ void ring_issue(TmaRing &rg, const RunGeo &gq, int ci, int lane)
+{
+    if (lane != 0 || ci >= gq.nch) return;
+    const uint32_t st = (rg.seq + ci) % TMA_NST;
+    const int64_t off = (int64_t)ci * TMA_STB;
+    const int64_t bytes = gq.bulk - off < TMA_STB ? gq.bulk - off : TMA_STB;
+    unsigned char *dst = rg.ring + st * TMA_STB;
+    if (gq.tail && gq.bulk >= off && gq.bulk < off + TMA_STB) {
+        // the (< 16 byte) tail after the last 16-byte boundary: plain copy, made visible by the
+        // release semantics of the mbarrier arrive below
+        const int64_t toff = gq.bulk - off;
+        for (uint32_t b = 0; b < gq.tail; b += 4)
+            *reinterpret_cast<uint32_t *>(dst + toff + b) = *reinterpret_cast<const uint32_t *>(gq.g0 + gq.bulk + b);
+    }
+    if (bytes > 0) {
+        mbar_expect_tx(&rg.mbar[st], (uint32_t)bytes);
+        bulk_g2s(dst, gq.g0 + off, (uint32_t)bytes, &rg.mbar[st]);
+    } else {
+        mbar_expect_tx(&rg.mbar[st], 0);
+    }
+}
+
+__device__ __forceinline__ void ring_wait(TmaRing &rg, int ci)
+{
+    const uint32_t q = rg.seq + ci;
+    mbar_wait(&rg.mbar[q % TMA_NST], (q / TMA_NST) & 1);
+}
+
+template <typename T>
+__device__ __forceinline__ T ring_ld(const TmaRing &rg, uint32_t byte_pos)
+{
+    return *reinterpret_cast<const T *>(rg.ring + (byte_pos & (TMA_RING - 1)));
+}
+
+// Simt consumer: acc += A_run (r x K) * xs (K x nvc, smem, ld K)
+template <typename T, int RPL, int NVB>
+__device__ __forceinline__ void simt_tma_run(SimtAcc<T, RPL, NVB> &acc, TmaRing &rg, const T *A0, int r, int K,
+                                             const T *xs, int lane)
+{
+    const RunGeo gq = run_geo(A0, (int64_t)K * r * sizeof(T));
+    for (int ci = 0; ci < TMA_NST - 1; ++ci) ring_issue(rg, gq, ci, lane);
+    const int colb = r * (int)sizeof(T);
+    // chunk ci lives in stage (seq + ci) % NST: ring byte of run byte p = base + p (mod RING)
+    const uint32_t base = (rg.seq % TMA_NST) * TMA_STB + gq.shift;
+    int J = 0;
+    for (int ci = 0; ci < gq.nch; ++ci) {
+        ring_wait(rg, ci);
+        int64_t lim = ((int64_t)(ci + 1) * TMA_STB - gq.shift) / colb;
+        const int J1 = (ci == gq.nch - 1 || lim > K) ? K : (int)lim;
+#pragma unroll 8
+        for (; J < J1; ++J) {
+            const uint32_t pos0 = base + (uint32_t)J * colb;
+            T a[RPL];
+#pragma unroll
+            for (int ri = 0; ri < RPL; ++ri) {
+                const int i = lane + 32 * ri;
+                a[ri] = (i < r) ? ring_ld<T>(rg, pos0 + i * (uint32_t)sizeof(T)) : T(0);
+            }
+#pragma unroll
+            for (int n = 0; n < NVB; ++n) {
+                const T xv = xs[J + n * K];
+#pragma unroll
+                for (int ri = 0; ri < RPL; ++ri) acc.v[ri][n] = fma(a[ri], xv, acc.v[ri][n]);
+            }
+        }
+        __syncwarp();
+        fence_proxy_async();
+        ring_issue(rg, gq, ci + TMA_NST - 1, lane);
+    }
+    rg.seq += gq.nch;
+}
+
+template <typename T, int RPL, int NVB>
+__device__ __forceinline__ void simt_tma_stream(SimtAcc<T, RPL, NVB> &acc, const T *__restrict__ A0, int r,
+                                                int c, int nblk, const Blk *__restrict__ blks,
+                                                const Src<T> &src, int nvc, int lane, TmaRing &rg, T *xs,
+                                                int xcap)
+{
+    int per = xcap / (c * NVB);
+    per = per < 1 ? 1 : (per > 32 ? 32 : per);
+    for (int b0 = 0; b0 < nblk; b0 += per) {
+        const int nb = min(per, nblk - b0);
+        const int K = nb * c;
+        int64_t xo = 0;
+        int xr = 0, xl = 0;
+        if (lane < nb) {
+            const Blk b = blks[b0 + lane];
+            xo = b.x; xr = b.xrows; xl = b.xld;
+        }
+        __syncwarp();
+        for (int e0 = 0; e0 < K; e0 += 32) {
+            const int e = e0 + lane;
+            const int bb = min(e / c, nb - 1), j = e - bb * c;
+            const int64_t bxo = __shfl_sync(FULL, xo, bb);
+            const int bxr = __shfl_sync(FULL, xr, bb), bxl = __shfl_sync(FULL, xl, bb);
+            if (e < K) {
+                int64_t ld;
+                const T *p = resolve(src, bxo, bxl, ld);
+#pragma unroll
+                for (int n = 0; n < NVB; ++n) xs[e + n * K] = (j < bxr && n < nvc) ? p[j + n * ld] : T(0);
+            }
+        }
+        __syncwarp();
+        simt_tma_run<T, RPL, NVB>(acc, rg, A0 + (int64_t)b0 * r * c, r, K, xs, lane);
+        __syncwarp();
+    }
+}
+
+// DMMA consumer over the TMA ring: A fragments from shared memory, B from the x sources
+template <int MT, int NT>
+__device__ __forceinline__ void mma_tma_stream(MmaAcc<MT, NT> &acc, const double *__restrict__ A0, int r, int c,
+                                               int nblk, const Blk *__restrict__ blks, const Src<double> &src,
+                                               int nvc, int lane, TmaRing &rg, MmaDesc *ds)
+{
+    const int g = lane >> 2, t = lane & 3;
+    for (int b0 = 0; b0 < nblk; b0 += 32) {
+        const int nb = min(32, nblk - b0);
+        const int K = nb * c;
+        __syncwarp();
+        if (lane < nb) {
+            const Blk b = blks[b0 + lane];
+            int64_t ld;
+            const double *p = resolve(src, b.x, b.xld, ld);
+            ds[lane] = MmaDesc{p, ld, b.xrows, 0};
+        }
+        __syncwarp();
+        const double *A = A0 + (int64_t)b0 * r * c;
+        const RunGeo gq = run_geo(A, (int64_t)K * r * 8);
+        for (int ci = 0; ci < TMA_NST - 1; ++ci) ring_issue(rg, gq, ci, lane);
+        int bb = 0, j = t;
+        while (j >= c) { j -= c; ++bb; }
+        MmaDesc d = ds[min(bb, nb - 1)];
+        const int ksn = (K + 3) >> 2;
+        const int colb = r * 8;
+        const uint32_t base = (rg.seq % TMA_NST) * TMA_STB + gq.shift;   // see simt_tma_run
+        int ks = 0;
+        for (int ci = 0; ci < gq.nch; ++ci) {
+            ring_wait(rg, ci);
+            // k-steps whose last column ends in chunk ci
+            const int64_t lim = ((int64_t)(ci + 1) * TMA_STB - gq.shift) / colb;   // full columns
+            const int ks1 = (ci == gq.nch - 1 || lim >= K) ? ksn : (int)(lim >> 2);
+#pragma unroll 2
+            for (; ks < ks1; ++ks) {
+                const int col = ks * 4 + t;
+                double a[MT], b[NT];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const int row = mt * 8 + g;
+                    a[mt] = (row < r && col < K) ? ring_ld<double>(rg, base + (uint32_t)(col * r + row) * 8u) : 0.0;
+                }
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const int n = nt * 8 + g;
+                    b[nt] = (col < K && j < d.xrows && n < nvc) ? d.p[j + n * d.ld] : 0.0;
+                }
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a[mt], b[nt]);
+                j += 4;
+                if (j >= c) {
+                    do { j -= c; ++bb; } while (j >= c);
+                    d = ds[min(bb, nb - 1)];
+                }
+            }
+            __syncwarp();
+            fence_proxy_async();
+            ring_issue(rg, gq, ci + TMA_NST - 1, lane);
+        }
+        rg.seq += gq.nch;
     }
 }
 
@@ -333,6 +607,10 @@ struct Simt {
     __device__ static void stream(Acc &acc, const T *A0, int r, int c, int nblk, const Blk *blks,
                                   const Src<T> &src, int nvc, int lane, void *scratch)
     { simt_stream<T, RPL, NVB>(acc, A0, r, c, nblk, blks, src, nvc, lane, (T *)scratch, XCAP_BYTES / (int)sizeof(T)); }
+    static constexpr int TSCRATCH = XCAP_BYTES;     // per-warp smem next to the TMA ring
+    __device__ static void tstream(Acc &acc, const T *A0, int r, int c, int nblk, const Blk *blks,
+                                   const Src<T> &src, int nvc, int lane, TmaRing &rg, void *scratch)
+    { simt_tma_stream<T, RPL, NVB>(acc, A0, r, c, nblk, blks, src, nvc, lane, rg, (T *)scratch, XCAP_BYTES / (int)sizeof(T)); }
 };
 
 template <int MT, int NT>
@@ -346,7 +624,14 @@ struct Mma {
     __device__ static void stream(Acc &acc, const double *A0, int r, int c, int nblk, const Blk *blks,
                                   const Src<double> &src, int nvc, int lane, void *scratch)
     { mma_stream<MT, NT>(acc, A0, r, c, nblk, blks, src, nvc, lane, (MmaDesc *)scratch); }
+    static constexpr int TSCRATCH = 32 * sizeof(MmaDesc);
+    __device__ static void tstream(Acc &acc, const double *A0, int r, int c, int nblk, const Blk *blks,
+                                   const Src<double> &src, int nvc, int lane, TmaRing &rg, void *scratch)
+    { mma_tma_stream<MT, NT>(acc, A0, r, c, nblk, blks, src, nvc, lane, rg, (MmaDesc *)scratch); }
 };
+
+template <typename Eng>
+__host__ __device__ constexpr int warp_tma_bytes() { return TMA_RING + 128 + Eng::TSCRATCH; }
 
 // ---------------------------------------------------------------------------------------
 // Upsweep leaves: x^_s (k x nv) = Vt_s (k x m) x_s (m x nv), Vt = V^T re-laid out at create.
@@ -376,16 +661,20 @@ k_up_leaf(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blk
 // Generic row tasks whose x operands and output live in the x^/y^ workspaces:
 //   MODE_WRITE  out  = sum_b A_b x_b    (upsweep transfers, coupling multiply)
 //   MODE_ACCUM  out += sum_b A_b x_b    (downsweep transfers, off-diagonal coupling pass)
-template <typename T, typename Eng, int MODE>
+template <typename T, typename Eng, int MODE, bool TMA>
 __global__ void __launch_bounds__(WPB * 32, 2)
 k_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
        const T *__restrict__ src, int64_t src_ld, T *__restrict__ dst, int64_t dst_ld, int nv)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int task = blockIdx.x * WPB + wid;
-    if (task >= ntask) return;
-    void *scratch = smem_raw + wid * Eng::SCRATCH;
+    if (blockIdx.x * WPB + wid >= ntask) return;
+    unsigned char *wsm = smem_raw + (size_t)wid * (TMA ? warp_tma_bytes<Eng>() : Eng::SCRATCH);
+    TmaRing rg{};
+    if (TMA) rg = ring_init(wsm, lane);
+    void *scratch = TMA ? (void *)(wsm + TMA_RING + 128) : (void *)wsm;
+    // grid-stride over tasks (the launcher may cap the grid: persistent bandwidth kernels)
+    for (int task = blockIdx.x * WPB + wid; task < ntask; task += gridDim.x * WPB) {
     const Task tk = tasks[task];
     for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
         const int nvc = min(Eng::NV, nv - n0);
@@ -395,8 +684,12 @@ k_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
         if ((tk.flags & TF_ACONTIG) && tk.nblk > 0) {
             const Blk b0 = blks[tk.blk0];
             const Src<T> sr{src, src_ld, nullptr, n0};
-            Eng::stream(acc, static_cast<const T *>(b0.A), tk.r, tk.c, tk.nblk, blks + tk.blk0, sr, nvc,
-                        lane, scratch);
+            if (TMA)
+                Eng::tstream(acc, static_cast<const T *>(b0.A), tk.r, tk.c, tk.nblk, blks + tk.blk0, sr, nvc,
+                             lane, rg, scratch);
+            else
+                Eng::stream(acc, static_cast<const T *>(b0.A), tk.r, tk.c, tk.nblk, blks + tk.blk0, sr, nvc,
+                            lane, scratch);
             acc_store(acc, dst + tk.out + (int64_t)n0 * dst_ld, dst_ld, tk.r, nvc, lane);
             continue;
         }
@@ -407,6 +700,7 @@ k_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
                        b.xrows, nvc, lane);
         }
         acc_store(acc, dst + tk.out + (int64_t)n0 * dst_ld, dst_ld, tk.r, nvc, lane);
+    }
     }
 }
 
@@ -420,7 +714,7 @@ __global__ void __launch_bounds__(WPB * 32, 2)
 k_tree(TreeStage st, const Task *__restrict__ tasks, const Blk *__restrict__ blks, T *__restrict__ buf,
        int64_t ld, int nv)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     void *scratch = smem_raw + wid * Eng::SCRATCH;
     for (int lv = 0; lv < st.nlev; ++lv) {
@@ -454,6 +748,76 @@ k_tree(TreeStage st, const Task *__restrict__ tasks, const Blk *__restrict__ blk
 }
 
 // ---------------------------------------------------------------------------------------
+// Dependency-driven tree sweep in ONE launch (upsweep transfers bottom-up, or downsweep transfers
+// top-down): warps take tasks in topological order from an atomic
+// ticket, wait until the task's tree neighbours (children for the upsweep, the parent for the
+// downsweep) have published this call's epoch in their completion flags, compute, and publish
+// their own flag.  A parent starts as soon as its own children are done -- no per-level launch
+// or grid barrier.  Tickets are handed out in order and every dependency has a smaller ticket
+// held by a running warp, so the waits cannot deadlock.
+__device__ __forceinline__ int ld_acquire(const int32_t *p)
+{
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(int32_t *p, int v)
+{
+    asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+template <typename T, typename Eng, int MODE>
+__global__ void __launch_bounds__(WPB * 32, 2)
+k_chain(const Task *__restrict__ tasks, const ChainDep *__restrict__ deps, int ntask,
+        const Blk *__restrict__ blks, T *__restrict__ buf, int64_t ld, int nv, int32_t *flags,
+        CallArgs<T> *args, int which)
+{
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    void *scratch = smem_raw + wid * Eng::SCRATCH;
+    const int epoch = *((volatile int32_t *)&args->epoch);
+    unsigned *ticket = &args->ticket[which];
+    for (;;) {
+        int t = 0;
+        if (lane == 0) t = (int)atomicAdd(ticket, 1u);
+        t = __shfl_sync(FULL, t, 0);
+        if (t >= ntask) break;
+        const ChainDep dp = deps[t];
+        if (lane == 0) {
+            if (dp.dep0 >= 0) while (ld_acquire(flags + dp.dep0) != epoch) __nanosleep(20);
+            if (dp.dep1 >= 0) while (ld_acquire(flags + dp.dep1) != epoch) __nanosleep(20);
+            __threadfence();           // (CCTL.IVALL) no stale L1 lines of the producers' outputs
+        }
+        __syncwarp();
+        const Task tk = tasks[t];
+        for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
+            const int nvc = min(Eng::NV, nv - n0);
+            typename Eng::Acc acc;
+            if (MODE == MODE_ACCUM) acc_load(acc, buf + tk.out + (int64_t)n0 * ld, ld, tk.r, nvc, lane);
+            else acc_zero(acc, lane);
+            if (tk.flags & TF_ACONTIG) {
+                const Src<T> sr{buf, ld, nullptr, n0};
+                Eng::stream(acc, static_cast<const T *>(blks[tk.blk0].A), tk.r, tk.c, tk.nblk, blks + tk.blk0,
+                            sr, nvc, lane, scratch);
+            } else {
+                for (int bi = 0; bi < tk.nblk; ++bi) {
+                    const Blk b = blks[tk.blk0 + bi];
+                    Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.c, buf + b.x + (int64_t)n0 * ld, ld,
+                               b.xrows, nvc, lane);
+                }
+            }
+            acc_store(acc, buf + tk.out + (int64_t)n0 * ld, ld, tk.r, nvc, lane);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            st_release(flags + dp.self, epoch);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
 // Leaf kernel: last downsweep transfer + leaf expansion, added into Y:
 //   z_t = y^_t + E_t y^_parent ;  Y_t += alpha U_t z_t
 // blocks: [E_t (if TF_HAS_E), x = parent y^ offset] [U_t, x = own y^ offset].  k_dense has
@@ -470,7 +834,7 @@ k_leaf_u(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks
     const T alpha = args->alpha;
     static_assert(EngK::NV == EngM::NV, "engines must agree on the vector chunk");
     constexpr int NV = EngM::NV;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int task = blockIdx.x * WPB + wid;
     if (task >= ntask) return;
@@ -508,7 +872,7 @@ k_leaf_u(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks
 // Dense near field + epilogue (reading R12), on its own low-priority stream
 // concurrent with the tree phases:  Y_t = alpha sum_s D_ts x_s + beta Y_t  (beta == 0: Y is
 // write-only).  Every leaf has a task (rows without dense blocks still apply beta).
-template <typename T, typename Eng>
+template <typename T, typename Eng, bool TMA>
 __global__ void __launch_bounds__(WPB * 32, 2)
 k_dense(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
         const CallArgs<T> *__restrict__ args, const T *__restrict__ halo, int nv)
@@ -517,11 +881,14 @@ k_dense(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
     T *__restrict__ Y = args->Y;
     const int64_t ldx = args->ldx, ldy = args->ldy;
     const T alpha = args->alpha, beta = args->beta;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int task = blockIdx.x * WPB + wid;
-    if (task >= ntask) return;
-    void *scratch = smem_raw + wid * Eng::SCRATCH;
+    if (blockIdx.x * WPB + wid >= ntask) return;
+    unsigned char *wsm = smem_raw + (size_t)wid * (TMA ? warp_tma_bytes<Eng>() : Eng::SCRATCH);
+    TmaRing rg{};
+    if (TMA) rg = ring_init(wsm, lane);
+    void *scratch = TMA ? (void *)(wsm + TMA_RING + 128) : (void *)wsm;
+    for (int task = blockIdx.x * WPB + wid; task < ntask; task += gridDim.x * WPB) {
     const Task tk = tasks[task];
     for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
         const int nvc = min(Eng::NV, nv - n0);
@@ -529,8 +896,12 @@ k_dense(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
         acc_zero(acc, lane);
         if ((tk.flags & TF_ACONTIG) && tk.nblk > 0) {
             const Src<T> sr{X, ldx, halo, n0};
-            Eng::stream(acc, static_cast<const T *>(blks[tk.blk0].A), tk.r, tk.r, tk.nblk, blks + tk.blk0,
-                        sr, nvc, lane, scratch);
+            if (TMA)
+                Eng::tstream(acc, static_cast<const T *>(blks[tk.blk0].A), tk.r, tk.c, tk.nblk, blks + tk.blk0,
+                             sr, nvc, lane, rg, scratch);
+            else
+                Eng::stream(acc, static_cast<const T *>(blks[tk.blk0].A), tk.r, tk.c, tk.nblk, blks + tk.blk0,
+                            sr, nvc, lane, scratch);
         } else {
             for (int bi = 0; bi < tk.nblk; ++bi) {
                 const Blk b = blks[tk.blk0 + bi];
@@ -538,7 +909,7 @@ k_dense(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
                 int64_t ld;
                 if (b.x >= 0) { src = X + b.x; ld = ldx; }
                 else          { src = halo + (-b.x - 1); ld = b.xld; }
-                Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.r, src + (int64_t)n0 * ld, ld,
+                Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.c, src + (int64_t)n0 * ld, ld,
                            b.xrows, nvc, lane);
             }
         }
@@ -551,12 +922,15 @@ k_dense(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
             }
         });
     }
+    }
 }
 
 template <typename T>
 __global__ void k_set_args(CallArgs<T> *a, const T *X, int64_t ldx, T *Y, int64_t ldy, T alpha, T beta)
 {
     a->X = X; a->ldx = ldx; a->Y = Y; a->ldy = ldy; a->alpha = alpha; a->beta = beta;
+    a->epoch = a->epoch + 1;
+    for (int i = 0; i < 4; ++i) a->ticket[i] = 0;
 }
 
 template <typename T>
@@ -679,19 +1053,31 @@ cudaError_t launch_up_leaf(const Task *t, int ntask, const Blk *b, const CallArg
     return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t launch_rows(int mode, const Task *t, int ntask, const Blk *b, const T *src,
-                        int64_t src_ld, T *dst, int64_t dst_ld, int nv, int r, cudaStream_t s)
+template <typename T, bool TMA>
+cudaError_t launch_rows_t(int mode, const Task *t, int ntask, const Blk *b, const T *src,
+                          int64_t src_ld, T *dst, int64_t dst_ld, int nv, int r, int max_ctas, cudaStream_t s)
 {
     if (ntask == 0) return cudaSuccess;
+    cudaError_t err = cudaSuccess;
     Dispatch<T>::run(r, nv, [&](auto e) {
         using E = decltype(e);
-        const size_t sm = (size_t)WPB * E::SCRATCH;
+        const size_t sm = (size_t)WPB * (TMA ? warp_tma_bytes<E>() : E::SCRATCH);
+        auto kw = k_rows<T, E, MODE_WRITE, TMA>;
+        auto ka = k_rows<T, E, MODE_ACCUM, TMA>;
+        static bool attr_set = false;
+        if (!attr_set) {
+            err = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (err == cudaSuccess) err = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            attr_set = (err == cudaSuccess);
+        }
+        if (err != cudaSuccess) return;
+        const int grid = max_ctas > 0 ? min(grid_for(ntask), max_ctas) : grid_for(ntask);
         if (mode == MODE_WRITE)
-            k_rows<T, E, MODE_WRITE><<<grid_for(ntask), WPB * 32, sm, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv);
+            kw<<<grid, WPB * 32, sm, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv);
         else
-            k_rows<T, E, MODE_ACCUM><<<grid_for(ntask), WPB * 32, sm, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv);
+            ka<<<grid, WPB * 32, sm, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv);
     });
+    if (err != cudaSuccess) return err;
     return cudaGetLastError();
 }
 
@@ -736,15 +1122,59 @@ cudaError_t launch_leaf_u(const Task *t, int ntask, const Blk *b, const T *yh, i
     return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t launch_dense(const Task *t, int ntask, const Blk *b, const CallArgs<T> *args, const T *halo,
-                         int nv, int m, cudaStream_t s)
+template <typename T, bool TMA>
+cudaError_t launch_dense_t(const Task *t, int ntask, const Blk *b, const CallArgs<T> *args, const T *halo,
+                           int nv, int m, int max_ctas, cudaStream_t s)
 {
     if (ntask == 0) return cudaSuccess;
+    cudaError_t err = cudaSuccess;
     Dispatch<T>::run(m, nv, [&](auto e) {
         using E = decltype(e);
+        const size_t sm = (size_t)WPB * (TMA ? warp_tma_bytes<E>() : E::SCRATCH);
+        auto kd = k_dense<T, E, TMA>;
+        static bool attr_set = false;
+        if (!attr_set) {
+            err = cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            attr_set = (err == cudaSuccess);
+        }
+        if (err != cudaSuccess) return;
+        const int grid = max_ctas > 0 ? min(grid_for(ntask), max_ctas) : grid_for(ntask);
+        kd<<<grid, WPB * 32, sm, s>>>(t, ntask, b, args, halo, nv);
+    });
+    if (err != cudaSuccess) return err;
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_rows(int mode, const Task *t, int ntask, const Blk *b, const T *src, int64_t src_ld, T *dst,
+                        int64_t dst_ld, int nv, int r, bool tma, int max_ctas, cudaStream_t s)
+{
+    return tma ? launch_rows_t<T, true>(mode, t, ntask, b, src, src_ld, dst, dst_ld, nv, r, max_ctas, s)
+               : launch_rows_t<T, false>(mode, t, ntask, b, src, src_ld, dst, dst_ld, nv, r, max_ctas, s);
+}
+
+template <typename T>
+cudaError_t launch_dense(const Task *t, int ntask, const Blk *b, const CallArgs<T> *args, const T *halo,
+                         int nv, int m, bool tma, int max_ctas, cudaStream_t s)
+{
+    return tma ? launch_dense_t<T, true>(t, ntask, b, args, halo, nv, m, max_ctas, s)
+               : launch_dense_t<T, false>(t, ntask, b, args, halo, nv, m, max_ctas, s);
+}
+
+template <typename T>
+cudaError_t launch_chain(int mode, const Task *t, const ChainDep *deps, int ntask, const Blk *b, T *buf,
+                         int64_t ld, int nv, int r, int32_t *flags, CallArgs<T> *args, int which,
+                         int max_ctas, cudaStream_t s)
+{
+    if (ntask == 0) return cudaSuccess;
+    Dispatch<T>::run(r, nv, [&](auto e) {
+        using E = decltype(e);
         const size_t sm = (size_t)WPB * E::SCRATCH;
-        k_dense<T, E><<<grid_for(ntask), WPB * 32, sm, s>>>(t, ntask, b, args, halo, nv);
+        const int grid = max_ctas > 0 ? min(grid_for(ntask), max_ctas) : grid_for(ntask);
+        if (mode == MODE_WRITE)
+            k_chain<T, E, MODE_WRITE><<<grid, WPB * 32, sm, s>>>(t, deps, ntask, b, buf, ld, nv, flags, args, which);
+        else
+            k_chain<T, E, MODE_ACCUM><<<grid, WPB * 32, sm, s>>>(t, deps, ntask, b, buf, ld, nv, flags, args, which);
     });
     return cudaGetLastError();
 }
@@ -781,12 +1211,15 @@ cudaError_t launch_pack(const PackSeg *segs, int64_t nseg, const T *src, int64_t
     template cudaError_t launch_up_leaf<T>(const Task *, int, const Blk *, const CallArgs<T> *, \
                                            T *, int64_t, int, int, cudaStream_t);              \
     template cudaError_t launch_rows<T>(int, const Task *, int, const Blk *, const T *,        \
-                                        int64_t, T *, int64_t, int, int, cudaStream_t);        \
+                                        int64_t, T *, int64_t, int, int, bool, int, cudaStream_t); \
     template cudaError_t launch_leaf_u<T>(const Task *, int, const Blk *, const T *, int64_t,  \
                                           const CallArgs<T> *, int, int, int, int, cudaStream_t); \
     template cudaError_t launch_dense<T>(const Task *, int, const Blk *, const CallArgs<T> *,   \
-                                         const T *, int, int, cudaStream_t);                   \
+                                         const T *, int, int, bool, int, cudaStream_t);        \
     template cudaError_t launch_scale<T>(T *, int64_t, int64_t, int, T, cudaStream_t);          \
+    template cudaError_t launch_chain<T>(int, const Task *, const ChainDep *, int, const Blk *, T *, \
+                                         int64_t, int, int, int32_t *, CallArgs<T> *, int, int, \
+                                         cudaStream_t);                                         \
     template cudaError_t launch_tree<T>(int, const TreeStage &, int, const Task *, const Blk *, T *, \
                                         int64_t, int, int, cudaStream_t);                      \
     template cudaError_t launch_transpose<T>(const T *, T *, int64_t, int, int, cudaStream_t);  \
