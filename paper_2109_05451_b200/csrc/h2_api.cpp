@@ -241,7 +241,8 @@ struct h2_ctx {
     cudaStream_t s_leafc = nullptr;  // leaf-level coupling, concurrent with the upsweep transfers
     cudaEvent_t ev_packed = nullptr, ev_recv = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_dense = nullptr, ev_halo = nullptr;
-    cudaEvent_t ev_upleaf = nullptr, ev_leafc = nullptr;
+    cudaEvent_t ev_upleaf = nullptr, ev_leafc = nullptr, ev_cu = nullptr;
+    int sched = 0;                   // H2_SCHED: 0 dense from t = 0, 1 dense paired with the downsweep
     std::vector<void *> owned;       // device allocations to free
     // operator (device)
     const void *U = nullptr, *Vt = nullptr, *D = nullptr;
@@ -262,6 +263,11 @@ struct h2_ctx {
     struct Stage { TreeStage st; int nctas; int r; };
     std::vector<Stage> up_stages, top_stages, down_stages;
     // dependency-driven single-launch sweeps (k_chain): task ranges, their deps, the flags
+    // heap-addressed sweeps (k_sweep): bottom levels one launch each, small top levels fused
+    bool use_sweep = false;
+    std::vector<SweepParams> up_sweeps, dn_sweeps;
+    std::vector<int> up_sweep_ctas, dn_sweep_ctas;
+    int sweep_r_up = 1, sweep_r_dn = 1;
     bool use_chain = true;
     int chain_ctas = 0;
     int64_t up_c0 = 0, dn_c0 = 0;
@@ -355,7 +361,7 @@ int release(h2_ctx *h)
     if (h->s_comm) cudaStreamDestroy(h->s_comm);
     if (h->s_dense) cudaStreamDestroy(h->s_dense);
     if (h->s_leafc) cudaStreamDestroy(h->s_leafc);
-    for (cudaEvent_t e : {h->ev_packed, h->ev_recv, h->ev_fork, h->ev_dense, h->ev_halo, h->ev_upleaf, h->ev_leafc})
+    for (cudaEvent_t e : {h->ev_packed, h->ev_recv, h->ev_fork, h->ev_dense, h->ev_halo, h->ev_upleaf, h->ev_leafc, h->ev_cu})
         if (e) cudaEventDestroy(e);
     delete h;
     return H2_OK;
@@ -481,6 +487,9 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         H2_TRYC(cudaStreamCreateWithPriority(&h->s_leafc, cudaStreamNonBlocking, least));
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_upleaf, cudaEventDisableTiming));
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_leafc, cudaEventDisableTiming));
+        H2_TRYC(cudaEventCreateWithFlags(&h->ev_cu, cudaEventDisableTiming));
+        const char *sc = getenv("H2_SCHED");
+        h->sched = sc ? atoi(sc) : 0;
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_dense, cudaEventDisableTiming));
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
@@ -955,6 +964,58 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         group(h->top_up_lv, true, h->top_stages);
         group(h->down_lv, false, h->down_stages);
     }
+    // ---- heap-addressed sweeps (valid when every transfer level is a local standard level:
+    //      always for P = 1, and for P > 1 without top-tree couplings)
+    {
+        const int TOPN = 64;                     // levels with <= TOPN output nodes are fused
+        const char *sw = getenv("H2_SWEEP");
+        h->use_sweep = !h->has_top && !(sw && sw[0] == '0');
+        auto lvl_up = [&](int lc) {              // parents at lc - 1, children at lc
+            SweepLevel v{h->Ft[lc], h->xh_base[lc], h->xh_base[lc - 1], (int32_t)L.held(lc - 1),
+                         (int16_t)k[lc - 1], (int16_t)k[lc]};
+            return v;
+        };
+        auto lvl_dn = [&](int l) {
+            SweepLevel v{h->E[l], h->yh_base[l - 1], h->yh_base[l], (int32_t)L.held(l), (int16_t)k[l],
+                         (int16_t)k[l - 1]};
+            return v;
+        };
+        if (h->use_sweep) {
+            SweepParams top{};
+            for (int lc : h->up_lv_level) {
+                SweepLevel v = lvl_up(lc);
+                h->sweep_r_up = std::max(h->sweep_r_up, (int)v.r);
+                if (v.n > TOPN) {
+                    SweepParams one{};
+                    one.lv[0] = v;
+                    one.nlev = 1;
+                    h->up_sweeps.push_back(one);
+                    h->up_sweep_ctas.push_back((v.n + WPB - 1) / WPB);
+                } else if (top.nlev < SWEEP_MAXLEV) {
+                    top.lv[top.nlev++] = v;
+                }
+            }
+            if (top.nlev) { h->up_sweeps.push_back(top); h->up_sweep_ctas.push_back(1); }
+            SweepParams dtop{};
+            std::vector<SweepParams> dbot;
+            std::vector<int> dbot_ctas;
+            for (int l : h->down_level) {
+                SweepLevel v = lvl_dn(l);
+                h->sweep_r_dn = std::max(h->sweep_r_dn, (int)v.r);
+                if (v.n <= TOPN && dbot.empty() && dtop.nlev < SWEEP_MAXLEV) dtop.lv[dtop.nlev++] = v;
+                else {
+                    SweepParams one{};
+                    one.lv[0] = v;
+                    one.nlev = 1;
+                    dbot.push_back(one);
+                    dbot_ctas.push_back((v.n + WPB - 1) / WPB);
+                }
+            }
+            if (dtop.nlev) { h->dn_sweeps.push_back(dtop); h->dn_sweep_ctas.push_back(1); }
+            h->dn_sweeps.insert(h->dn_sweeps.end(), dbot.begin(), dbot.end());
+            h->dn_sweep_ctas.insert(h->dn_sweep_ctas.end(), dbot_ctas.begin(), dbot_ctas.end());
+        }
+    }
     // ---- chain sweeps: flat flag index per held node; deps on children (up) / parent (down)
     std::vector<ChainDep> cdeps;
     {
@@ -1054,8 +1115,9 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     for (auto &kv : need_h) hr += (int64_t)kv.second.size();
     int64_t c8[8] = {n_diag, n_off, n_root, nd_diag, nd_off, peers_n, xr, hr};
     memcpy(h->counts, c8, sizeof(c8));
-    int launches = 2 + (int)h->up_stages.size() + (int)h->coup_diag.size() + (int)h->coup_leaf.size() +
-                   (int)h->down_stages.size() + 2;
+    int launches = 2 + (int)(h->use_sweep ? h->up_sweeps.size() : h->up_stages.size()) +
+                   (int)h->coup_diag.size() + (int)h->coup_leaf.size() +
+                   (int)(h->use_sweep ? h->dn_sweeps.size() : h->down_stages.size()) + 2;
     if (P > 1) {
         launches += 2;   // pack x^, pack halo
         for (int ci = 0; ci < 3; ++ci) launches += h->coup_off[ci].n ? 1 : 0;
@@ -1130,10 +1192,19 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
         H2_CUDA(h, cudaEventRecord(h->ev_halo, h->s_comm));
         H2_CUDA(h, cudaStreamWaitEvent(s_dense, h->ev_halo, 0));
     }
-    if ((rc = mark(h, 9, s_dense)) != H2_OK) return rc;
-    H2_CUDA(h, launch_dense<T>(T0(h->dense), h->dense.n, h->d_blks, args, (const T *)h->hrecv, nv, h->dense.r, h->tma_on(nv), h->bw_ctas, s_dense));
-    if ((rc = mark(h, 10, s_dense)) != H2_OK) return rc;
-    H2_CUDA(h, cudaEventRecord(h->ev_dense, s_dense));
+    auto dense_now = [&]() -> int {
+        int rc2;
+        if ((rc2 = mark(h, 9, s_dense)) != H2_OK) return rc2;
+        H2_CUDA(h, launch_dense<T>(T0(h->dense), h->dense.n, h->d_blks, args, (const T *)h->hrecv, nv, h->dense.r,
+                                   h->tma_on(nv), h->bw_ctas, s_dense));
+        if ((rc2 = mark(h, 10, s_dense)) != H2_OK) return rc2;
+        H2_CUDA(h, cudaEventRecord(h->ev_dense, s_dense));
+        return H2_OK;
+    };
+    // schedule 0: dense from t = 0; schedule 1 (H2_SCHED=1): dense paired with the latency-bound
+    // downsweep (starts when the upper-level coupling is done), the leaf-level coupling paired
+    // with the upsweep transfers
+    if (h->sched == 0 && (rc = dense_now()) != H2_OK) return rc;
     H2_MARK(0);
     // 1. upsweep of the local branch (PAPER.md:281 / alg:upsweep2)
     H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
@@ -1149,7 +1220,12 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     if ((rc = mark(h, 12, s_leafc)) != H2_OK) return rc;
     H2_CUDA(h, cudaEventRecord(h->ev_leafc, s_leafc));
     H2_MARK(1);
-    if (h->use_chain)
+    if (h->use_sweep) {
+        for (size_t u = 0; u < h->up_sweeps.size(); ++u)
+            H2_CUDA(h, launch_sweep<T>(MODE_WRITE, h->up_sweeps[u], h->up_sweep_ctas[u],
+                                       h->up_sweep_ctas[u] == 1 && h->up_sweeps[u].nlev > 1 ? 512 : WPB * 32,
+                                       xh, h->xh_plane, nv, h->sweep_r_up, st));
+    } else if (h->use_chain)
         H2_CUDA(h, launch_chain<T>(MODE_WRITE, h->d_tasks + h->up_c0, h->d_deps, h->up_cn, h->d_blks, xh,
                                    h->xh_plane, nv, h->up_cr, h->d_flags, (CallArgs<T> *)h->dargs, 0,
                                    h->chain_ctas, st));
@@ -1192,6 +1268,11 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
         H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
                                   nv, ph.r, h->tma_on(nv), 0, st));
     H2_MARK(4);
+    if (h->sched == 1) {
+        H2_CUDA(h, cudaEventRecord(h->ev_cu, st));
+        H2_CUDA(h, cudaStreamWaitEvent(s_dense, h->ev_cu, 0));
+        if ((rc = dense_now()) != H2_OK) return rc;
+    }
     // 4. off-diagonal part after the exchange (waitAll, alg:optimized_dist_mult line 11-12);
     //    it accumulates into leaf-level rows too, so the leaf coupling stream joins first
     if (L.P > 1) {
@@ -1205,7 +1286,12 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     }
     H2_MARK(5);
     // 5. downsweep transfers (alg:downsweep)
-    if (h->use_chain)
+    if (h->use_sweep) {
+        for (size_t u = 0; u < h->dn_sweeps.size(); ++u)
+            H2_CUDA(h, launch_sweep<T>(MODE_ACCUM, h->dn_sweeps[u], h->dn_sweep_ctas[u],
+                                       h->dn_sweep_ctas[u] == 1 && h->dn_sweeps[u].nlev > 1 ? 512 : WPB * 32,
+                                       yh, h->yh_plane, nv, h->sweep_r_dn, st));
+    } else if (h->use_chain)
         H2_CUDA(h, launch_chain<T>(MODE_ACCUM, h->d_tasks + h->dn_c0, h->d_deps + h->up_cn, h->dn_cn, h->d_blks,
                                    yh, h->yh_plane, nv, h->dn_cr, h->d_flags + h->nflags, (CallArgs<T> *)h->dargs, 1,
                                    h->chain_ctas, st));

@@ -116,4 +116,28 @@ template <typename T>
 cudaError_t launch_tree(int mode, const TreeStage &st, int nctas, const Task *t, const Blk *b, T *buf,
                         int64_t ld, int nv, int r, cudaStream_t s);
 
+// Heap-addressed transfer levels (no task / block descriptors: every address follows from the
+// node index, PAPER.md:135-142 nested bases; children of slot i are slots 2i, 2i+1):
+//   up   (MODE_WRITE): out slot i of level l-1 = Ft_l[2i] x_l[2i] + Ft_l[2i+1] x_l[2i+1]
+//   down (MODE_ACCUM): out slot c of level l  += E_l[c] y_{l-1}[c >> 1]
+// Levels are processed in the order given; with one CTA the whole list runs in one launch with
+// a CTA barrier between levels (the small top levels), with more CTAs exactly one level.
+constexpr int SWEEP_MAXLEV = 32;
+struct SweepLevel {
+    const void *A;      // Ft_l (up) or E_l (down), first held node
+    int64_t xbase;      // element offset of the source level's slot 0
+    int64_t obase;      // element offset of the output level's slot 0
+    int32_t n;          // output nodes of the level
+    int16_t r, c;       // block rows (output rank) / columns (source rank)
+};
+struct SweepParams {
+    SweepLevel lv[SWEEP_MAXLEV];
+    int32_t nlev;
+};
+template <typename T>
+cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads, T *buf, int64_t ld, int nv,
+                         int r, cudaStream_t s);
+// L2 prefetch of a byte range (the small top-level transfers, read late in the chain)
+cudaError_t launch_prefetch_l2(const void *p, int64_t bytes, cudaStream_t s);
+
 }  // namespace h2

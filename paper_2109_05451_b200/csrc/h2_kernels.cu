@@ -22,6 +22,8 @@
 //             Y = alpha y + beta Y                      PAPER.md:399, 414, 225; reading R11/R12
 #include "h2_internal.h"
 
+#include <algorithm>
+
 namespace h2 {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -82,14 +84,19 @@ __device__ __forceinline__ void simt_cols(SimtAcc<T, RPL, NVB> &acc, const T *__
 }
 
 // acc += A (r x c, col-major) * x (c x nvc) with x in registers (x0/x1)
+// column unroll of the Simt engines: 16 (2 CTAs/SM budget) or 8 (3-4 CTAs/SM budget)
+template <int RPL, int NVB>
+__host__ __device__ constexpr int simt_unroll() { return NVB <= 2 ? 8 : 16; }
+
 template <typename T, int RPL, int NVB>
 __device__ __forceinline__ void simt_block_regs(SimtAcc<T, RPL, NVB> &acc, const T *__restrict__ A,
                                                 int r, int c, const T (&x0)[NVB], const T (&x1)[NVB],
                                                 int lane)
 {
     int j = 0;
-    for (; j + 16 <= c; j += 16) simt_cols<T, RPL, NVB, 16>(acc, A, r, j, x0, x1, lane);
-    if (j + 8 <= c) { simt_cols<T, RPL, NVB, 8>(acc, A, r, j, x0, x1, lane); j += 8; }
+    if (simt_unroll<RPL, NVB>() >= 16)
+        for (; j + 16 <= c; j += 16) simt_cols<T, RPL, NVB, 16>(acc, A, r, j, x0, x1, lane);
+    for (; j + 8 <= c; j += 8) simt_cols<T, RPL, NVB, 8>(acc, A, r, j, x0, x1, lane);
     if (j + 4 <= c) { simt_cols<T, RPL, NVB, 4>(acc, A, r, j, x0, x1, lane); j += 4; }
     for (; j < c; ++j) simt_cols<T, RPL, NVB, 1>(acc, A, r, j, x0, x1, lane);
 }
@@ -131,31 +138,56 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b)
 // shared).  Fragments (PTX m8n8k4 .f64): A row = 8mt + lane/4, col = 4ks + lane%4;
 // B row = 4ks + lane%4, col = 8nt + lane/4; rows >= xrows / cols >= nvc read as 0.
 template <int MT, int NT, bool A_STREAM>
+__device__ __forceinline__ void mma_block_step(double (&a)[MT], double (&b)[NT], const double *__restrict__ A,
+                                               int r, int c, const double *src, int64_t ld, int xrows,
+                                               int nvc, int ks, int g, int t)
+{
+    const int col = ks * 4 + t;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        const int row = mt * 8 + g;
+        const double *p = A + (int64_t)col * r + row;
+        a[mt] = (row < r && col < c) ? (A_STREAM ? ld_stream(p) : *p) : 0.0;
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        const int n = nt * 8 + g;
+        b[nt] = (col < xrows && n < nvc) ? src[col + n * ld] : 0.0;
+    }
+}
+
+// acc += A (r x c, col-major, global) * B (c x nvc; element (j, n) at src[j + n*ld], global or
+// shared).  Fragments (PTX m8n8k4 .f64): A row = 8mt + lane/4, col = 4ks + lane%4;
+// B row = 4ks + lane%4, col = 8nt + lane/4; rows >= xrows / cols >= nvc read as 0.
+// Two fragment sets in flight (loads of k-step ks+2 issued behind the DMMAs of k-step ks).
+template <int MT, int NT, bool A_STREAM>
 __device__ __forceinline__ void mma_block(MmaAcc<MT, NT> &acc, const double *__restrict__ A, int r,
                                           int c, const double *src, int64_t ld, int xrows, int nvc,
                                           int lane)
 {
     const int g = lane >> 2, t = lane & 3;
     const int ksn = (c + 3) >> 2;
-#pragma unroll 2
-    for (int ks = 0; ks < ksn; ++ks) {
-        const int col = ks * 4 + t;
-        double a[MT], b[NT];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-            const int row = mt * 8 + g;
-            const double *p = A + (int64_t)col * r + row;
-            a[mt] = (row < r && col < c) ? (A_STREAM ? ld_stream(p) : *p) : 0.0;
-        }
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            const int n = nt * 8 + g;
-            b[nt] = (col < xrows && n < nvc) ? src[col + n * ld] : 0.0;
-        }
+    double a0[MT], b0[NT], a1[MT], b1[NT];
+    mma_block_step<MT, NT, A_STREAM>(a0, b0, A, r, c, src, ld, xrows, nvc, 0, g, t);
+    mma_block_step<MT, NT, A_STREAM>(a1, b1, A, r, c, src, ld, xrows, nvc, 1, g, t);
+    int ks = 0;
+    for (; ks + 2 <= ksn; ks += 2) {
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a[mt], b[nt]);
+            for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a0[mt], b0[nt]);
+        mma_block_step<MT, NT, A_STREAM>(a0, b0, A, r, c, src, ld, xrows, nvc, ks + 2, g, t);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a1[mt], b1[nt]);
+        mma_block_step<MT, NT, A_STREAM>(a1, b1, A, r, c, src, ld, xrows, nvc, ks + 3, g, t);
+    }
+    if (ks < ksn) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a0[mt], b0[nt]);
     }
 }
 
@@ -181,27 +213,50 @@ __device__ __forceinline__ const T *resolve(const Src<T> &s, int64_t x, int32_t 
     return s.neg + (-x - 1) + s.n0 * ld;
 }
 
-// acc += A (r x K, col-major, contiguous) * xs (K x nvc in shared memory, ld xld)
-template <typename T, int RPL, int NVB, int U>
-__device__ __forceinline__ void simt_cols_smem(SimtAcc<T, RPL, NVB> &acc, const T *__restrict__ A,
-                                               int r, int j, const T *xs, int xld, int lane)
+// acc += A (r x K, col-major, contiguous) * xs (K x nvc in shared memory, ld xld): columns in
+// groups of U with two groups in flight (the loads of group g+2 are issued behind the FMAs of
+// group g), so each warp keeps 2U column loads outstanding without exposing HBM latency.
+template <typename T, int RPL, int U>
+__device__ __forceinline__ void simt_load_cols(T (&a)[U][RPL], const T *__restrict__ A, int r, int j, int K,
+                                               int lane)
 {
-    T a[U][RPL];
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int ri = 0; ri < RPL; ++ri) {
-            int i = lane + 32 * ri;
-            a[u][ri] = (i < r) ? ld_stream(A + (int64_t)(j + u) * r + i) : T(0);
+            const int i = lane + 32 * ri;
+            a[u][ri] = (i < r && j + u < K) ? ld_stream(A + (int64_t)(j + u) * r + i) : T(0);
         }
+}
+
+template <typename T, int RPL, int NVB, int U>
+__device__ __forceinline__ void simt_fma_cols(SimtAcc<T, RPL, NVB> &acc, const T (&a)[U][RPL], int j, int K,
+                                              const T *xs, int xld)
+{
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int n = 0; n < NVB; ++n) {
-            T xv = xs[j + u + n * xld];
+            const T xv = (j + u < K) ? xs[j + u + n * xld] : T(0);
 #pragma unroll
             for (int ri = 0; ri < RPL; ++ri) acc.v[ri][n] = fma(a[u][ri], xv, acc.v[ri][n]);
         }
+}
+
+template <typename T, int RPL, int NVB>
+__device__ __forceinline__ void simt_cols_pipelined(SimtAcc<T, RPL, NVB> &acc, const T *__restrict__ A, int r,
+                                                    int K, const T *xs, int xld, int lane)
+{
+    constexpr int U = RPL == 1 ? 8 : 4;
+    T a0[U][RPL], a1[U][RPL];
+    simt_load_cols<T, RPL, U>(a0, A, r, 0, K, lane);
+    simt_load_cols<T, RPL, U>(a1, A, r, U, K, lane);
+    for (int j = 0; j < K; j += 2 * U) {
+        simt_fma_cols<T, RPL, NVB, U>(acc, a0, j, K, xs, xld);
+        simt_load_cols<T, RPL, U>(a0, A, r, j + 2 * U, K, lane);
+        simt_fma_cols<T, RPL, NVB, U>(acc, a1, j + U, K, xs, xld);
+        simt_load_cols<T, RPL, U>(a1, A, r, j + 3 * U, K, lane);
+    }
 }
 
 template <typename T, int RPL, int NVB>
@@ -234,12 +289,7 @@ __device__ __forceinline__ void simt_stream(SimtAcc<T, RPL, NVB> &acc, const T *
             }
         }
         __syncwarp();
-        const T *A = A0 + (int64_t)b0 * r * c;
-        int j = 0;
-        for (; j + 16 <= K; j += 16) simt_cols_smem<T, RPL, NVB, 16>(acc, A, r, j, xs, K, lane);
-        if (j + 8 <= K) { simt_cols_smem<T, RPL, NVB, 8>(acc, A, r, j, xs, K, lane); j += 8; }
-        if (j + 4 <= K) { simt_cols_smem<T, RPL, NVB, 4>(acc, A, r, j, xs, K, lane); j += 4; }
-        for (; j < K; ++j) simt_cols_smem<T, RPL, NVB, 1>(acc, A, r, j, xs, K, lane);
+        simt_cols_pipelined<T, RPL, NVB>(acc, A0 + (int64_t)b0 * r * c, r, K, xs, K, lane);
         __syncwarp();
     }
 }
@@ -251,6 +301,56 @@ struct MmaDesc {
     int32_t pad;
 };
 
+template <int MT, int NT>
+struct MmaFrag {
+    double a[MT], b[NT];
+};
+
+// Load cursor of the stacked-B operand: lane's row j of block bb (descriptor d)
+struct BCursor {
+    int j, bb;
+    MmaDesc d;
+};
+
+template <int MT, int NT>
+__device__ __forceinline__ void mma_load_step(MmaFrag<MT, NT> &f, const double *__restrict__ A, int r, int K,
+                                              int ks, int g, int t, const BCursor &cur, int nvc)
+{
+    const int col = ks * 4 + t;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+        const int row = mt * 8 + g;
+        f.a[mt] = (row < r && col < K) ? ld_stream(A + (int64_t)col * r + row) : 0.0;
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        const int n = nt * 8 + g;
+        f.b[nt] = (col < K && cur.j < cur.d.xrows && n < nvc) ? cur.d.p[cur.j + n * cur.d.ld] : 0.0;
+    }
+}
+
+__device__ __forceinline__ void bcursor_advance(BCursor &cur, int c, int nb, const MmaDesc *ds)
+{
+    cur.j += 4;
+    if (cur.j >= c) {
+        do { cur.j -= c; ++cur.bb; } while (cur.j >= c);
+        cur.d = ds[min(cur.bb, nb - 1)];
+    }
+}
+
+template <int MT, int NT>
+__device__ __forceinline__ void mma_frag_mma(MmaAcc<MT, NT> &acc, const MmaFrag<MT, NT> &f)
+{
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], f.a[mt], f.b[nt]);
+}
+
+// DMMA over a contiguous run with an explicit two-stage register pipeline: the fragments of
+// k-step ks+2 are loaded before the tensor-core work of k-step ks is issued, so HBM latency is
+// covered by two k-steps of DMMA instead of being exposed every k-step (ncu round 1: the
+// unpipelined loop kept the FP64 tensor pipe 45 % busy at 54 % DRAM).
 template <int MT, int NT>
 __device__ __forceinline__ void mma_stream(MmaAcc<MT, NT> &acc, const double *__restrict__ A0, int r,
                                            int c, int nblk, const Blk *__restrict__ blks,
@@ -269,35 +369,29 @@ __device__ __forceinline__ void mma_stream(MmaAcc<MT, NT> &acc, const double *__
         }
         __syncwarp();
         const double *A = A0 + (int64_t)b0 * r * c;
-        int bb = 0, j = t;
-        while (j >= c) { j -= c; ++bb; }
-        MmaDesc d = ds[min(bb, nb - 1)];
+        BCursor cur;
+        cur.j = t;
+        cur.bb = 0;
+        while (cur.j >= c) { cur.j -= c; ++cur.bb; }
+        cur.d = ds[min(cur.bb, nb - 1)];
         const int ksn = (K + 3) >> 2;
-        // deeper unroll (more loads in flight) when the accumulator leaves registers for it
-#pragma unroll (MT <= 4 ? 4 : 2)
-        for (int ks = 0; ks < ksn; ++ks) {
-            const int col = ks * 4 + t;
-            double a[MT], b[NT];
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-                const int row = mt * 8 + g;
-                a[mt] = (row < r && col < K) ? ld_stream(A + (int64_t)col * r + row) : 0.0;
-            }
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                const int n = nt * 8 + g;
-                b[nt] = (col < K && j < d.xrows && n < nvc) ? d.p[j + n * d.ld] : 0.0;
-            }
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a[mt], b[nt]);
-            j += 4;
-            if (j >= c) {
-                do { j -= c; ++bb; } while (j >= c);
-                d = ds[min(bb, nb - 1)];
-            }
+        // two fragment sets in flight: f0 holds k-step ks, f1 k-step ks+1; after the DMMAs of
+        // a set are issued, the set is refilled with the k-step two ahead
+        MmaFrag<MT, NT> f0, f1;
+        mma_load_step(f0, A, r, K, 0, g, t, cur, nvc);
+        bcursor_advance(cur, c, nb, ds);
+        mma_load_step(f1, A, r, K, 1, g, t, cur, nvc);
+        bcursor_advance(cur, c, nb, ds);
+        int ks = 0;
+        for (; ks + 2 <= ksn; ks += 2) {
+            mma_frag_mma(acc, f0);
+            mma_load_step(f0, A, r, K, ks + 2, g, t, cur, nvc);
+            bcursor_advance(cur, c, nb, ds);
+            mma_frag_mma(acc, f1);
+            mma_load_step(f1, A, r, K, ks + 3, g, t, cur, nvc);
+            bcursor_advance(cur, c, nb, ds);
         }
+        if (ks < ksn) mma_frag_mma(acc, f0);
     }
 }
 
@@ -600,6 +694,9 @@ template <typename T, int RPL, int NVB>
 struct Simt {
     using Acc = SimtAcc<T, RPL, NVB>;
     static constexpr int NV = NVB;
+    // CTAs per SM the register budget is sized for (__launch_bounds__ min blocks): the nv <= 2
+    // streaming engines are latency-bound at 2 CTAs (16 warps, 25 % occupancy; ncu round 1)
+    static constexpr int MINB = NVB <= 2 ? (RPL == 1 ? 4 : 3) : 2;
     static constexpr int SCRATCH = XCAP_BYTES;      // per-warp smem for the stream staging
     __device__ static void block(Acc &acc, const T *A, int r, int c, const T *src, int64_t ld, int xrows,
                                  int nvc, int lane)
@@ -617,6 +714,7 @@ template <int MT, int NT>
 struct Mma {
     using Acc = MmaAcc<MT, NT>;
     static constexpr int NV = 8 * NT;
+    static constexpr int MINB = 2;
     static constexpr int SCRATCH = 32 * sizeof(MmaDesc);
     __device__ static void block(Acc &acc, const double *A, int r, int c, const double *src, int64_t ld,
                                  int xrows, int nvc, int lane)
@@ -636,7 +734,7 @@ __host__ __device__ constexpr int warp_tma_bytes() { return TMA_RING + 128 + Eng
 // ---------------------------------------------------------------------------------------
 // Upsweep leaves: x^_s (k x nv) = Vt_s (k x m) x_s (m x nv), Vt = V^T re-laid out at create.
 template <typename T, typename Eng>
-__global__ void __launch_bounds__(WPB * 32, 2)
+__global__ void __launch_bounds__(WPB * 32, Eng::MINB)
 k_up_leaf(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
           const CallArgs<T> *__restrict__ args, T *__restrict__ xh, int64_t xh_ld, int nv)
 {
@@ -662,7 +760,7 @@ k_up_leaf(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blk
 //   MODE_WRITE  out  = sum_b A_b x_b    (upsweep transfers, coupling multiply)
 //   MODE_ACCUM  out += sum_b A_b x_b    (downsweep transfers, off-diagonal coupling pass)
 template <typename T, typename Eng, int MODE, bool TMA>
-__global__ void __launch_bounds__(WPB * 32, 2)
+__global__ void __launch_bounds__(WPB * 32, TMA ? 1 : Eng::MINB)
 k_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
        const T *__restrict__ src, int64_t src_ld, T *__restrict__ dst, int64_t dst_ld, int nv)
 {
@@ -705,12 +803,54 @@ k_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
 }
 
 // ---------------------------------------------------------------------------------------
+// Heap-addressed transfer sweep (see SweepParams): one warp per output node, no descriptor
+// loads -- the A blocks and x operands are computed from the slot index, so a task is a single
+// round of independent loads.  nlev > 1 only with one CTA (barrier between levels).
+template <typename T, typename Eng, int MODE>
+__global__ void __launch_bounds__(512, 1)
+k_sweep(const __grid_constant__ SweepParams p, T *__restrict__ buf, int64_t ld, int nv)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int lv = 0; lv < p.nlev; ++lv) {
+        const SweepLevel L = p.lv[lv];
+        const int64_t blk = (int64_t)L.r * L.c;
+        for (int i = blockIdx.x * nw + wid; i < L.n; i += gridDim.x * nw) {
+            for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
+                const int nvc = min(Eng::NV, nv - n0);
+                typename Eng::Acc acc;
+                T *out = buf + L.obase + (int64_t)i * L.r + (int64_t)n0 * ld;
+                if (MODE == MODE_ACCUM) {
+                    acc_load(acc, out, ld, L.r, nvc, lane);
+                    Eng::block(acc, static_cast<const T *>(L.A) + i * blk, L.r, L.c,
+                               buf + L.xbase + (int64_t)(i >> 1) * L.c + (int64_t)n0 * ld, ld, L.c, nvc, lane);
+                } else {
+                    acc_zero(acc, lane);
+#pragma unroll
+                    for (int ch = 0; ch < 2; ++ch)
+                        Eng::block(acc, static_cast<const T *>(L.A) + (2 * (int64_t)i + ch) * blk, L.r, L.c,
+                                   buf + L.xbase + (2 * (int64_t)i + ch) * L.c + (int64_t)n0 * ld, ld, L.c, nvc, lane);
+                }
+                acc_store(acc, out, ld, L.r, nvc, lane);
+            }
+        }
+        if (p.nlev > 1) __syncthreads();
+    }
+}
+
+__global__ void k_prefetch_l2(const char *p, int64_t bytes)
+{
+    for (int64_t o = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 128; o < bytes;
+         o += (int64_t)gridDim.x * blockDim.x * 128)
+        asm volatile("prefetch.global.L2::evict_last [%0];\n" ::"l"(p + o));
+}
+
+// ---------------------------------------------------------------------------------------
 // Fused tree stage: one CTA owns a subtree and runs `nlev` consecutive transfer levels of it,
 // level by level, with a CTA barrier between levels (the upsweep levels q-1 .. 0 or the
 // downsweep levels 1 .. q-1 in a few launches instead of one launch per level, PAPER.md:263,
 // 408).  Level i's tasks of CTA c are [t0[i] + c * per[i], t0[i] + (c + 1) * per[i]).
 template <typename T, typename Eng, int MODE>
-__global__ void __launch_bounds__(WPB * 32, 2)
+__global__ void __launch_bounds__(WPB * 32, Eng::MINB)
 k_tree(TreeStage st, const Task *__restrict__ tasks, const Blk *__restrict__ blks, T *__restrict__ buf,
        int64_t ld, int nv)
 {
@@ -768,7 +908,7 @@ __device__ __forceinline__ void st_release(int32_t *p, int v)
 }
 
 template <typename T, typename Eng, int MODE>
-__global__ void __launch_bounds__(WPB * 32, 2)
+__global__ void __launch_bounds__(WPB * 32, Eng::MINB)
 k_chain(const Task *__restrict__ tasks, const ChainDep *__restrict__ deps, int ntask,
         const Blk *__restrict__ blks, T *__restrict__ buf, int64_t ld, int nv, int32_t *flags,
         CallArgs<T> *args, int which)
@@ -824,7 +964,7 @@ k_chain(const Task *__restrict__ tasks, const ChainDep *__restrict__ deps, int n
 // already written Y = alpha A_de X + beta Y on the dense stream (reading R11).
 // EngK computes z (rows k), EngM the leaf rows (m); z is handed over through warp smem.
 template <typename T, typename EngK, typename EngM>
-__global__ void __launch_bounds__(WPB * 32, 2)
+__global__ void __launch_bounds__(WPB * 32, EngM::MINB < EngK::MINB ? EngM::MINB : EngK::MINB)
 k_leaf_u(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
          const T *__restrict__ yh, int64_t yh_ld, const CallArgs<T> *__restrict__ args, int nv, int k,
          int kp)
@@ -873,7 +1013,7 @@ k_leaf_u(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks
 // concurrent with the tree phases:  Y_t = alpha sum_s D_ts x_s + beta Y_t  (beta == 0: Y is
 // write-only).  Every leaf has a task (rows without dense blocks still apply beta).
 template <typename T, typename Eng, bool TMA>
-__global__ void __launch_bounds__(WPB * 32, 2)
+__global__ void __launch_bounds__(WPB * 32, TMA ? 1 : Eng::MINB)
 k_dense(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
         const CallArgs<T> *__restrict__ args, const T *__restrict__ halo, int nv)
 {
@@ -1180,6 +1320,28 @@ cudaError_t launch_chain(int mode, const Task *t, const ChainDep *deps, int ntas
 }
 
 template <typename T>
+cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads, T *buf, int64_t ld, int nv,
+                         int r, cudaStream_t s)
+{
+    if (p.nlev == 0 || nctas == 0) return cudaSuccess;
+    Dispatch<T>::run(r, nv, [&](auto e) {
+        using E = decltype(e);
+        if (mode == MODE_WRITE) k_sweep<T, E, MODE_WRITE><<<nctas, threads, 0, s>>>(p, buf, ld, nv);
+        else                    k_sweep<T, E, MODE_ACCUM><<<nctas, threads, 0, s>>>(p, buf, ld, nv);
+    });
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prefetch_l2(const void *p, int64_t bytes, cudaStream_t s)
+{
+    if (!p || bytes <= 0) return cudaSuccess;
+    int64_t lines = (bytes + 127) / 128;
+    int blocks = (int)std::min<int64_t>(148, (lines + 255) / 256);
+    k_prefetch_l2<<<blocks, 256, 0, s>>>(static_cast<const char *>(p), bytes);
+    return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t launch_scale(T *Y, int64_t ldy, int64_t n, int nv, T beta, cudaStream_t s)
 {
     if (n == 0) return cudaSuccess;
@@ -1217,6 +1379,8 @@ cudaError_t launch_pack(const PackSeg *segs, int64_t nseg, const T *src, int64_t
     template cudaError_t launch_dense<T>(const Task *, int, const Blk *, const CallArgs<T> *,   \
                                          const T *, int, int, bool, int, cudaStream_t);        \
     template cudaError_t launch_scale<T>(T *, int64_t, int64_t, int, T, cudaStream_t);          \
+    template cudaError_t launch_sweep<T>(int, const SweepParams &, int, int, T *, int64_t, int, int, \
+                                         cudaStream_t);                                        \
     template cudaError_t launch_chain<T>(int, const Task *, const ChainDep *, int, const Blk *, T *, \
                                          int64_t, int, int, int32_t *, CallArgs<T> *, int, int, \
                                          cudaStream_t);                                         \
