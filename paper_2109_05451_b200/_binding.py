@@ -21,7 +21,7 @@ PHASES = ["up_leaf", "up_transfer", "exchange_top", "coupling_diag", "coupling_o
           "down_transfer", "leaf_u", "dense", "coupling_leaf"]
 KERNEL_OF_PHASE = {"up_leaf": "k_up_leaf", "up_transfer": "k_tree<WRITE>", "exchange_top": "k_pack",
                    "coupling_diag": "k_rows<WRITE>", "coupling_offdiag": "k_rows<ACCUM>",
-                   "down_transfer": "k_tree<ACCUM>", "leaf_u": "k_leaf_u", "dense": "k_dense",
+                   "down_transfer": "k_tree<ACCUM>", "leaf_u": "k_leaf_dense (fused leaf expansion + dense near field + epilogue)", "dense": "k_dense",
                    "coupling_leaf": "k_rows<WRITE>"}
 
 

@@ -242,7 +242,8 @@ struct h2_ctx {
     cudaEvent_t ev_packed = nullptr, ev_recv = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_dense = nullptr, ev_halo = nullptr;
     cudaEvent_t ev_upleaf = nullptr, ev_leafc = nullptr, ev_cu = nullptr;
-    int sched = 0;                   // H2_SCHED: 0 dense from t = 0, 1 dense paired with the downsweep
+    int sched = 0;                   // H2_SCHED: 0 fused leaf+dense kernel (default), 1 dense on its own
+                                     // stream from t = 0, 2 dense paired with the downsweep
     std::vector<void *> owned;       // device allocations to free
     // operator (device)
     const void *U = nullptr, *Vt = nullptr, *D = nullptr;
@@ -1179,7 +1180,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     //    parallel with the tree phases; for P > 1 the x-leaf halo it needs is
     //    exchanged first on the comm stream (X is an input, so it can start at t = 0)
     H2_CUDA(h, cudaEventRecord(h->ev_fork, st));
-    H2_CUDA(h, cudaStreamWaitEvent(s_dense, h->ev_fork, 0));
+    if (h->sched != 0) H2_CUDA(h, cudaStreamWaitEvent(s_dense, h->ev_fork, 0));
     if (L.P > 1) {
         H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_fork, 0));
         H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_h0, h->nseg_h, (const T *)nullptr, 0, args, (T *)h->hsend, nv, h->s_comm));
@@ -1190,7 +1191,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
         }
         H2_NCCL(h, g_nccl.GroupEnd());
         H2_CUDA(h, cudaEventRecord(h->ev_halo, h->s_comm));
-        H2_CUDA(h, cudaStreamWaitEvent(s_dense, h->ev_halo, 0));
+        if (h->sched != 0) H2_CUDA(h, cudaStreamWaitEvent(s_dense, h->ev_halo, 0));
     }
     auto dense_now = [&]() -> int {
         int rc2;
@@ -1204,7 +1205,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     // schedule 0: dense from t = 0; schedule 1 (H2_SCHED=1): dense paired with the latency-bound
     // downsweep (starts when the upper-level coupling is done), the leaf-level coupling paired
     // with the upsweep transfers
-    if (h->sched == 0 && (rc = dense_now()) != H2_OK) return rc;
+    if (h->sched == 1 && (rc = dense_now()) != H2_OK) return rc;
     H2_MARK(0);
     // 1. upsweep of the local branch (PAPER.md:281 / alg:upsweep2)
     H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
@@ -1268,7 +1269,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
         H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
                                   nv, ph.r, h->tma_on(nv), 0, st));
     H2_MARK(4);
-    if (h->sched == 1) {
+    if (h->sched == 2) {
         H2_CUDA(h, cudaEventRecord(h->ev_cu, st));
         H2_CUDA(h, cudaStreamWaitEvent(s_dense, h->ev_cu, 0));
         if ((rc = dense_now()) != H2_OK) return rc;
@@ -1300,14 +1301,23 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
             H2_CUDA(h, launch_tree<T>(MODE_ACCUM, sg.st, sg.nctas, h->d_tasks, h->d_blks, yh, h->yh_plane, nv,
                                       sg.r, st));
     H2_MARK(6);
-    // 6. leaves: last transfer + U expansion added into Y after the dense and leaf-coupling
-    //    streams joined
-    H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_dense, 0));
+    // 6. leaves: last transfer + U expansion (+ the dense near field in the fused schedule),
+    //    after the side streams joined
+    if (h->sched != 0) H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_dense, 0));
+    else if (L.P > 1) H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_halo, 0));   // fused kernel reads the halo
     H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_leafc, 0));
     H2_MARK(7);
+    if (h->sched == 0) {                     // fused schedule: the dense phase is inside phase 6
+        if ((rc = mark(h, 9, st)) != H2_OK) return rc;
+        if ((rc = mark(h, 10, st)) != H2_OK) return rc;
+    }
     const int kq = L.k[q], kp = q >= 1 ? L.k[q - 1] : 1;
-    H2_CUDA(h, launch_leaf_u<T>(T0(h->leaf), h->leaf.n, h->d_blks, yh, h->yh_plane, args, nv, kq, kp,
-                                h->leaf.r, st));
+    if (h->sched == 0)
+        H2_CUDA(h, launch_leaf_dense<T>(T0(h->leaf), T0(h->dense), h->leaf.n, h->d_blks, yh, h->yh_plane, args,
+                                        (const T *)h->hrecv, nv, kq, kp, h->leaf.r, st));
+    else
+        H2_CUDA(h, launch_leaf_u<T>(T0(h->leaf), h->leaf.n, h->d_blks, yh, h->yh_plane, args, nv, kq, kp,
+                                    h->leaf.r, st));
     H2_MARK(8);
     if (h->prof) h->ev_used += NEV;
 #undef H2_MARK
@@ -1441,13 +1451,16 @@ extern "C" int h2_phase_times(h2_handle h, double ms[H2_NPHASE + 1], int64_t *nc
     // phase -> (start event, end event) of a call; see enqueue()
     static const int span[H2_NPHASE + 1][2] = {{0, 11}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6},
                                                {7, 8}, {9, 10}, {11, 12}, {9, 8}};
+    int sp[H2_NPHASE + 1][2];
+    memcpy(sp, span, sizeof(sp));
+    if (h->sched == 0) { sp[H2_NPHASE][0] = 0; }     // fused: the call starts at marker 0
     if (calls) {
         H2_CUDA(h, cudaDeviceSynchronize());
         for (int64_t c = 0; c < calls; ++c) {
             cudaEvent_t *e = &h->ev_pool[c * NEV];
             for (int i = 0; i <= H2_NPHASE; ++i) {
                 float t = 0;
-                H2_CUDA(h, cudaEventElapsedTime(&t, e[span[i][0]], e[span[i][1]]));
+                H2_CUDA(h, cudaEventElapsedTime(&t, e[sp[i][0]], e[sp[i][1]]));
                 ms[i] += t;
             }
         }
@@ -1462,9 +1475,16 @@ extern "C" int h2_phase_stats(h2_handle h, int nv, double bytes[H2_NPHASE + 1], 
 {
     if (!h || nv < 1) return fail(H2_ERR_ARG, "bad argument");
     double tb = 0, tf = 0;
+    double ops[H2_NPHASE], vec[H2_NPHASE];
+    for (int i = 0; i < H2_NPHASE; ++i) { ops[i] = h->ph_ops[i]; vec[i] = h->ph_vec[i]; }
+    if (h->sched == 0) {      // fused leaf + dense kernel: one phase (6), Y written once
+        ops[6] += ops[7];
+        vec[6] += vec[7] - 2.0 * h->n_local;    // Y read+write of k_leaf_u replaced by one write
+        ops[7] = vec[7] = 0;
+    }
     for (int i = 0; i < H2_NPHASE; ++i) {
-        double b = (double)h->esz * (h->ph_ops[i] + nv * h->ph_vec[i]);
-        double f = 2.0 * nv * h->ph_ops[i];
+        double b = (double)h->esz * (ops[i] + nv * vec[i]);
+        double f = 2.0 * nv * ops[i];
         if (bytes) bytes[i] = b;
         if (flops) flops[i] = f;
         tb += b; tf += f;

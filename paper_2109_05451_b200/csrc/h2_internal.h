@@ -87,6 +87,9 @@ cudaError_t launch_rows(int mode, const Task *t, int ntask, const Blk *b, const 
                         int64_t src_ld, T *dst, int64_t dst_ld, int nv, int r, bool tma, int max_ctas,
                         cudaStream_t s);
 template <typename T>
+cudaError_t launch_leaf_dense(const Task *lt, const Task *dt, int ntask, const Blk *b, const T *yh, int64_t yh_ld,
+                              const CallArgs<T> *args, const T *halo, int nv, int k, int kp, int m, cudaStream_t s);
+template <typename T>
 cudaError_t launch_leaf_u(const Task *t, int ntask, const Blk *b, const T *yh, int64_t yh_ld,
                           const CallArgs<T> *args, int nv, int k, int kp, int m, cudaStream_t s);
 template <typename T>

@@ -88,6 +88,38 @@ __device__ __forceinline__ void simt_cols(SimtAcc<T, RPL, NVB> &acc, const T *__
 template <int RPL, int NVB>
 __host__ __device__ constexpr int simt_unroll() { return NVB <= 2 ? 8 : 16; }
 
+template <typename T, int RPL, int U>
+__device__ __forceinline__ void simt_load_cols(T (&a)[U][RPL], const T *__restrict__ A, int r, int j, int K,
+                                               int lane)
+{
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int ri = 0; ri < RPL; ++ri) {
+            const int i = lane + 32 * ri;
+            a[u][ri] = (i < r && j + u < K) ? ld_stream(A + (int64_t)(j + u) * r + i) : T(0);
+        }
+}
+
+template <typename T, int RPL, int NVB, int U>
+__device__ __forceinline__ void simt_fma_cols_regs(SimtAcc<T, RPL, NVB> &acc, const T (&a)[U][RPL], int j,
+                                                   const T (&x0)[NVB], const T (&x1)[NVB])
+{
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int jj = j + u;                       // warp-uniform; columns >= c have a == 0
+#pragma unroll
+        for (int n = 0; n < NVB; ++n) {
+            T xv = __shfl_sync(FULL, jj < 32 ? x0[n] : x1[n], jj & 31);
+#pragma unroll
+            for (int ri = 0; ri < RPL; ++ri) acc.v[ri][n] = fma(a[u][ri], xv, acc.v[ri][n]);
+        }
+    }
+}
+
+// acc += A (r x c, col-major) * x (c x nvc) with x in registers (x0/x1), columns in batches
+// (a two-group register pipeline here measured slower at nv = 1: the single-block tasks are
+// short and the deeper pipeline spilled at the 3-4 CTA/SM register budget)
 template <typename T, int RPL, int NVB>
 __device__ __forceinline__ void simt_block_regs(SimtAcc<T, RPL, NVB> &acc, const T *__restrict__ A,
                                                 int r, int c, const T (&x0)[NVB], const T (&x1)[NVB],
@@ -216,19 +248,6 @@ __device__ __forceinline__ const T *resolve(const Src<T> &s, int64_t x, int32_t 
 // acc += A (r x K, col-major, contiguous) * xs (K x nvc in shared memory, ld xld): columns in
 // groups of U with two groups in flight (the loads of group g+2 are issued behind the FMAs of
 // group g), so each warp keeps 2U column loads outstanding without exposing HBM latency.
-template <typename T, int RPL, int U>
-__device__ __forceinline__ void simt_load_cols(T (&a)[U][RPL], const T *__restrict__ A, int r, int j, int K,
-                                               int lane)
-{
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int ri = 0; ri < RPL; ++ri) {
-            const int i = lane + 32 * ri;
-            a[u][ri] = (i < r && j + u < K) ? ld_stream(A + (int64_t)(j + u) * r + i) : T(0);
-        }
-}
-
 template <typename T, int RPL, int NVB, int U>
 __device__ __forceinline__ void simt_fma_cols(SimtAcc<T, RPL, NVB> &acc, const T (&a)[U][RPL], int j, int K,
                                               const T *xs, int xld)
@@ -734,7 +753,7 @@ __host__ __device__ constexpr int warp_tma_bytes() { return TMA_RING + 128 + Eng
 // ---------------------------------------------------------------------------------------
 // Upsweep leaves: x^_s (k x nv) = Vt_s (k x m) x_s (m x nv), Vt = V^T re-laid out at create.
 template <typename T, typename Eng>
-__global__ void __launch_bounds__(WPB * 32, Eng::MINB)
+__global__ void __launch_bounds__(WPB * 32, Eng::MINB < 3 ? Eng::MINB : 3)
 k_up_leaf(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
           const CallArgs<T> *__restrict__ args, T *__restrict__ xh, int64_t xh_ld, int nv)
 {
@@ -964,7 +983,7 @@ k_chain(const Task *__restrict__ tasks, const ChainDep *__restrict__ deps, int n
 // already written Y = alpha A_de X + beta Y on the dense stream (reading R11).
 // EngK computes z (rows k), EngM the leaf rows (m); z is handed over through warp smem.
 template <typename T, typename EngK, typename EngM>
-__global__ void __launch_bounds__(WPB * 32, EngM::MINB < EngK::MINB ? EngM::MINB : EngK::MINB)
+__global__ void __launch_bounds__(WPB * 32, (EngM::MINB < EngK::MINB ? EngM::MINB : EngK::MINB) < 3 ? (EngM::MINB < EngK::MINB ? EngM::MINB : EngK::MINB) : 3)
 k_leaf_u(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
          const T *__restrict__ yh, int64_t yh_ld, const CallArgs<T> *__restrict__ args, int nv, int k,
          int kp)
@@ -1006,6 +1025,73 @@ k_leaf_u(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks
             }
         });
         __syncwarp();
+    }
+}
+
+// Fused leaf kernel (default schedule): last transfer + leaf expansion + dense near field +
+// epilogue, Y written once:  z_t = y^_t + E_t y^_p ;  Y_t = alpha (U_t z_t + sum_s D_ts x_s) + beta Y_t
+// (reading R11).  Leaf task t = ltasks[t] ([E][U]) and dtasks[t] (dense row).
+template <typename T, typename EngK, typename EngM>
+__global__ void __launch_bounds__(WPB * 32, (EngM::MINB < EngK::MINB ? EngM::MINB : EngK::MINB))
+k_leaf_dense(const Task *__restrict__ ltasks, const Task *__restrict__ dtasks, int ntask,
+             const Blk *__restrict__ blks, const T *__restrict__ yh, int64_t yh_ld,
+             const CallArgs<T> *__restrict__ args, const T *__restrict__ halo, int nv, int k, int kp)
+{
+    const T *__restrict__ X = args->X;
+    T *__restrict__ Y = args->Y;
+    const int64_t ldx = args->ldx, ldy = args->ldy;
+    const T alpha = args->alpha, beta = args->beta;
+    static_assert(EngK::NV == EngM::NV, "engines must agree on the vector chunk");
+    constexpr int NV = EngM::NV;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T *zs = reinterpret_cast<T *>(smem_raw) + wid * NV * ZLD;
+    void *scratch = smem_raw + (size_t)WPB * NV * ZLD * sizeof(T) + wid * EngM::SCRATCH;
+    for (int task = blockIdx.x * WPB + wid; task < ntask; task += gridDim.x * WPB) {
+        const Task tk = ltasks[task];
+        const Task dk = dtasks[task];
+        const bool hasE = tk.flags & TF_HAS_E;
+        const Blk bU = blks[tk.blk0 + (hasE ? 1 : 0)];
+        for (int n0 = 0; n0 < nv; n0 += NV) {
+            const int nvc = min(NV, nv - n0);
+            typename EngK::Acc z;
+            acc_load(z, yh + bU.x + (int64_t)n0 * yh_ld, yh_ld, k, nvc, lane);
+            if (hasE) {
+                const Blk bE = blks[tk.blk0];
+                EngK::block(z, static_cast<const T *>(bE.A), k, kp, yh + bE.x + (int64_t)n0 * yh_ld, yh_ld,
+                            bE.xrows, nvc, lane);
+            }
+            __syncwarp();
+            acc_store(z, zs, (int64_t)ZLD, k, nvc, lane);
+            __syncwarp();
+            typename EngM::Acc acc;
+            acc_zero(acc, lane);
+            EngM::block(acc, static_cast<const T *>(bU.A), tk.r, k, zs, (int64_t)ZLD, k, nvc, lane);
+            if ((dk.flags & TF_ACONTIG) && dk.nblk > 0) {
+                const Src<T> sr{X, ldx, halo, n0};
+                EngM::stream(acc, static_cast<const T *>(blks[dk.blk0].A), dk.r, dk.c, dk.nblk, blks + dk.blk0, sr,
+                             nvc, lane, scratch);
+            } else {
+                for (int bi = 0; bi < dk.nblk; ++bi) {
+                    const Blk b = blks[dk.blk0 + bi];
+                    const T *src;
+                    int64_t ld;
+                    if (b.x >= 0) { src = X + b.x; ld = ldx; }
+                    else          { src = halo + (-b.x - 1); ld = b.xld; }
+                    EngM::block(acc, static_cast<const T *>(b.A), dk.r, dk.c, src + (int64_t)n0 * ld, ld,
+                                b.xrows, nvc, lane);
+                }
+            }
+            T *Yb = Y + tk.out + (int64_t)n0 * ldy;
+            const int rows = tk.rows;
+            acc.each(lane, [&](int row, int n, auto &v) {
+                if (row < rows && n < nvc) {
+                    T *p = Yb + row + n * ldy;
+                    *p = (beta == T(0)) ? alpha * v : fma(alpha, (T)v, beta * *p);
+                }
+            });
+            __syncwarp();
+        }
     }
 }
 
@@ -1262,6 +1348,29 @@ cudaError_t launch_leaf_u(const Task *t, int ntask, const Blk *b, const T *yh, i
     return cudaGetLastError();
 }
 
+template <typename T>
+cudaError_t launch_leaf_dense(const Task *lt, const Task *dt, int ntask, const Blk *b, const T *yh, int64_t yh_ld,
+                              const CallArgs<T> *args, const T *halo, int nv, int k, int kp, int m, cudaStream_t s)
+{
+    if (ntask == 0) return cudaSuccess;
+    cudaError_t err = cudaSuccess;
+    Dispatch<T>::run2(k, m, nv, [&](auto ek, auto em) {
+        using EK = decltype(ek);
+        using EM = decltype(em);
+        auto kern = k_leaf_dense<T, EK, EM>;
+        const size_t sm = (size_t)WPB * (EM::NV * ZLD * sizeof(T) + EM::SCRATCH);
+        static bool attr_set = false;
+        if (!attr_set) {
+            err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            attr_set = (err == cudaSuccess);
+        }
+        if (err == cudaSuccess)
+            kern<<<grid_for(ntask), WPB * 32, sm, s>>>(lt, dt, ntask, b, yh, yh_ld, args, halo, nv, k, kp);
+    });
+    if (err != cudaSuccess) return err;
+    return cudaGetLastError();
+}
+
 template <typename T, bool TMA>
 cudaError_t launch_dense_t(const Task *t, int ntask, const Blk *b, const CallArgs<T> *args, const T *halo,
                            int nv, int m, int max_ctas, cudaStream_t s)
@@ -1374,6 +1483,9 @@ cudaError_t launch_pack(const PackSeg *segs, int64_t nseg, const T *src, int64_t
                                            T *, int64_t, int, int, cudaStream_t);              \
     template cudaError_t launch_rows<T>(int, const Task *, int, const Blk *, const T *,        \
                                         int64_t, T *, int64_t, int, int, bool, int, cudaStream_t); \
+    template cudaError_t launch_leaf_dense<T>(const Task *, const Task *, int, const Blk *, const T *, \
+                                              int64_t, const CallArgs<T> *, const T *, int, int, int, \
+                                              int, cudaStream_t);                                  \
     template cudaError_t launch_leaf_u<T>(const Task *, int, const Blk *, const T *, int64_t,  \
                                           const CallArgs<T> *, int, int, int, int, cudaStream_t); \
     template cudaError_t launch_dense<T>(const Task *, int, const Blk *, const CallArgs<T> *,   \
