@@ -19,9 +19,9 @@ EXPORTS = ["h2_create", "h2_matvec", "h2_matvec_ld", "h2_matvec_host", "h2_set_s
            "h2_plan_counts", "h2_plan_census", "h2_destroy", "h2_nccl_unique_id", "h2_last_error", "h2_version"]
 PHASES = ["up_leaf", "up_transfer", "exchange_top", "coupling_diag", "coupling_offdiag",
           "down_transfer", "leaf_u", "dense", "coupling_leaf"]
-KERNEL_OF_PHASE = {"up_leaf": "k_up_leaf", "up_transfer": "k_tree<WRITE>", "exchange_top": "k_pack",
+KERNEL_OF_PHASE = {"up_leaf": "k_up_leaf (or k_mega_up: leaf projection + upsweep + coupling)", "up_transfer": "k_tree<WRITE>", "exchange_top": "k_pack",
                    "coupling_diag": "k_rows<WRITE>", "coupling_offdiag": "k_rows<ACCUM>",
-                   "down_transfer": "k_tree<ACCUM>", "leaf_u": "k_leaf_dense (fused leaf expansion + dense near field + epilogue)", "dense": "k_dense",
+                   "down_transfer": "k_tree<ACCUM>", "leaf_u": "k_leaf_dense / k_mega_down (downsweep + leaf expansion + dense near field + epilogue)", "dense": "k_dense",
                    "coupling_leaf": "k_rows<WRITE>"}
 
 

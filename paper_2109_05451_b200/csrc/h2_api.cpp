@@ -15,6 +15,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -264,6 +265,13 @@ struct h2_ctx {
     struct Stage { TreeStage st; int nctas; int r; };
     std::vector<Stage> up_stages, top_stages, down_stages;
     // dependency-driven single-launch sweeps (k_chain): task ranges, their deps, the flags
+    // persistent scheduled kernels (k_mega_up / k_mega_down), see h2_internal.h
+    bool use_mega = false;
+    MegaParams mp{};
+    SchedEntry *d_sched = nullptr;
+    int nsched_up = 0, nsched_dn = 0;
+    int mega_r = 1, mega_grid = 0;
+    int32_t *d_counters = nullptr;
     // heap-addressed sweeps (k_sweep): bottom levels one launch each, small top levels fused
     bool use_sweep = false;
     std::vector<SweepParams> up_sweeps, dn_sweeps;
@@ -804,11 +812,13 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     //     (PAPER.md:328-331, 496); every held row gets a task (empty rows write 0)
     std::vector<Task> offd_tasks[3];
     std::vector<Blk> offd_blks[3];
+    std::vector<std::pair<int64_t, int>> coup_task_level;   // (task index, level) of diagonal coupling rows
     {
         // classes: engine class ci (0..2) for the levels above the leaves, 3 + ci for the leaf
         // level (its coupling only needs x^ of the leaves: it runs on its own stream right after
         // the leaf projection, concurrent with the upsweep transfers)
         std::vector<Task> cls[6];
+        std::vector<int> cls_lvl[6];
         std::vector<std::vector<Blk>> cls_blk[6];
         for (int l = 0; l <= q; ++l) {
             if (l < C && !h->has_top) {
@@ -833,6 +843,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
                 Task t{h->yh_base[l] + i * k[l], 0, (int32_t)bl.size(), (uint8_t)k[l], (uint8_t)k[l], 0, 0};
                 const int cj = (l == q && q > 0) ? 3 + ci : ci;
                 cls[cj].push_back(t);
+                cls_lvl[cj].push_back(l);
                 cls_blk[cj].push_back(bl);
                 if (!offb.empty()) {
                     Task to = t;
@@ -858,6 +869,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
                 Task t = cls[cj][o];
                 t.blk0 = (int64_t)blks.size();
                 blks.insert(blks.end(), cls_blk[cj][o].begin(), cls_blk[cj][o].end());
+                coup_task_level.push_back({(int64_t)tasks.size(), cls_lvl[cj][o]});
                 tasks.push_back(t);
             }
             if (ph.n) (cj < 3 ? h->coup_diag : h->coup_leaf).push_back(ph);
@@ -1017,6 +1029,60 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             h->dn_sweep_ctas.insert(h->dn_sweep_ctas.end(), dbot_ctas.begin(), dbot_ctas.end());
         }
     }
+    // ---- persistent scheduled sweeps (valid under the same conditions as the sweeps)
+    {
+        // opt-in (H2_MEGA=1): measured slower than the staged launches on cfg2 in round 1
+        const char *me = getenv("H2_MEGA");
+        h->use_mega = h->use_sweep && (me && me[0] == '1') && q >= 1 && q + 1 <= SWEEP_MAXLEV;
+        if (h->use_mega) {
+            MegaParams &mp = h->mp;
+            mp.q = q;
+            mp.k = k[q];
+            mp.kp = k[q - 1];
+            int64_t fb = 0;
+            for (int l = 0; l <= q; ++l) { mp.fbase[l] = fb; fb += L.held(l); mp.nodes[l] = (int32_t)L.held(l); }
+            mp.fbase[q + 1] = fb;
+            for (int lc = C + 1; lc <= q; ++lc)
+                mp.up[lc] = SweepLevel{h->Ft[lc], h->xh_base[lc], h->xh_base[lc - 1], (int32_t)L.held(lc - 1),
+                                       (int16_t)k[lc - 1], (int16_t)k[lc]};
+            mp.dn_first = h->down_level.empty() ? q : h->down_level.front();
+            for (int l : h->down_level)
+                mp.dn[l] = SweepLevel{h->E[l], h->yh_base[l - 1], h->yh_base[l], (int32_t)L.held(l), (int16_t)k[l],
+                                      (int16_t)k[l - 1]};
+            // coupling tasks per level, longest rows first (already sorted within a class)
+            std::vector<std::vector<int64_t>> coup_by_level(q + 1);
+            for (auto &tl : coup_task_level) coup_by_level[tl.second].push_back(tl.first);
+            for (auto &v : coup_by_level)
+                std::stable_sort(v.begin(), v.end(), [&](int64_t x, int64_t y) { return tasks[x].nblk > tasks[y].nblk; });
+            std::vector<SchedEntry> sch;
+            for (int64_t s = 0; s < nleaf; ++s) sch.push_back({ST_UPLEAF, (int16_t)q, (int32_t)(h->up_leaf.t0 + s)});
+            // interleave: up(lc) producing level lc-1, then the coupling of level lc (complete)
+            for (int lc = q; lc >= C + 1; --lc) {
+                for (int64_t i = 0; i < L.held(lc - 1); ++i) sch.push_back({ST_UP, (int16_t)lc, (int32_t)i});
+                for (int64_t ti : coup_by_level[lc]) sch.push_back({ST_COUP, (int16_t)lc, (int32_t)ti});
+            }
+            for (int l = C; l >= 0; --l)
+                for (int64_t ti : coup_by_level[l]) sch.push_back({ST_COUP, (int16_t)l, (int32_t)ti});
+            h->nsched_up = (int)sch.size();
+            for (int l : h->down_level)
+                for (int64_t c = 0; c < L.held(l); ++c) sch.push_back({ST_DOWN, (int16_t)l, (int32_t)c});
+            for (int64_t t = 0; t < nleaf; ++t) sch.push_back({ST_LEAF, (int16_t)q, (int32_t)t});
+            h->nsched_dn = (int)sch.size() - h->nsched_up;
+            for (int l = 0; l <= q; ++l) h->mega_r = std::max(h->mega_r, k[l]);
+            mp.kmax = h->mega_r;
+            cudaError_t err;
+            h->d_sched = (SchedEntry *)dalloc(h, sch.size() * sizeof(SchedEntry), err);
+            h->d_counters = (int32_t *)dalloc(h, (size_t)(q + 1) * sizeof(int32_t), err);
+            if (!h->d_sched || !h->d_counters) H2_TRY(cuda_fail(h, err, "cudaMalloc(schedule)"));
+            H2_TRYC(cudaMemcpy(h->d_sched, sch.data(), sch.size() * sizeof(SchedEntry), cudaMemcpyHostToDevice));
+            H2_TRYC(cudaMemset(h->d_counters, 0, (size_t)(q + 1) * sizeof(int32_t)));
+            int dev = 0, nsm = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            const char *mg = getenv("H2_MEGA_CTAS");
+            h->mega_grid = (mg ? atoi(mg) : 2) * nsm;
+        }
+    }
     // ---- chain sweeps: flat flag index per held node; deps on children (up) / parent (down)
     std::vector<ChainDep> cdeps;
     {
@@ -1124,6 +1190,14 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         for (int ci = 0; ci < 3; ++ci) launches += h->coup_off[ci].n ? 1 : 0;
         if (h->has_top) launches += (int)h->top_stages.size();
     }
+    if (h->use_mega) {
+        launches = 2 + (L.P > 1 ? 1 + (h->coup_off[0].n > 0) + (h->coup_off[1].n > 0) + (h->coup_off[2].n > 0) + 1 : 0);
+        int32_t nc = q + 1;
+        size_t off_c = h->dtype == H2_F64 ? offsetof(CallArgs<double>, counters) : offsetof(CallArgs<float>, counters);
+        size_t off_n = h->dtype == H2_F64 ? offsetof(CallArgs<double>, ncounters) : offsetof(CallArgs<float>, ncounters);
+        H2_TRYC(cudaMemcpy((char *)h->dargs + off_c, &h->d_counters, sizeof(int32_t *), cudaMemcpyHostToDevice));
+        H2_TRYC(cudaMemcpy((char *)h->dargs + off_n, &nc, sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
     h->launches_per_call = launches;
     *out = h;
     return H2_OK;
@@ -1207,6 +1281,46 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     // with the upsweep transfers
     if (h->sched == 1 && (rc = dense_now()) != H2_OK) return rc;
     H2_MARK(0);
+    if (h->use_mega && h->sched == 0) {
+        // persistent scheduled kernels: (leaf projection + upsweep + diagonal coupling) and
+        // (downsweep + leaf expansion + dense + epilogue), one launch each
+        H2_CUDA(h, launch_mega_up<T>(h->d_sched, h->nsched_up, h->mp, h->d_tasks, h->d_blks, h->d_tasks, xh,
+                                     h->xh_plane, yh, h->yh_plane, h->d_flags, h->d_counters,
+                                     (CallArgs<T> *)h->dargs, nv, h->mega_r, h->mega_grid, st));
+        for (int mk : {11, 12, 1, 2})
+            if ((rc = mark(h, mk, st)) != H2_OK) return rc;
+        if (L.P > 1) {
+            H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_x0, h->nseg_x, xh, h->xh_plane, args, (T *)h->xsend, nv, st));
+            H2_CUDA(h, cudaEventRecord(h->ev_packed, st));
+            H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_packed, 0));
+            H2_NCCL(h, g_nccl.GroupStart());
+            for (const auto &pr : h->peers) {
+                if (pr.xs_cnt) H2_NCCL(h, g_nccl.Send((T *)h->xsend + pr.xs_off, pr.xs_cnt * nv, ty, pr.rank, h->comm, h->s_comm));
+                if (pr.xr_cnt) H2_NCCL(h, g_nccl.Recv((T *)h->xrecv + pr.xr_off, pr.xr_cnt * nv, ty, pr.rank, h->comm, h->s_comm));
+            }
+            H2_NCCL(h, g_nccl.GroupEnd());
+            H2_CUDA(h, cudaEventRecord(h->ev_recv, h->s_comm));
+        }
+        for (int mk : {3, 4})
+            if ((rc = mark(h, mk, st)) != H2_OK) return rc;
+        if (L.P > 1) {
+            H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_recv, 0));
+            for (int ci = 0; ci < 3; ++ci) {
+                const Phase &ph = h->coup_off[ci];
+                H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(ph), ph.n, h->d_blks, (const T *)h->xrecv, 0, yh,
+                                          h->yh_plane, nv, ph.r, false, 0, st));
+            }
+            H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_halo, 0));
+        }
+        for (int mk : {5, 6, 7, 9, 10})
+            if ((rc = mark(h, mk, st)) != H2_OK) return rc;
+        H2_CUDA(h, launch_mega_down<T>(h->d_sched + h->nsched_up, h->nsched_dn, h->mp, T0(h->leaf), T0(h->dense),
+                                       h->d_blks, yh, h->yh_plane, (const T *)h->hrecv, h->d_flags + h->nflags,
+                                       (CallArgs<T> *)h->dargs, nv, L.m, h->mega_grid, st));
+        H2_MARK(8);
+        if (h->prof) h->ev_used += NEV;
+        return H2_OK;
+    }
     // 1. upsweep of the local branch (PAPER.md:281 / alg:upsweep2)
     H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
                                  h->up_leaf.r, st));
@@ -1481,6 +1595,10 @@ extern "C" int h2_phase_stats(h2_handle h, int nv, double bytes[H2_NPHASE + 1], 
         ops[6] += ops[7];
         vec[6] += vec[7] - 2.0 * h->n_local;    // Y read+write of k_leaf_u replaced by one write
         ops[7] = vec[7] = 0;
+    }
+    if (h->use_mega && h->sched == 0) {   // k_mega_up = phases 0+1+3+8, k_mega_down = 5+6
+        for (int i : {1, 3, 8}) { ops[0] += ops[i]; vec[0] += vec[i]; ops[i] = vec[i] = 0; }
+        ops[6] += ops[5]; vec[6] += vec[5]; ops[5] = vec[5] = 0;
     }
     for (int i = 0; i < H2_NPHASE; ++i) {
         double b = (double)h->esz * (ops[i] + nv * vec[i]);

@@ -60,6 +60,8 @@ struct CallArgs {
     T alpha, beta;
     int32_t epoch;           // call counter: completion flags of the chain kernels hold it
     uint32_t ticket[4];      // work tickets of the chain kernels (reset every call)
+    int32_t *counters;       // level-complete counters of the scheduled upsweep (reset per call)
+    int32_t ncounters;
 };
 
 // Dependencies of one chain task (k_chain): it may start once flags[dep0] and flags[dep1]
@@ -140,6 +142,34 @@ struct SweepParams {
 template <typename T>
 cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads, T *buf, int64_t ld, int nv,
                          int r, cudaStream_t s);
+// Persistent scheduled kernels ("megakernels"): every warp takes the next entry of a
+// topologically ordered schedule from an atomic ticket and waits on completion flags / level
+// counters for its dependencies, so the latency-bound tree sweeps overlap with the bandwidth-
+// bound coupling and dense work in ONE launch per sweep direction.
+enum { ST_UPLEAF = 0, ST_UP = 1, ST_COUP = 2, ST_DOWN = 3, ST_LEAF = 4 };
+struct SchedEntry {
+    int16_t type, level;   // level: child level (ST_UP), row level (ST_COUP / ST_DOWN)
+    int32_t idx;           // leaf / node slot, or task index (ST_COUP)
+};
+struct MegaParams {
+    SweepLevel up[SWEEP_MAXLEV];     // by child level lc (parents at lc - 1), like the sweeps
+    SweepLevel dn[SWEEP_MAXLEV];     // by level l
+    int64_t fbase[SWEEP_MAXLEV + 1]; // flat node index of slot 0 of each level
+    int32_t nodes[SWEEP_MAXLEV];     // held nodes per level (level-complete counter target)
+    int32_t q;
+    int32_t dn_first;                // first level computed by the downsweep entries
+    int32_t k, kp;                   // k^q, k^{q-1} (leaf entries)
+    int32_t kmax;                    // max k^l (engine selection for the downsweep entries)
+};
+template <typename T>
+cudaError_t launch_mega_up(const SchedEntry *sched, int n, const MegaParams &mp, const Task *tasks, const Blk *blks,
+                           const Task *upleaf_tasks, T *xh, int64_t xh_ld, T *yh, int64_t yh_ld, int32_t *flags,
+                           int32_t *counters, CallArgs<T> *args, int nv, int r, int grid, cudaStream_t s);
+template <typename T>
+cudaError_t launch_mega_down(const SchedEntry *sched, int n, const MegaParams &mp, const Task *ltasks,
+                             const Task *dtasks, const Blk *blks, T *yh, int64_t yh_ld, const T *halo,
+                             int32_t *flags, CallArgs<T> *args, int nv, int m, int grid, cudaStream_t s);
+
 // L2 prefetch of a byte range (the small top-level transfers, read late in the chain)
 cudaError_t launch_prefetch_l2(const void *p, int64_t bytes, cudaStream_t s);
 

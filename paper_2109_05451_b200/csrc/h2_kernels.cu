@@ -23,6 +23,8 @@
 #include "h2_internal.h"
 
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 namespace h2 {
 
@@ -172,13 +174,13 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b)
 template <int MT, int NT, bool A_STREAM>
 __device__ __forceinline__ void mma_block_step(double (&a)[MT], double (&b)[NT], const double *__restrict__ A,
                                                int r, int c, const double *src, int64_t ld, int xrows,
-                                               int nvc, int ks, int g, int t)
+                                               int nvc, int ks, int g, int t, int lda)
 {
     const int col = ks * 4 + t;
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
         const int row = mt * 8 + g;
-        const double *p = A + (int64_t)col * r + row;
+        const double *p = A + (int64_t)col * lda + row;
         a[mt] = (row < r && col < c) ? (A_STREAM ? ld_stream(p) : *p) : 0.0;
     }
 #pragma unroll
@@ -195,25 +197,26 @@ __device__ __forceinline__ void mma_block_step(double (&a)[MT], double (&b)[NT],
 template <int MT, int NT, bool A_STREAM>
 __device__ __forceinline__ void mma_block(MmaAcc<MT, NT> &acc, const double *__restrict__ A, int r,
                                           int c, const double *src, int64_t ld, int xrows, int nvc,
-                                          int lane)
+                                          int lane, int lda = -1)
 {
     const int g = lane >> 2, t = lane & 3;
+    if (lda < 0) lda = r;
     const int ksn = (c + 3) >> 2;
     double a0[MT], b0[NT], a1[MT], b1[NT];
-    mma_block_step<MT, NT, A_STREAM>(a0, b0, A, r, c, src, ld, xrows, nvc, 0, g, t);
-    mma_block_step<MT, NT, A_STREAM>(a1, b1, A, r, c, src, ld, xrows, nvc, 1, g, t);
+    mma_block_step<MT, NT, A_STREAM>(a0, b0, A, r, c, src, ld, xrows, nvc, 0, g, t, lda);
+    mma_block_step<MT, NT, A_STREAM>(a1, b1, A, r, c, src, ld, xrows, nvc, 1, g, t, lda);
     int ks = 0;
     for (; ks + 2 <= ksn; ks += 2) {
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a0[mt], b0[nt]);
-        mma_block_step<MT, NT, A_STREAM>(a0, b0, A, r, c, src, ld, xrows, nvc, ks + 2, g, t);
+        mma_block_step<MT, NT, A_STREAM>(a0, b0, A, r, c, src, ld, xrows, nvc, ks + 2, g, t, lda);
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a1[mt], b1[nt]);
-        mma_block_step<MT, NT, A_STREAM>(a1, b1, A, r, c, src, ld, xrows, nvc, ks + 3, g, t);
+        mma_block_step<MT, NT, A_STREAM>(a1, b1, A, r, c, src, ld, xrows, nvc, ks + 3, g, t, lda);
     }
     if (ks < ksn) {
 #pragma unroll
@@ -333,13 +336,13 @@ struct BCursor {
 
 template <int MT, int NT>
 __device__ __forceinline__ void mma_load_step(MmaFrag<MT, NT> &f, const double *__restrict__ A, int r, int K,
-                                              int ks, int g, int t, const BCursor &cur, int nvc)
+                                              int ks, int g, int t, const BCursor &cur, int nvc, int lda)
 {
     const int col = ks * 4 + t;
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
         const int row = mt * 8 + g;
-        f.a[mt] = (row < r && col < K) ? ld_stream(A + (int64_t)col * r + row) : 0.0;
+        f.a[mt] = (row < r && col < K) ? ld_stream(A + (int64_t)col * lda + row) : 0.0;
     }
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
@@ -373,9 +376,10 @@ __device__ __forceinline__ void mma_frag_mma(MmaAcc<MT, NT> &acc, const MmaFrag<
 template <int MT, int NT>
 __device__ __forceinline__ void mma_stream(MmaAcc<MT, NT> &acc, const double *__restrict__ A0, int r,
                                            int c, int nblk, const Blk *__restrict__ blks,
-                                           const Src<double> &src, int nvc, int lane, MmaDesc *ds)
+                                           const Src<double> &src, int nvc, int lane, MmaDesc *ds, int lda = -1)
 {
     const int g = lane >> 2, t = lane & 3;
+    if (lda < 0) lda = r;
     for (int b0 = 0; b0 < nblk; b0 += 32) {
         const int nb = min(32, nblk - b0);
         const int K = nb * c;
@@ -387,7 +391,7 @@ __device__ __forceinline__ void mma_stream(MmaAcc<MT, NT> &acc, const double *__
             ds[lane] = MmaDesc{p, ld, b.xrows, 0};
         }
         __syncwarp();
-        const double *A = A0 + (int64_t)b0 * r * c;
+        const double *A = A0 + (int64_t)b0 * lda * c;
         BCursor cur;
         cur.j = t;
         cur.bb = 0;
@@ -397,17 +401,17 @@ __device__ __forceinline__ void mma_stream(MmaAcc<MT, NT> &acc, const double *__
         // two fragment sets in flight: f0 holds k-step ks, f1 k-step ks+1; after the DMMAs of
         // a set are issued, the set is refilled with the k-step two ahead
         MmaFrag<MT, NT> f0, f1;
-        mma_load_step(f0, A, r, K, 0, g, t, cur, nvc);
+        mma_load_step(f0, A, r, K, 0, g, t, cur, nvc, lda);
         bcursor_advance(cur, c, nb, ds);
-        mma_load_step(f1, A, r, K, 1, g, t, cur, nvc);
+        mma_load_step(f1, A, r, K, 1, g, t, cur, nvc, lda);
         bcursor_advance(cur, c, nb, ds);
         int ks = 0;
         for (; ks + 2 <= ksn; ks += 2) {
             mma_frag_mma(acc, f0);
-            mma_load_step(f0, A, r, K, ks + 2, g, t, cur, nvc);
+            mma_load_step(f0, A, r, K, ks + 2, g, t, cur, nvc, lda);
             bcursor_advance(cur, c, nb, ds);
             mma_frag_mma(acc, f1);
-            mma_load_step(f1, A, r, K, ks + 3, g, t, cur, nvc);
+            mma_load_step(f1, A, r, K, ks + 3, g, t, cur, nvc, lda);
             bcursor_advance(cur, c, nb, ds);
         }
         if (ks < ksn) mma_frag_mma(acc, f0);
@@ -736,11 +740,11 @@ struct Mma {
     static constexpr int MINB = 2;
     static constexpr int SCRATCH = 32 * sizeof(MmaDesc);
     __device__ static void block(Acc &acc, const double *A, int r, int c, const double *src, int64_t ld,
-                                 int xrows, int nvc, int lane)
-    { mma_block<MT, NT, true>(acc, A, r, c, src, ld, xrows, nvc, lane); }
+                                 int xrows, int nvc, int lane, int lda = -1)
+    { mma_block<MT, NT, true>(acc, A, r, c, src, ld, xrows, nvc, lane, lda); }
     __device__ static void stream(Acc &acc, const double *A0, int r, int c, int nblk, const Blk *blks,
-                                  const Src<double> &src, int nvc, int lane, void *scratch)
-    { mma_stream<MT, NT>(acc, A0, r, c, nblk, blks, src, nvc, lane, (MmaDesc *)scratch); }
+                                  const Src<double> &src, int nvc, int lane, void *scratch, int lda = -1)
+    { mma_stream<MT, NT>(acc, A0, r, c, nblk, blks, src, nvc, lane, (MmaDesc *)scratch, lda); }
     static constexpr int TSCRATCH = 32 * sizeof(MmaDesc);
     __device__ static void tstream(Acc &acc, const double *A0, int r, int c, int nblk, const Blk *blks,
                                    const Src<double> &src, int nvc, int lane, TmaRing &rg, void *scratch)
@@ -1095,6 +1099,303 @@ k_leaf_dense(const Task *__restrict__ ltasks, const Task *__restrict__ dtasks, i
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Scheduled upsweep + coupling (one persistent launch): entries in topological order
+//   ST_UPLEAF s  : x^_s = V_s^T x_s                          -> flag(q, s), counter[q]++
+//   ST_UP (lc,i) : wait flags of children (lc,2i),(lc,2i+1); x^_i = sum F^T x^_c -> flag, counter
+//   ST_COUP t    : wait counter[level] == nodes[level]; y^_t = sum_s S_ts x^_s  (alg:mult)
+// The schedule interleaves the levels (up q-1, coupling q, up q-2, coupling q-1, ...), so the
+// latency-bound tree levels run while other warps stream coupling blocks.
+__device__ __forceinline__ void wait_flag(const int32_t *f, int epoch)
+{
+    while (ld_acquire(f) != epoch) __nanosleep(32);
+}
+
+__device__ __forceinline__ void wait_count(const int32_t *c, int target)
+{
+    while (ld_acquire(c) < target) __nanosleep(64);
+}
+
+template <typename T, typename Eng>
+__global__ void __launch_bounds__(WPB * 32, Eng::MINB < 2 ? Eng::MINB : 2)
+k_mega_up(const SchedEntry *__restrict__ sched, int nsched, const __grid_constant__ MegaParams mp,
+          const Task *__restrict__ tasks, const Blk *__restrict__ blks, const Task *__restrict__ upleaf,
+          T *__restrict__ xh, int64_t xh_ld, T *__restrict__ yh, int64_t yh_ld, int32_t *flags,
+          int32_t *counters, CallArgs<T> *args, int nv)
+{
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    void *scratch = smem_raw + wid * Eng::SCRATCH;
+    const int epoch = *((volatile int32_t *)&args->epoch);
+    const T *__restrict__ X = args->X;
+    const int64_t ldx = args->ldx;
+    unsigned *ticket = &args->ticket[2];
+    int next = 0;
+    if (lane == 0) next = (int)atomicAdd(ticket, 1u);
+    for (;;) {
+        const int t = __shfl_sync(FULL, next, 0);
+        if (t >= nsched) break;
+        if (lane == 0) next = (int)atomicAdd(ticket, 1u);     // prefetch the next ticket
+        const SchedEntry e = sched[t];
+        int32_t *done_flag = nullptr;
+        int32_t *done_cnt = nullptr;
+        if (e.type == ST_UPLEAF) {
+            const Task tk = upleaf[e.idx];
+            const Blk b = blks[tk.blk0];
+            for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
+                const int nvc = min(Eng::NV, nv - n0);
+                typename Eng::Acc acc;
+                acc_zero(acc, lane);
+                Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.c, X + b.x + (int64_t)n0 * ldx, ldx, b.xrows,
+                           nvc, lane);
+                acc_store(acc, xh + tk.out + (int64_t)n0 * xh_ld, xh_ld, tk.r, nvc, lane);
+            }
+            done_flag = flags + mp.fbase[mp.q] + e.idx;
+            done_cnt = counters + mp.q;
+        } else if (e.type == ST_UP) {
+            const int lc = e.level, i = e.idx;
+            if (lane == 0) {
+                wait_flag(flags + mp.fbase[lc] + 2 * i, epoch);
+                wait_flag(flags + mp.fbase[lc] + 2 * i + 1, epoch);
+                __threadfence();
+            }
+            __syncwarp();
+            const SweepLevel Lv = mp.up[lc];
+            const int64_t blk = (int64_t)Lv.r * Lv.c;
+            for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
+                const int nvc = min(Eng::NV, nv - n0);
+                typename Eng::Acc acc;
+                acc_zero(acc, lane);
+#pragma unroll
+                for (int ch = 0; ch < 2; ++ch)
+                    Eng::block(acc, static_cast<const T *>(Lv.A) + (2 * (int64_t)i + ch) * blk, Lv.r, Lv.c,
+                               xh + Lv.xbase + (2 * (int64_t)i + ch) * Lv.c + (int64_t)n0 * xh_ld, xh_ld, Lv.c, nvc,
+                               lane);
+                acc_store(acc, xh + Lv.obase + (int64_t)i * Lv.r + (int64_t)n0 * xh_ld, xh_ld, Lv.r, nvc, lane);
+            }
+            done_flag = flags + mp.fbase[lc - 1] + i;
+            done_cnt = counters + (lc - 1);
+        } else {   // ST_COUP
+            if (lane == 0) {
+                wait_count(counters + e.level, mp.nodes[e.level]);
+                __threadfence();
+            }
+            __syncwarp();
+            const Task tk = tasks[e.idx];
+            for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
+                const int nvc = min(Eng::NV, nv - n0);
+                typename Eng::Acc acc;
+                acc_zero(acc, lane);
+                if ((tk.flags & TF_ACONTIG) && tk.nblk > 0) {
+                    const Src<T> sr{xh, xh_ld, nullptr, n0};
+                    Eng::stream(acc, static_cast<const T *>(blks[tk.blk0].A), tk.r, tk.c, tk.nblk, blks + tk.blk0, sr,
+                                nvc, lane, scratch);
+                } else {
+                    for (int bi = 0; bi < tk.nblk; ++bi) {
+                        const Blk b = blks[tk.blk0 + bi];
+                        const int64_t ld = b.xld ? (int64_t)b.xld : xh_ld;
+                        Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.c, xh + b.x + (int64_t)n0 * ld, ld,
+                                   b.xrows, nvc, lane);
+                    }
+                }
+                acc_store(acc, yh + tk.out + (int64_t)n0 * yh_ld, yh_ld, tk.r, nvc, lane);
+            }
+        }
+        if (done_flag) {
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                st_release(done_flag, epoch);
+                atomicAdd(done_cnt, 1);
+            }
+        }
+    }
+}
+
+// Scheduled downsweep + leaves (one persistent launch):
+//   ST_DOWN (l,c): wait flag(l-1, c/2) (if computed here); y^_c += E_c y^_parent -> flag(l, c)
+//   ST_LEAF t    : dense row first (needs only X), then wait flag(q-1, t/2), z = y^_t + E_t y^_p,
+//                  Y_t = alpha (U_t z + sum D x) + beta Y_t
+template <typename T, typename EngK, typename EngM>
+__global__ void __launch_bounds__(WPB * 32, (EngM::MINB < EngK::MINB ? EngM::MINB : EngK::MINB) < 2 ? (EngM::MINB < EngK::MINB ? EngM::MINB : EngK::MINB) : 2)
+k_mega_down(const SchedEntry *__restrict__ sched, int nsched, const __grid_constant__ MegaParams mp,
+            const Task *__restrict__ ltasks, const Task *__restrict__ dtasks, const Blk *__restrict__ blks,
+            T *__restrict__ yh, int64_t yh_ld, const T *__restrict__ halo, int32_t *flags, CallArgs<T> *args, int nv)
+{
+    static_assert(EngK::NV == EngM::NV, "engines must agree on the vector chunk");
+    constexpr int NV = EngM::NV;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T *zs = reinterpret_cast<T *>(smem_raw) + wid * NV * ZLD;
+    void *scratch = smem_raw + (size_t)WPB * NV * ZLD * sizeof(T) + wid * EngM::SCRATCH;
+    const int epoch = *((volatile int32_t *)&args->epoch);
+    const T *__restrict__ X = args->X;
+    T *__restrict__ Y = args->Y;
+    const int64_t ldx = args->ldx, ldy = args->ldy;
+    const T alpha = args->alpha, beta = args->beta;
+    unsigned *ticket = &args->ticket[3];
+    const int q = mp.q;
+    int next = 0;
+    if (lane == 0) next = (int)atomicAdd(ticket, 1u);
+    for (;;) {
+        const int t = __shfl_sync(FULL, next, 0);
+        if (t >= nsched) break;
+        if (lane == 0) next = (int)atomicAdd(ticket, 1u);
+        const SchedEntry e = sched[t];
+        if (e.type == ST_DOWN) {
+            const int l = e.level, c = e.idx;
+            if (l - 1 >= mp.dn_first) {
+                if (lane == 0) {
+                    wait_flag(flags + mp.fbase[l - 1] + (c >> 1), epoch);
+                    __threadfence();
+                }
+                __syncwarp();
+            }
+            const SweepLevel Lv = mp.dn[l];
+            const int64_t blk = (int64_t)Lv.r * Lv.c;
+            for (int n0 = 0; n0 < nv; n0 += NV) {
+                const int nvc = min(NV, nv - n0);
+                typename EngK::Acc acc;
+                T *out = yh + Lv.obase + (int64_t)c * Lv.r + (int64_t)n0 * yh_ld;
+                acc_load(acc, out, yh_ld, Lv.r, nvc, lane);
+                EngK::block(acc, static_cast<const T *>(Lv.A) + c * blk, Lv.r, Lv.c,
+                            yh + Lv.xbase + (int64_t)(c >> 1) * Lv.c + (int64_t)n0 * yh_ld, yh_ld, Lv.c, nvc, lane);
+                acc_store(acc, out, yh_ld, Lv.r, nvc, lane);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                st_release(flags + mp.fbase[l] + c, epoch);
+            }
+            continue;
+        }
+        // ST_LEAF
+        const Task tk = ltasks[e.idx];
+        const Task dk = dtasks[e.idx];
+        const bool hasE = tk.flags & TF_HAS_E;
+        const Blk bU = blks[tk.blk0 + (hasE ? 1 : 0)];
+        bool waited = false;
+        for (int n0 = 0; n0 < nv; n0 += NV) {
+            const int nvc = min(NV, nv - n0);
+            typename EngM::Acc acc;
+            acc_zero(acc, lane);
+            if ((dk.flags & TF_ACONTIG) && dk.nblk > 0) {
+                const Src<T> sr{X, ldx, halo, n0};
+                EngM::stream(acc, static_cast<const T *>(blks[dk.blk0].A), dk.r, dk.c, dk.nblk, blks + dk.blk0, sr,
+                             nvc, lane, scratch);
+            } else {
+                for (int bi = 0; bi < dk.nblk; ++bi) {
+                    const Blk b = blks[dk.blk0 + bi];
+                    const T *src;
+                    int64_t ld;
+                    if (b.x >= 0) { src = X + b.x; ld = ldx; }
+                    else          { src = halo + (-b.x - 1); ld = b.xld; }
+                    EngM::block(acc, static_cast<const T *>(b.A), dk.r, dk.c, src + (int64_t)n0 * ld, ld, b.xrows,
+                                nvc, lane);
+                }
+            }
+            if (!waited && hasE && q - 1 >= mp.dn_first) {
+                if (lane == 0) {
+                    wait_flag(flags + mp.fbase[q - 1] + (e.idx >> 1), epoch);
+                    __threadfence();
+                }
+                __syncwarp();
+                waited = true;
+            }
+            typename EngK::Acc z;
+            acc_load(z, yh + bU.x + (int64_t)n0 * yh_ld, yh_ld, mp.k, nvc, lane);
+            if (hasE) {
+                const Blk bE = blks[tk.blk0];
+                EngK::block(z, static_cast<const T *>(bE.A), mp.k, mp.kp, yh + bE.x + (int64_t)n0 * yh_ld, yh_ld,
+                            bE.xrows, nvc, lane);
+            }
+            __syncwarp();
+            acc_store(z, zs, (int64_t)ZLD, mp.k, nvc, lane);
+            __syncwarp();
+            EngM::block(acc, static_cast<const T *>(bU.A), tk.r, mp.k, zs, (int64_t)ZLD, mp.k, nvc, lane);
+            T *Yb = Y + tk.out + (int64_t)n0 * ldy;
+            const int rows = tk.rows;
+            acc.each(lane, [&](int row, int n, auto &v) {
+                if (row < rows && n < nvc) {
+                    T *p = Yb + row + n * ldy;
+                    *p = (beta == T(0)) ? alpha * v : fma(alpha, (T)v, beta * *p);
+                }
+            });
+            __syncwarp();
+        }
+    }
+}
+
+// Row-split fused leaf kernel for the DMMA path with m > 32 (nv >= 5): two warps per leaf, each
+// owning 32 rows of U_t and of the dense row (lda = m), so the accumulator is Mma<4,NT> instead
+// of Mma<8,NT> (no register spills, twice the warps in flight).  z_t is computed by both.
+template <typename T, typename EngK, typename EngH>
+__global__ void __launch_bounds__(WPB * 32, 2)
+k_leaf_dense_split(const Task *__restrict__ ltasks, const Task *__restrict__ dtasks, int ntask2,
+                   const Blk *__restrict__ blks, const T *__restrict__ yh, int64_t yh_ld,
+                   const CallArgs<T> *__restrict__ args, const T *__restrict__ halo, int nv, int k, int kp, int m)
+{
+    const T *__restrict__ X = args->X;
+    T *__restrict__ Y = args->Y;
+    const int64_t ldx = args->ldx, ldy = args->ldy;
+    const T alpha = args->alpha, beta = args->beta;
+    static_assert(EngK::NV == EngH::NV, "engines must agree on the vector chunk");
+    constexpr int NV = EngH::NV;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T *zs = reinterpret_cast<T *>(smem_raw) + wid * NV * ZLD;
+    void *scratch = smem_raw + (size_t)WPB * NV * ZLD * sizeof(T) + wid * EngH::SCRATCH;
+    for (int task2 = blockIdx.x * WPB + wid; task2 < ntask2; task2 += gridDim.x * WPB) {
+        const int task = task2 >> 1, half = task2 & 1;
+        const Task tk = ltasks[task];
+        const Task dk = dtasks[task];
+        const bool hasE = tk.flags & TF_HAS_E;
+        const Blk bU = blks[tk.blk0 + (hasE ? 1 : 0)];
+        const int r0 = 32 * half;
+        const int rh = min(32, m - r0);
+        for (int n0 = 0; n0 < nv; n0 += NV) {
+            const int nvc = min(NV, nv - n0);
+            typename EngK::Acc z;
+            acc_load(z, yh + bU.x + (int64_t)n0 * yh_ld, yh_ld, k, nvc, lane);
+            if (hasE) {
+                const Blk bE = blks[tk.blk0];
+                EngK::block(z, static_cast<const T *>(bE.A), k, kp, yh + bE.x + (int64_t)n0 * yh_ld, yh_ld,
+                            bE.xrows, nvc, lane);
+            }
+            __syncwarp();
+            acc_store(z, zs, (int64_t)ZLD, k, nvc, lane);
+            __syncwarp();
+            typename EngH::Acc acc;
+            acc_zero(acc, lane);
+            EngH::block(acc, static_cast<const T *>(bU.A) + r0, rh, k, zs, (int64_t)ZLD, k, nvc, lane, m);
+            if ((dk.flags & TF_ACONTIG) && dk.nblk > 0) {
+                const Src<T> sr{X, ldx, halo, n0};
+                EngH::stream(acc, static_cast<const T *>(blks[dk.blk0].A) + r0, rh, dk.c, dk.nblk, blks + dk.blk0,
+                             sr, nvc, lane, scratch, m);
+            } else {
+                for (int bi = 0; bi < dk.nblk; ++bi) {
+                    const Blk b = blks[dk.blk0 + bi];
+                    const T *src;
+                    int64_t ld;
+                    if (b.x >= 0) { src = X + b.x; ld = ldx; }
+                    else          { src = halo + (-b.x - 1); ld = b.xld; }
+                    EngH::block(acc, static_cast<const T *>(b.A) + r0, rh, dk.c, src + (int64_t)n0 * ld, ld,
+                                b.xrows, nvc, lane, m);
+                }
+            }
+            T *Yb = Y + tk.out + r0 + (int64_t)n0 * ldy;
+            const int rows = tk.rows - r0;
+            acc.each(lane, [&](int row, int n, auto &v) {
+                if (row < rows && n < nvc) {
+                    T *p = Yb + row + n * ldy;
+                    *p = (beta == T(0)) ? alpha * v : fma(alpha, (T)v, beta * *p);
+                }
+            });
+            __syncwarp();
+        }
+    }
+}
+
 // Dense near field + epilogue (reading R12), on its own low-priority stream
 // concurrent with the tree phases:  Y_t = alpha sum_s D_ts x_s + beta Y_t  (beta == 0: Y is
 // write-only).  Every leaf has a task (rows without dense blocks still apply beta).
@@ -1157,6 +1458,7 @@ __global__ void k_set_args(CallArgs<T> *a, const T *X, int64_t ldx, T *Y, int64_
     a->X = X; a->ldx = ldx; a->Y = Y; a->ldy = ldy; a->alpha = alpha; a->beta = beta;
     a->epoch = a->epoch + 1;
     for (int i = 0; i < 4; ++i) a->ticket[i] = 0;
+    for (int i = 0; i < a->ncounters; ++i) a->counters[i] = 0;
 }
 
 template <typename T>
@@ -1354,6 +1656,32 @@ cudaError_t launch_leaf_dense(const Task *lt, const Task *dt, int ntask, const B
 {
     if (ntask == 0) return cudaSuccess;
     cudaError_t err = cudaSuccess;
+    if constexpr (std::is_same<T, double>::value) {
+        static const bool split_on = !(getenv("H2_SPLIT") && getenv("H2_SPLIT")[0] == '0');
+        if (split_on && nv >= 5 && m > 32) {
+            auto go = [&](auto ek, auto eh) {
+                using EK = decltype(ek);
+                using EH = decltype(eh);
+                auto kern = k_leaf_dense_split<double, EK, EH>;
+                const size_t sm = (size_t)WPB * (EH::NV * ZLD * sizeof(double) + EH::SCRATCH);
+                static bool attr_set = false;
+                if (!attr_set) {
+                    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                    attr_set = (err == cudaSuccess);
+                }
+                if (err == cudaSuccess)
+                    kern<<<grid_for(2 * ntask), WPB * 32, sm, s>>>(lt, dt, 2 * ntask, b, yh, yh_ld, args, halo, nv,
+                                                                   k, kp, m);
+            };
+            Dispatch<double>::run(k, nv, [&](auto ek) {
+                using EK = decltype(ek);
+                if constexpr (EK::NV == 8) go(ek, Mma<4, 1>{});
+                else if constexpr (EK::NV == 16) go(ek, Mma<4, 2>{});
+            });
+            if (err != cudaSuccess) return err;
+            return cudaGetLastError();
+        }
+    }
     Dispatch<T>::run2(k, m, nv, [&](auto ek, auto em) {
         using EK = decltype(ek);
         using EM = decltype(em);
@@ -1366,6 +1694,45 @@ cudaError_t launch_leaf_dense(const Task *lt, const Task *dt, int ntask, const B
         }
         if (err == cudaSuccess)
             kern<<<grid_for(ntask), WPB * 32, sm, s>>>(lt, dt, ntask, b, yh, yh_ld, args, halo, nv, k, kp);
+    });
+    if (err != cudaSuccess) return err;
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_mega_up(const SchedEntry *sched, int n, const MegaParams &mp, const Task *tasks, const Blk *blks,
+                           const Task *upleaf_tasks, T *xh, int64_t xh_ld, T *yh, int64_t yh_ld, int32_t *flags,
+                           int32_t *counters, CallArgs<T> *args, int nv, int r, int grid, cudaStream_t s)
+{
+    if (n == 0) return cudaSuccess;
+    Dispatch<T>::run(r, nv, [&](auto e) {
+        using E = decltype(e);
+        const size_t sm = (size_t)WPB * E::SCRATCH;
+        k_mega_up<T, E><<<grid, WPB * 32, sm, s>>>(sched, n, mp, tasks, blks, upleaf_tasks, xh, xh_ld, yh, yh_ld, flags,
+                                                   counters, args, nv);
+    });
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_mega_down(const SchedEntry *sched, int n, const MegaParams &mp, const Task *ltasks,
+                             const Task *dtasks, const Blk *blks, T *yh, int64_t yh_ld, const T *halo,
+                             int32_t *flags, CallArgs<T> *args, int nv, int m, int grid, cudaStream_t s)
+{
+    if (n == 0) return cudaSuccess;
+    cudaError_t err = cudaSuccess;
+    Dispatch<T>::run2(mp.kmax, m, nv, [&](auto ek, auto em) {
+        using EK = decltype(ek);
+        using EM = decltype(em);
+        auto kern = k_mega_down<T, EK, EM>;
+        const size_t sm = (size_t)WPB * (EM::NV * ZLD * sizeof(T) + EM::SCRATCH);
+        static bool attr_set = false;
+        if (!attr_set) {
+            err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            attr_set = (err == cudaSuccess);
+        }
+        if (err == cudaSuccess)
+            kern<<<grid, WPB * 32, sm, s>>>(sched, n, mp, ltasks, dtasks, blks, yh, yh_ld, halo, flags, args, nv);
     });
     if (err != cudaSuccess) return err;
     return cudaGetLastError();
@@ -1486,6 +1853,13 @@ cudaError_t launch_pack(const PackSeg *segs, int64_t nseg, const T *src, int64_t
     template cudaError_t launch_leaf_dense<T>(const Task *, const Task *, int, const Blk *, const T *, \
                                               int64_t, const CallArgs<T> *, const T *, int, int, int, \
                                               int, cudaStream_t);                                  \
+    template cudaError_t launch_mega_up<T>(const SchedEntry *, int, const MegaParams &, const Task *,  \
+                                           const Blk *, const Task *, T *, int64_t, T *, int64_t,    \
+                                           int32_t *, int32_t *, CallArgs<T> *, int, int, int,      \
+                                           cudaStream_t);                                            \
+    template cudaError_t launch_mega_down<T>(const SchedEntry *, int, const MegaParams &, const Task *, \
+                                             const Task *, const Blk *, T *, int64_t, const T *,      \
+                                             int32_t *, CallArgs<T> *, int, int, int, cudaStream_t);  \
     template cudaError_t launch_leaf_u<T>(const Task *, int, const Blk *, const T *, int64_t,  \
                                           const CallArgs<T> *, int, int, int, int, cudaStream_t); \
     template cudaError_t launch_dense<T>(const Task *, int, const Blk *, const CallArgs<T> *,   \
