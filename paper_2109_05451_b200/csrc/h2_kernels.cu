@@ -202,28 +202,30 @@ __device__ __forceinline__ void mma_block(MmaAcc<MT, NT> &acc, const double *__r
     const int g = lane >> 2, t = lane & 3;
     if (lda < 0) lda = r;
     const int ksn = (c + 3) >> 2;
-    double a0[MT], b0[NT], a1[MT], b1[NT];
-    mma_block_step<MT, NT, A_STREAM>(a0, b0, A, r, c, src, ld, xrows, nvc, 0, g, t, lda);
-    mma_block_step<MT, NT, A_STREAM>(a1, b1, A, r, c, src, ld, xrows, nvc, 1, g, t, lda);
+    constexpr int PD = MT <= 4 ? 3 : 2;      // fragment sets in flight (see mma_stream)
+    double a[PD][MT], b[PD][NT];
+#pragma unroll
+    for (int p = 0; p < PD; ++p)
+        mma_block_step<MT, NT, A_STREAM>(a[p], b[p], A, r, c, src, ld, xrows, nvc, p, g, t, lda);
     int ks = 0;
-    for (; ks + 2 <= ksn; ks += 2) {
+    for (; ks + PD <= ksn; ks += PD) {
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
+        for (int p = 0; p < PD; ++p) {
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a0[mt], b0[nt]);
-        mma_block_step<MT, NT, A_STREAM>(a0, b0, A, r, c, src, ld, xrows, nvc, ks + 2, g, t, lda);
+            for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a1[mt], b1[nt]);
-        mma_block_step<MT, NT, A_STREAM>(a1, b1, A, r, c, src, ld, xrows, nvc, ks + 3, g, t, lda);
+                for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a[p][mt], b[p][nt]);
+            mma_block_step<MT, NT, A_STREAM>(a[p], b[p], A, r, c, src, ld, xrows, nvc, ks + PD + p, g, t, lda);
+        }
     }
-    if (ks < ksn) {
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
+    for (int p = 0; p < PD; ++p)
+        if (ks + p < ksn) {
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a0[mt], b0[nt]);
-    }
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a[p][mt], b[p][nt]);
+        }
 }
 
 // =========================================================================== streaming rows
@@ -398,23 +400,27 @@ __device__ __forceinline__ void mma_stream(MmaAcc<MT, NT> &acc, const double *__
         while (cur.j >= c) { cur.j -= c; ++cur.bb; }
         cur.d = ds[min(cur.bb, nb - 1)];
         const int ksn = (K + 3) >> 2;
-        // two fragment sets in flight: f0 holds k-step ks, f1 k-step ks+1; after the DMMAs of
-        // a set are issued, the set is refilled with the k-step two ahead
-        MmaFrag<MT, NT> f0, f1;
-        mma_load_step(f0, A, r, K, 0, g, t, cur, nvc, lda);
-        bcursor_advance(cur, c, nb, ds);
-        mma_load_step(f1, A, r, K, 1, g, t, cur, nvc, lda);
-        bcursor_advance(cur, c, nb, ds);
-        int ks = 0;
-        for (; ks + 2 <= ksn; ks += 2) {
-            mma_frag_mma(acc, f0);
-            mma_load_step(f0, A, r, K, ks + 2, g, t, cur, nvc, lda);
-            bcursor_advance(cur, c, nb, ds);
-            mma_frag_mma(acc, f1);
-            mma_load_step(f1, A, r, K, ks + 3, g, t, cur, nvc, lda);
+        // PD fragment sets in flight (k-steps ks .. ks+PD-1); after the DMMAs of a set are issued,
+        // the set is refilled with the k-step PD ahead
+        constexpr int PD = MT <= 4 ? 3 : 2;
+        MmaFrag<MT, NT> f[PD];
+#pragma unroll
+        for (int p = 0; p < PD; ++p) {
+            mma_load_step(f[p], A, r, K, p, g, t, cur, nvc, lda);
             bcursor_advance(cur, c, nb, ds);
         }
-        if (ks < ksn) mma_frag_mma(acc, f0);
+        int ks = 0;
+        for (; ks + PD <= ksn; ks += PD) {
+#pragma unroll
+            for (int p = 0; p < PD; ++p) {
+                mma_frag_mma(acc, f[p]);
+                mma_load_step(f[p], A, r, K, ks + PD + p, g, t, cur, nvc, lda);
+                bcursor_advance(cur, c, nb, ds);
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < PD; ++p)
+            if (ks + p < ksn) mma_frag_mma(acc, f[p]);
     }
 }
 
