@@ -122,11 +122,24 @@ __device__ __forceinline__ void simt_fma_cols_regs(SimtAcc<T, RPL, NVB> &acc, co
 // acc += A (r x c, col-major) * x (c x nvc) with x in registers (x0/x1), columns in batches
 // (a two-group register pipeline here measured slower at nv = 1: the single-block tasks are
 // short and the deeper pipeline spilled at the 3-4 CTA/SM register budget)
-template <typename T, int RPL, int NVB>
+template <typename T, int RPL, int NVB, bool WIDE = false>
 __device__ __forceinline__ void simt_block_regs(SimtAcc<T, RPL, NVB> &acc, const T *__restrict__ A,
                                                 int r, int c, const T (&x0)[NVB], const T (&x1)[NVB],
                                                 int lane)
 {
+    if (WIDE && RPL == 1 && NVB == 1 && c <= 32) {
+        // small block (a transfer or coupling block, k <= 32): every column load in flight at
+        // once -- one HBM round trip per block instead of one per batch of 8 columns
+        T a[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) a[u] = (lane < r && u < c) ? ld_stream(A + (int64_t)u * r + lane) : T(0);
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+            const T xv = __shfl_sync(FULL, x0[0], u);
+            acc.v[0][0] = fma(a[u], xv, acc.v[0][0]);
+        }
+        return;
+    }
     int j = 0;
     if (simt_unroll<RPL, NVB>() >= 16)
         for (; j + 16 <= c; j += 16) simt_cols<T, RPL, NVB, 16>(acc, A, r, j, x0, x1, lane);
@@ -135,14 +148,14 @@ __device__ __forceinline__ void simt_block_regs(SimtAcc<T, RPL, NVB> &acc, const
     for (; j < c; ++j) simt_cols<T, RPL, NVB, 1>(acc, A, r, j, x0, x1, lane);
 }
 
-template <typename T, int RPL, int NVB>
+template <typename T, int RPL, int NVB, bool WIDE = false>
 __device__ __forceinline__ void simt_block(SimtAcc<T, RPL, NVB> &acc, const T *__restrict__ A, int r,
                                            int c, const T *__restrict__ src, int64_t ld, int xrows,
                                            int nvc, int lane)
 {
     T x0[NVB], x1[NVB];
     simt_load_x<T, NVB>(x0, x1, src, ld, xrows, nvc, lane);
-    simt_block_regs<T, RPL, NVB>(acc, A, r, c, x0, x1, lane);
+    simt_block_regs<T, RPL, NVB, WIDE>(acc, A, r, c, x0, x1, lane);
 }
 
 // =========================================================================== Mma engine
@@ -726,10 +739,15 @@ struct Simt {
     // CTAs per SM the register budget is sized for (__launch_bounds__ min blocks): the nv <= 2
     // streaming engines are latency-bound at 2 CTAs (16 warps, 25 % occupancy; ncu round 1)
     static constexpr int MINB = NVB <= 2 ? (RPL == 1 ? 4 : 3) : 2;
+    static constexpr bool SIMT1 = (RPL == 1 && NVB == 1);
     static constexpr int SCRATCH = XCAP_BYTES;      // per-warp smem for the stream staging
     __device__ static void block(Acc &acc, const T *A, int r, int c, const T *src, int64_t ld, int xrows,
-                                 int nvc, int lane)
+                                 int nvc, int lane, int lda = -1)
     { simt_block<T, RPL, NVB>(acc, A, r, c, src, ld, xrows, nvc, lane); }
+    // all columns of a small block in flight at once (needs ~2x the registers: k_sweep only)
+    __device__ static void block_wide(Acc &acc, const T *A, int r, int c, const T *src, int64_t ld, int xrows,
+                                      int nvc, int lane)
+    { simt_block<T, RPL, NVB, true>(acc, A, r, c, src, ld, xrows, nvc, lane); }
     __device__ static void stream(Acc &acc, const T *A0, int r, int c, int nblk, const Blk *blks,
                                   const Src<T> &src, int nvc, int lane, void *scratch)
     { simt_stream<T, RPL, NVB>(acc, A0, r, c, nblk, blks, src, nvc, lane, (T *)scratch, XCAP_BYTES / (int)sizeof(T)); }
@@ -744,10 +762,14 @@ struct Mma {
     using Acc = MmaAcc<MT, NT>;
     static constexpr int NV = 8 * NT;
     static constexpr int MINB = 2;
+    static constexpr bool SIMT1 = false;
     static constexpr int SCRATCH = 32 * sizeof(MmaDesc);
     __device__ static void block(Acc &acc, const double *A, int r, int c, const double *src, int64_t ld,
                                  int xrows, int nvc, int lane, int lda = -1)
     { mma_block<MT, NT, true>(acc, A, r, c, src, ld, xrows, nvc, lane, lda); }
+    __device__ static void block_wide(Acc &acc, const double *A, int r, int c, const double *src, int64_t ld,
+                                      int xrows, int nvc, int lane)
+    { mma_block<MT, NT, true>(acc, A, r, c, src, ld, xrows, nvc, lane); }
     __device__ static void stream(Acc &acc, const double *A0, int r, int c, int nblk, const Blk *blks,
                                   const Src<double> &src, int nvc, int lane, void *scratch, int lda = -1)
     { mma_stream<MT, NT>(acc, A0, r, c, nblk, blks, src, nvc, lane, (MmaDesc *)scratch, lda); }
@@ -850,13 +872,13 @@ k_sweep(const __grid_constant__ SweepParams p, T *__restrict__ buf, int64_t ld, 
                 T *out = buf + L.obase + (int64_t)i * L.r + (int64_t)n0 * ld;
                 if (MODE == MODE_ACCUM) {
                     acc_load(acc, out, ld, L.r, nvc, lane);
-                    Eng::block(acc, static_cast<const T *>(L.A) + i * blk, L.r, L.c,
+                    Eng::block_wide(acc, static_cast<const T *>(L.A) + i * blk, L.r, L.c,
                                buf + L.xbase + (int64_t)(i >> 1) * L.c + (int64_t)n0 * ld, ld, L.c, nvc, lane);
                 } else {
                     acc_zero(acc, lane);
 #pragma unroll
                     for (int ch = 0; ch < 2; ++ch)
-                        Eng::block(acc, static_cast<const T *>(L.A) + (2 * (int64_t)i + ch) * blk, L.r, L.c,
+                        Eng::block_wide(acc, static_cast<const T *>(L.A) + (2 * (int64_t)i + ch) * blk, L.r, L.c,
                                    buf + L.xbase + (2 * (int64_t)i + ch) * L.c + (int64_t)n0 * ld, ld, L.c, nvc, lane);
                 }
                 acc_store(acc, out, ld, L.r, nvc, lane);
