@@ -277,6 +277,7 @@ struct h2_ctx {
     std::vector<SweepParams> up_sweeps, dn_sweeps;
     std::vector<int> up_sweep_ctas, dn_sweep_ctas;
     int sweep_r_up = 1, sweep_r_dn = 1;
+    PrefetchList top_pf{};           // top-level F^T / E blocks prefetched into L2 every call
     bool use_chain = true;
     int chain_ctas = 0;
     int64_t up_c0 = 0, dn_c0 = 0;
@@ -993,6 +994,16 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
                          (int16_t)k[l - 1]};
             return v;
         };
+        // L2 prefetch list: F^T and E of the levels with <= 1024 held nodes (opt-in H2_PREFETCH=1:
+        // shortens the top sweep levels but measured net-neutral on cfg2)
+        const char *pf = getenv("H2_PREFETCH");
+        if (pf && pf[0] == '1')
+            for (int l = 1; l <= q && h->top_pf.n + 2 <= PREFETCH_MAX; ++l) {
+                if (L.held(l) > 1024) break;
+                const int64_t bytes = L.held(l) * k[l] * k[l - 1] * (int64_t)h->esz;
+                h->top_pf.ptr[h->top_pf.n] = h->Ft[l]; h->top_pf.bytes[h->top_pf.n++] = bytes;
+                h->top_pf.ptr[h->top_pf.n] = h->E[l]; h->top_pf.bytes[h->top_pf.n++] = bytes;
+            }
         if (h->use_sweep) {
             SweepParams top{};
             for (int lc : h->up_lv_level) {
@@ -1182,7 +1193,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     for (auto &kv : need_h) hr += (int64_t)kv.second.size();
     int64_t c8[8] = {n_diag, n_off, n_root, nd_diag, nd_off, peers_n, xr, hr};
     memcpy(h->counts, c8, sizeof(c8));
-    int launches = 2 + (int)(h->use_sweep ? h->up_sweeps.size() : h->up_stages.size()) +
+    int launches = 2 + (h->top_pf.n > 0) + (int)(h->use_sweep ? h->up_sweeps.size() : h->up_stages.size()) +
                    (int)h->coup_diag.size() + (int)h->coup_leaf.size() +
                    (int)(h->use_sweep ? h->dn_sweeps.size() : h->down_stages.size()) + 2;
     if (P > 1) {
@@ -1280,6 +1291,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     // downsweep (starts when the upper-level coupling is done), the leaf-level coupling paired
     // with the upsweep transfers
     if (h->sched == 1 && (rc = dense_now()) != H2_OK) return rc;
+    H2_CUDA(h, launch_prefetch_l2(h->top_pf, st));
     H2_MARK(0);
     if (h->use_mega && h->sched == 0) {
         // persistent scheduled kernels: (leaf projection + upsweep + diagonal coupling) and

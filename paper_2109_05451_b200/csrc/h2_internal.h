@@ -170,7 +170,13 @@ cudaError_t launch_mega_down(const SchedEntry *sched, int n, const MegaParams &m
                              const Task *dtasks, const Blk *blks, T *yh, int64_t yh_ld, const T *halo,
                              int32_t *flags, CallArgs<T> *args, int nv, int m, int grid, cudaStream_t s);
 
-// L2 prefetch of a byte range (the small top-level transfers, read late in the chain)
-cudaError_t launch_prefetch_l2(const void *p, int64_t bytes, cudaStream_t s);
+// L2 prefetch of byte ranges (the small top-level transfers, read late in the chain)
+constexpr int PREFETCH_MAX = 64;
+struct PrefetchList {
+    const void *ptr[PREFETCH_MAX];
+    int64_t bytes[PREFETCH_MAX];
+    int32_t n;
+};
+cudaError_t launch_prefetch_l2(const PrefetchList &pl, cudaStream_t s);
 
 }  // namespace h2

@@ -888,10 +888,14 @@ k_sweep(const __grid_constant__ SweepParams p, T *__restrict__ buf, int64_t ld, 
     }
 }
 
-__global__ void k_prefetch_l2(const char *p, int64_t bytes)
+__global__ void k_prefetch_l2(const PrefetchList pl)
 {
-    for (int64_t o = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 128; o < bytes;
-         o += (int64_t)gridDim.x * blockDim.x * 128)
+    // one CTA per range: L2 prefetch (evict_last) of the small top-level transfer blocks, read
+    // late by latency-bound sweep levels (PAPER.md:263, 408 top of the trees)
+    if (blockIdx.x >= pl.n) return;
+    const char *p = static_cast<const char *>(pl.ptr[blockIdx.x]);
+    const int64_t bytes = pl.bytes[blockIdx.x];
+    for (int64_t o = (int64_t)threadIdx.x * 128; o < bytes; o += (int64_t)blockDim.x * 128)
         asm volatile("prefetch.global.L2::evict_last [%0];\n" ::"l"(p + o));
 }
 
@@ -1836,12 +1840,10 @@ cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads,
     return cudaGetLastError();
 }
 
-cudaError_t launch_prefetch_l2(const void *p, int64_t bytes, cudaStream_t s)
+cudaError_t launch_prefetch_l2(const PrefetchList &pl, cudaStream_t s)
 {
-    if (!p || bytes <= 0) return cudaSuccess;
-    int64_t lines = (bytes + 127) / 128;
-    int blocks = (int)std::min<int64_t>(148, (lines + 255) / 256);
-    k_prefetch_l2<<<blocks, 256, 0, s>>>(static_cast<const char *>(p), bytes);
+    if (pl.n <= 0) return cudaSuccess;
+    k_prefetch_l2<<<pl.n, 256, 0, s>>>(pl);
     return cudaGetLastError();
 }
 
