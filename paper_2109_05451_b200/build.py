@@ -10,8 +10,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libh2b200.so")
-SOURCES = [os.path.join(CSRC, "h2_kernels.cu"), os.path.join(CSRC, "h2_api.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, "h2_internal.h"), os.path.join(ROOT, "include", "h2.h")]
+SOURCES = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.startswith("h2_k_") and f.endswith(".cu")) + \
+    [os.path.join(CSRC, "h2_api.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, "h2_internal.h"), os.path.join(CSRC, "h2_kernels.cuh"),
+                  os.path.join(ROOT, "include", "h2.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

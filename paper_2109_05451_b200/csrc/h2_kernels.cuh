@@ -1,4 +1,6 @@
-// h2_kernels.cu -- sm_100a kernels of the H^2 matvec hot path.
+// h2_kernels.cuh -- sm_100a kernels of the H^2 matvec hot path.
+// Included by the h2_k_*.cu translation units, each instantiating a subset of the launchers
+// for one element type (parallel compilation).
 //
 // Every phase is a set of warp tasks over a static plan built once by h2_create (the paper's
 // per-level marshaling, done at setup instead of per call).  A task owns one
@@ -888,6 +890,7 @@ k_sweep(const __grid_constant__ SweepParams p, T *__restrict__ buf, int64_t ld, 
     }
 }
 
+#ifdef H2_TU_COMMON
 __global__ void k_prefetch_l2(const PrefetchList pl)
 {
     // one CTA per range: L2 prefetch (evict_last) of the small top-level transfer blocks, read
@@ -898,6 +901,7 @@ __global__ void k_prefetch_l2(const PrefetchList pl)
     for (int64_t o = (int64_t)threadIdx.x * 128; o < bytes; o += (int64_t)blockDim.x * 128)
         asm volatile("prefetch.global.L2::evict_last [%0];\n" ::"l"(p + o));
 }
+#endif
 
 // ---------------------------------------------------------------------------------------
 // Fused tree stage: one CTA owns a subtree and runs `nlev` consecutive transfer levels of it,
@@ -1840,12 +1844,14 @@ cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads,
     return cudaGetLastError();
 }
 
+#ifdef H2_TU_COMMON
 cudaError_t launch_prefetch_l2(const PrefetchList &pl, cudaStream_t s)
 {
     if (pl.n <= 0) return cudaSuccess;
     k_prefetch_l2<<<pl.n, 256, 0, s>>>(pl);
     return cudaGetLastError();
 }
+#endif
 
 template <typename T>
 cudaError_t launch_scale(T *Y, int64_t ldy, int64_t n, int nv, T beta, cudaStream_t s)
@@ -1872,41 +1878,5 @@ cudaError_t launch_pack(const PackSeg *segs, int64_t nseg, const T *src, int64_t
     k_pack<T><<<(int)(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(segs, nseg, src, src_ld, args, dst, nv);
     return cudaGetLastError();
 }
-
-#define H2_INSTANTIATE(T)                                                                      \
-    template cudaError_t launch_set_args<T>(CallArgs<T> *, const T *, int64_t, T *, int64_t, T, T, \
-                                            cudaStream_t);                                     \
-    template cudaError_t launch_up_leaf<T>(const Task *, int, const Blk *, const CallArgs<T> *, \
-                                           T *, int64_t, int, int, cudaStream_t);              \
-    template cudaError_t launch_rows<T>(int, const Task *, int, const Blk *, const T *,        \
-                                        int64_t, T *, int64_t, int, int, bool, int, cudaStream_t); \
-    template cudaError_t launch_leaf_dense<T>(const Task *, const Task *, int, const Blk *, const T *, \
-                                              int64_t, const CallArgs<T> *, const T *, int, int, int, \
-                                              int, cudaStream_t);                                  \
-    template cudaError_t launch_mega_up<T>(const SchedEntry *, int, const MegaParams &, const Task *,  \
-                                           const Blk *, const Task *, T *, int64_t, T *, int64_t,    \
-                                           int32_t *, int32_t *, CallArgs<T> *, int, int, int,      \
-                                           cudaStream_t);                                            \
-    template cudaError_t launch_mega_down<T>(const SchedEntry *, int, const MegaParams &, const Task *, \
-                                             const Task *, const Blk *, T *, int64_t, const T *,      \
-                                             int32_t *, CallArgs<T> *, int, int, int, cudaStream_t);  \
-    template cudaError_t launch_leaf_u<T>(const Task *, int, const Blk *, const T *, int64_t,  \
-                                          const CallArgs<T> *, int, int, int, int, cudaStream_t); \
-    template cudaError_t launch_dense<T>(const Task *, int, const Blk *, const CallArgs<T> *,   \
-                                         const T *, int, int, bool, int, cudaStream_t);        \
-    template cudaError_t launch_scale<T>(T *, int64_t, int64_t, int, T, cudaStream_t);          \
-    template cudaError_t launch_sweep<T>(int, const SweepParams &, int, int, T *, int64_t, int, int, \
-                                         cudaStream_t);                                        \
-    template cudaError_t launch_chain<T>(int, const Task *, const ChainDep *, int, const Blk *, T *, \
-                                         int64_t, int, int, int32_t *, CallArgs<T> *, int, int, \
-                                         cudaStream_t);                                         \
-    template cudaError_t launch_tree<T>(int, const TreeStage &, int, const Task *, const Blk *, T *, \
-                                        int64_t, int, int, cudaStream_t);                      \
-    template cudaError_t launch_transpose<T>(const T *, T *, int64_t, int, int, cudaStream_t);  \
-    template cudaError_t launch_pack<T>(const PackSeg *, int64_t, const T *, int64_t,          \
-                                        const CallArgs<T> *, T *, int, cudaStream_t);
-
-H2_INSTANTIATE(double)
-H2_INSTANTIATE(float)
 
 }  // namespace h2
