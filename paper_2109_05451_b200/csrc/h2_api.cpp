@@ -981,7 +981,10 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     // ---- heap-addressed sweeps (valid when every transfer level is a local standard level:
     //      always for P = 1, and for P > 1 without top-tree couplings)
     {
-        const int TOPN = 64;                     // levels with <= TOPN output nodes are fused
+        // levels with <= TOPN output nodes are fused into one single-CTA launch; one SM streams
+        // only ~1/148 of the HBM bandwidth, so only the tiniest levels are worth fusing
+        const char *tn = getenv("H2_TOPN");
+        const int TOPN = tn ? atoi(tn) : 8;
         const char *sw = getenv("H2_SWEEP");
         h->use_sweep = !h->has_top && !(sw && sw[0] == '0');
         auto lvl_up = [&](int lc) {              // parents at lc - 1, children at lc
