@@ -32,6 +32,9 @@ namespace h2 {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int XCAP_BYTES = 4096;   // per-warp staging of the stacked x in the Simt stream
+#ifndef H2_SPLIT_MINB
+#define H2_SPLIT_MINB 2
+#endif
 constexpr int ZLD = KMAX + 4;   // smem leading dimension of the z hand-over (2 wavefronts per
                                 // DMMA B-fragment load: no extra bank conflicts)
 
@@ -351,11 +354,22 @@ struct BCursor {
     MmaDesc d;
 };
 
+#ifndef H2_APF
+#define H2_APF 8          // k-steps of L2 prefetch ahead of the A fragment loads (0 = off)
+#endif
 template <int MT, int NT>
 __device__ __forceinline__ void mma_load_step(MmaFrag<MT, NT> &f, const double *__restrict__ A, int r, int K,
                                               int ks, int g, int t, const BCursor &cur, int nvc, int lda)
 {
     const int col = ks * 4 + t;
+    if (H2_APF > 0) {
+        // L2 prefetch of the A columns H2_APF k-steps ahead: lanes g < ceil(8 MT / 16) each
+        // touch one 128-byte line of their column (no registers, no wait)
+        const int pcol = (ks + H2_APF) * 4 + t;
+        const int prow = g * 16;
+        if (pcol < K && prow < r && g < (MT * 8 + 15) / 16)
+            asm volatile("prefetch.global.L2 [%0];\n" ::"l"(A + (int64_t)pcol * lda + prow));
+    }
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
         const int row = mt * 8 + g;
@@ -1366,7 +1380,7 @@ k_mega_down(const SchedEntry *__restrict__ sched, int nsched, const __grid_const
 // owning 32 rows of U_t and of the dense row (lda = m), so the accumulator is Mma<4,NT> instead
 // of Mma<8,NT> (no register spills, twice the warps in flight).  z_t is computed by both.
 template <typename T, typename EngK, typename EngH>
-__global__ void __launch_bounds__(WPB * 32, 2)
+__global__ void __launch_bounds__(WPB * 32, H2_SPLIT_MINB)
 k_leaf_dense_split(const Task *__restrict__ ltasks, const Task *__restrict__ dtasks, int ntask2,
                    const Blk *__restrict__ blks, const T *__restrict__ yh, int64_t yh_ld,
                    const CallArgs<T> *__restrict__ args, const T *__restrict__ halo, int nv, int k, int kp, int m)
