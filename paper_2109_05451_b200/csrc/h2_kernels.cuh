@@ -31,6 +31,10 @@
 namespace h2 {
 
 constexpr unsigned FULL = 0xffffffffu;
+#ifndef H2_APF
+#define H2_APF 8          // k-steps of L2 prefetch ahead of the DMMA A-fragment loads (0 = off;
+                          // the same prefetch in the SIMT streams measured slower)
+#endif
 constexpr int XCAP_BYTES = 4096;   // per-warp staging of the stacked x in the Simt stream
 #ifndef H2_SPLIT_MINB
 #define H2_SPLIT_MINB 2
@@ -354,9 +358,6 @@ struct BCursor {
     MmaDesc d;
 };
 
-#ifndef H2_APF
-#define H2_APF 8          // k-steps of L2 prefetch ahead of the A fragment loads (0 = off)
-#endif
 template <int MT, int NT>
 __device__ __forceinline__ void mma_load_step(MmaFrag<MT, NT> &f, const double *__restrict__ A, int r, int K,
                                               int ks, int g, int t, const BCursor &cur, int nvc, int lda)
