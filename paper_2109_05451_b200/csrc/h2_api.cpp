@@ -274,6 +274,8 @@ struct h2_ctx {
     int32_t *d_counters = nullptr;
     // heap-addressed sweeps (k_sweep): bottom levels one launch each, small top levels fused
     bool use_sweep = false;
+    bool subtree_on = false;         // H2_SUBTREE=1: leaf projection fused with the first levels
+                                     // (measured neutral / slower on cfg2 in round 1)
     std::vector<SweepParams> up_sweeps, dn_sweeps;
     std::vector<int> up_sweep_ctas, dn_sweep_ctas;
     int sweep_r_up = 1, sweep_r_dn = 1;
@@ -985,6 +987,8 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         // only ~1/148 of the HBM bandwidth, so only the tiniest levels are worth fusing
         const char *tn = getenv("H2_TOPN");
         const int TOPN = tn ? atoi(tn) : 8;
+        const char *stv = getenv("H2_SUBTREE");
+        h->subtree_on = stv && stv[0] == '1';
         const char *sw = getenv("H2_SWEEP");
         h->use_sweep = !h->has_top && !(sw && sw[0] == '0');
         auto lvl_up = [&](int lc) {              // parents at lc - 1, children at lc
@@ -1336,9 +1340,26 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
         if (h->prof) h->ev_used += NEV;
         return H2_OK;
     }
-    // 1. upsweep of the local branch (PAPER.md:281 / alg:upsweep2)
-    H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
-                                 h->up_leaf.r, st));
+    // 1. upsweep of the local branch (PAPER.md:281 / alg:upsweep2): the leaf projection fused
+    //    with the first J transfer levels (warp-level subtrees), when those are standard levels
+    int J = 0;
+    if (h->use_sweep && h->subtree_on) {
+        const int want = nv <= 4 ? 2 : 1;
+        bool ok = (int)h->up_sweeps.size() >= want && (h->nleaf % (1 << want)) == 0;
+        for (int u = 0; ok && u < want; ++u) ok = h->up_sweeps[u].nlev == 1 && h->up_sweep_ctas[u] > 1;
+        if (ok) J = want;
+    }
+    if (J > 0) {
+        SweepParams sp{};
+        sp.nlev = J;
+        int rmax = h->up_leaf.r;
+        for (int u = 0; u < J; ++u) { sp.lv[u] = h->up_sweeps[u].lv[0]; rmax = std::max(rmax, (int)sp.lv[u].r); }
+        H2_CUDA(h, launch_up_subtree<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv, rmax, J,
+                                        sp, st));
+    } else {
+        H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
+                                     h->up_leaf.r, st));
+    }
     // 1b. leaf-level coupling (diagonal part) as soon as x^ of the leaves exists (alg:mult's
     //     levels are independent), on its own stream
     H2_CUDA(h, cudaEventRecord(h->ev_upleaf, st));
@@ -1351,7 +1372,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     H2_CUDA(h, cudaEventRecord(h->ev_leafc, s_leafc));
     H2_MARK(1);
     if (h->use_sweep) {
-        for (size_t u = 0; u < h->up_sweeps.size(); ++u)
+        for (size_t u = J; u < h->up_sweeps.size(); ++u)
             H2_CUDA(h, launch_sweep<T>(MODE_WRITE, h->up_sweeps[u], h->up_sweep_ctas[u],
                                        h->up_sweep_ctas[u] == 1 && h->up_sweeps[u].nlev > 1 ? 512 : WPB * 32,
                                        xh, h->xh_plane, nv, h->sweep_r_up, st));

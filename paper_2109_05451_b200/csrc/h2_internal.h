@@ -170,6 +170,11 @@ cudaError_t launch_mega_down(const SchedEntry *sched, int n, const MegaParams &m
                              const Task *dtasks, const Blk *blks, T *yh, int64_t yh_ld, const T *halo,
                              int32_t *flags, CallArgs<T> *args, int nv, int m, int grid, cudaStream_t s);
 
+// leaf projection fused with the first J (1 or 2) upsweep levels; lv.lv[j-1] = level q-j
+template <typename T>
+cudaError_t launch_up_subtree(const Task *leaf_tasks, int nleaf, const Blk *b, const CallArgs<T> *args, T *xh,
+                              int64_t xh_ld, int nv, int r, int J, const SweepParams &lv, cudaStream_t s);
+
 // L2 prefetch of byte ranges (the small top-level transfers, read late in the chain)
 constexpr int PREFETCH_MAX = 64;
 struct PrefetchList {

@@ -823,6 +823,66 @@ k_up_leaf(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blk
     }
 }
 
+// Leaf projection fused with the first J upsweep levels: one warp owns a
+// subtree of 2^J sibling leaves, computes their x^ (written for the coupling), and sweeps the J
+// levels above in warp shared memory -- no launch and no global round trip for those levels.
+// Heap addressing: leaf slots g 2^J .. (g+1) 2^J - 1; level (q-j) slots g 2^(J-j) ...
+template <typename T, typename Eng, int J>
+__global__ void __launch_bounds__(WPB * 32, Eng::MINB < 2 ? Eng::MINB : 2)
+k_up_subtree(const Task *__restrict__ leaf_tasks, int ngroups, const Blk *__restrict__ blks,
+             const CallArgs<T> *__restrict__ args, T *__restrict__ xh, int64_t xh_ld, int nv, int SLD,
+             const __grid_constant__ SweepParams lv)     // lv.lv[j-1]: level produced at step j
+{
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int NV = Eng::NV;
+    constexpr int NODES = 1 << J;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int grp = blockIdx.x * WPB + wid;
+    if (grp >= ngroups) return;
+    // warp smem: NODES node slots of (SLD x NV), SLD = max rank + 1 (odd: fewer bank conflicts)
+    T *sm = reinterpret_cast<T *>(smem_raw) + (size_t)wid * NODES * NV * SLD;
+    const T *__restrict__ X = args->X;
+    const int64_t ldx = args->ldx;
+    for (int n0 = 0; n0 < nv; n0 += NV) {
+        const int nvc = min(NV, nv - n0);
+        // leaves
+        for (int u = 0; u < NODES; ++u) {
+            const Task tk = leaf_tasks[grp * NODES + u];
+            const Blk b = blks[tk.blk0];
+            typename Eng::Acc acc;
+            acc_zero(acc, lane);
+            Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.c, X + b.x + (int64_t)n0 * ldx, ldx, b.xrows,
+                       nvc, lane);
+            acc_store(acc, xh + tk.out + (int64_t)n0 * xh_ld, xh_ld, tk.r, nvc, lane);
+            __syncwarp();
+            acc_store(acc, sm + (size_t)u * NV * SLD, (int64_t)SLD, tk.r, nvc, lane);
+        }
+        // J levels up, in shared memory (children of slot i are slots 2i, 2i+1; results reuse slot 2i)
+#pragma unroll
+        for (int j = 1; j <= J; ++j) {
+            const SweepLevel L = lv.lv[j - 1];
+            const int64_t blk = (int64_t)L.r * L.c;
+            const int np = NODES >> j;
+            for (int i = 0; i < np; ++i) {
+                const int pslot = grp * np + i;            // parent slot within its level
+                typename Eng::Acc acc;
+                acc_zero(acc, lane);
+                __syncwarp();
+#pragma unroll
+                for (int ch = 0; ch < 2; ++ch) {
+                    const int cs = (2 * i + ch) << (j - 1);  // smem slot holding child 2i+ch
+                    Eng::block(acc, static_cast<const T *>(L.A) + (2 * (int64_t)pslot + ch) * blk, L.r, L.c,
+                               sm + (size_t)cs * NV * SLD, (int64_t)SLD, L.c, nvc, lane);
+                }
+                acc_store(acc, xh + L.obase + (int64_t)pslot * L.r + (int64_t)n0 * xh_ld, xh_ld, L.r, nvc, lane);
+                __syncwarp();
+                acc_store(acc, sm + (size_t)((2 * i) << (j - 1)) * NV * SLD, (int64_t)SLD, L.r, nvc, lane);
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // ---------------------------------------------------------------------------------------
 // Generic row tasks whose x operands and output live in the x^/y^ workspaces:
 //   MODE_WRITE  out  = sum_b A_b x_b    (upsweep transfers, coupling multiply)
@@ -1807,6 +1867,36 @@ cudaError_t launch_dense_t(const Task *t, int ntask, const Blk *b, const CallArg
         if (err != cudaSuccess) return;
         const int grid = max_ctas > 0 ? min(grid_for(ntask), max_ctas) : grid_for(ntask);
         kd<<<grid, WPB * 32, sm, s>>>(t, ntask, b, args, halo, nv);
+    });
+    if (err != cudaSuccess) return err;
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_up_subtree(const Task *leaf_tasks, int nleaf, const Blk *b, const CallArgs<T> *args, T *xh,
+                              int64_t xh_ld, int nv, int r, int J, const SweepParams &lv, cudaStream_t s)
+{
+    if (nleaf == 0) return cudaSuccess;
+    cudaError_t err = cudaSuccess;
+    Dispatch<T>::run(r, nv, [&](auto e) {
+        using E = decltype(e);
+        auto go = [&](auto jc) {
+            constexpr int JJ = decltype(jc)::value;
+            auto kern = k_up_subtree<T, E, JJ>;
+            const int sld = r | 1;
+            const size_t sm = (size_t)WPB * (1 << JJ) * E::NV * sld * sizeof(T);
+            static bool attr_set = false;       // sized once for the largest rank (KMAX + 1)
+            if (!attr_set) {
+                const size_t smax = (size_t)WPB * (1 << JJ) * E::NV * (KMAX + 1) * sizeof(T);
+                err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
+                attr_set = (err == cudaSuccess);
+            }
+            const int ng = nleaf >> JJ;
+            if (err == cudaSuccess)
+                kern<<<grid_for(ng), WPB * 32, sm, s>>>(leaf_tasks, ng, b, args, xh, xh_ld, nv, sld, lv);
+        };
+        if (J == 2) go(std::integral_constant<int, 2>{});
+        else go(std::integral_constant<int, 1>{});
     });
     if (err != cudaSuccess) return err;
     return cudaGetLastError();
