@@ -305,6 +305,8 @@ struct h2_ctx {
     int tma_mode = 0;                // H2_TMA: 0 never, 1 always, 2 for nv <= 4 only
     int bw_ctas = 0;                 // grid cap of the side-stream bandwidth kernels (H2_BW_CTAS)
     bool one_side = false;           // leaf-level coupling queued behind the dense kernel (H2_ONE_SIDE)
+    bool leafc_serial = false;       // leaf-level coupling on the main stream (H2_LEAFC_SERIAL=1)
+    int prio_lo = 0, prio_hi = 0;    // per-launch priorities (H2_PRIO=1): side bandwidth / sweep chain
     bool tma_on(int nv) const { return tma_mode == 1 || (tma_mode == 2 && nv <= 4); }
     cudaStream_t cap_stream = nullptr;
     cudaStream_t last_stream = nullptr;
@@ -514,6 +516,10 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         const char *bc = getenv("H2_BW_CTAS");      // per SM; default 0 = uncapped grid
         h->bw_ctas = (bc ? atoi(bc) : 0) * nsm;
+        const char *pr = getenv("H2_PRIO");
+        if (pr && pr[0] == '1') { h->prio_lo = least; h->prio_hi = greatest; }
+        const char *ls = getenv("H2_LEAFC_SERIAL");
+        h->leafc_serial = ls && ls[0] == '1';
         const char *os = getenv("H2_ONE_SIDE");
         h->one_side = os && os[0] == '1';
     }
@@ -1267,7 +1273,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     // profiling serializes the side streams onto the main one so every phase's events bracket
     // only its own kernels (clean per-kernel durations for the roofline)
     cudaStream_t s_dense = h->prof ? st : h->s_dense;
-    cudaStream_t s_leafc = h->prof ? st : (h->one_side ? h->s_dense : h->s_leafc);
+    cudaStream_t s_leafc = (h->prof || h->leafc_serial) ? st : (h->one_side ? h->s_dense : h->s_leafc);
     // 0. fork: the dense near field runs on its own low-priority stream from the start, in
     //    parallel with the tree phases; for P > 1 the x-leaf halo it needs is
     //    exchanged first on the comm stream (X is an input, so it can start at t = 0)
@@ -1365,12 +1371,15 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     H2_CUDA(h, cudaEventRecord(h->ev_upleaf, st));
     H2_CUDA(h, cudaStreamWaitEvent(s_leafc, h->ev_upleaf, 0));
     if ((rc = mark(h, 11, s_leafc)) != H2_OK) return rc;
+    g_launch_priority = h->prio_lo;
     for (const Phase &ph : h->coup_leaf)
         H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
                                   nv, ph.r, h->tma_on(nv), h->bw_ctas, s_leafc));
+    g_launch_priority = 0;
     if ((rc = mark(h, 12, s_leafc)) != H2_OK) return rc;
     H2_CUDA(h, cudaEventRecord(h->ev_leafc, s_leafc));
     H2_MARK(1);
+    g_launch_priority = h->prio_hi;
     if (h->use_sweep) {
         for (size_t u = J; u < h->up_sweeps.size(); ++u)
             H2_CUDA(h, launch_sweep<T>(MODE_WRITE, h->up_sweeps[u], h->up_sweep_ctas[u],
@@ -1384,6 +1393,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
         for (const auto &sg : h->up_stages)
             H2_CUDA(h, launch_tree<T>(MODE_WRITE, sg.st, sg.nctas, h->d_tasks, h->d_blks, xh, h->xh_plane, nv,
                                       sg.r, st));
+    g_launch_priority = 0;
     H2_MARK(2);
     // 2. exchange (P > 1): pack my x^ nodes that peers need, one NCCL group on the comm stream,
     //    overlapped with the diagonal multiply (alg:optimized_dist_mult)

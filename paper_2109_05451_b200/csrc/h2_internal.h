@@ -108,6 +108,11 @@ cudaError_t launch_pack(const PackSeg *segs, int64_t nseg, const T *src, int64_t
 
 enum { MODE_WRITE = 0, MODE_ACCUM = 1 };
 
+// Launch priority for the next launches (0 = the stream's own).  Set by the host plan around the
+// side-stream bandwidth kernels (low) and the sweep chain (high); applied with
+// cudaLaunchKernelEx + cudaLaunchAttributePriority so it is also recorded in captured graphs.
+inline int g_launch_priority = 0;
+
 // A fused run of consecutive tree levels (see k_tree): per level, the first task of the phase
 // and the number of tasks each CTA owns.
 constexpr int TREE_MAXLEV = 8;

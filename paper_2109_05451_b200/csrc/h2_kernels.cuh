@@ -25,6 +25,7 @@
 #include "h2_internal.h"
 
 #include <algorithm>
+#include <utility>
 #include <cstdlib>
 #include <type_traits>
 
@@ -1618,6 +1619,28 @@ __global__ void k_pack(const PackSeg *__restrict__ segs, int64_t nseg, const T *
 // dispatch: Simt for float or nv <= 4; Mma (DMMA) for double with nv >= 5
 static inline int grid_for(int ntask) { return (ntask + WPB - 1) / WPB; }
 
+// kernel<<<grid, block, smem, s>>>(args...) with the per-launch priority g_launch_priority
+template <typename... KArgs, typename... Args>
+static inline void launch_pri(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
+                              Args &&...args)
+{
+    if (g_launch_priority == 0) {
+        kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = g_launch_priority;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 template <typename T>
 struct Dispatch {
     // f(Eng) with Eng chosen from (rows r -> RPL / MT, nv -> NVB / NT)
@@ -1712,9 +1735,9 @@ cudaError_t launch_rows_t(int mode, const Task *t, int ntask, const Blk *b, cons
         if (err != cudaSuccess) return;
         const int grid = max_ctas > 0 ? min(grid_for(ntask), max_ctas) : grid_for(ntask);
         if (mode == MODE_WRITE)
-            kw<<<grid, WPB * 32, sm, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv);
+            launch_pri(kw, grid, WPB * 32, sm, s, t, ntask, b, src, src_ld, dst, dst_ld, nv);
         else
-            ka<<<grid, WPB * 32, sm, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv);
+            launch_pri(ka, grid, WPB * 32, sm, s, t, ntask, b, src, src_ld, dst, dst_ld, nv);
     });
     if (err != cudaSuccess) return err;
     return cudaGetLastError();
@@ -1943,8 +1966,8 @@ cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads,
     if (p.nlev == 0 || nctas == 0) return cudaSuccess;
     Dispatch<T>::run(r, nv, [&](auto e) {
         using E = decltype(e);
-        if (mode == MODE_WRITE) k_sweep<T, E, MODE_WRITE><<<nctas, threads, 0, s>>>(p, buf, ld, nv);
-        else                    k_sweep<T, E, MODE_ACCUM><<<nctas, threads, 0, s>>>(p, buf, ld, nv);
+        if (mode == MODE_WRITE) launch_pri(k_sweep<T, E, MODE_WRITE>, nctas, threads, 0, s, p, buf, ld, nv);
+        else                    launch_pri(k_sweep<T, E, MODE_ACCUM>, nctas, threads, 0, s, p, buf, ld, nv);
     });
     return cudaGetLastError();
 }
