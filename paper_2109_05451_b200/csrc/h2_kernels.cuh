@@ -758,6 +758,7 @@ struct Simt {
     // streaming engines are latency-bound at 2 CTAs (16 warps, 25 % occupancy; ncu round 1)
     static constexpr int MINB = NVB <= 2 ? (RPL == 1 ? 4 : 3) : 2;
     static constexpr bool SIMT1 = (RPL == 1 && NVB == 1);
+    static constexpr bool MMA = false;
     static constexpr int SCRATCH = XCAP_BYTES;      // per-warp smem for the stream staging
     __device__ static void block(Acc &acc, const T *A, int r, int c, const T *src, int64_t ld, int xrows,
                                  int nvc, int lane, int lda = -1)
@@ -781,6 +782,7 @@ struct Mma {
     static constexpr int NV = 8 * NT;
     static constexpr int MINB = 2;
     static constexpr bool SIMT1 = false;
+    static constexpr bool MMA = true;
     static constexpr int SCRATCH = 32 * sizeof(MmaDesc);
     __device__ static void block(Acc &acc, const double *A, int r, int c, const double *src, int64_t ld,
                                  int xrows, int nvc, int lane, int lda = -1)
@@ -954,10 +956,17 @@ k_sweep(const __grid_constant__ SweepParams p, T *__restrict__ buf, int64_t ld, 
                                buf + L.xbase + (int64_t)(i >> 1) * L.c + (int64_t)n0 * ld, ld, L.c, nvc, lane);
                 } else {
                     acc_zero(acc, lane);
+                    const T *A2 = static_cast<const T *>(L.A) + 2 * (int64_t)i * blk;
+                    const T *x2 = buf + L.xbase + 2 * (int64_t)i * L.c + (int64_t)n0 * ld;
+                    if constexpr (!Eng::MMA) {
 #pragma unroll
-                    for (int ch = 0; ch < 2; ++ch)
-                        Eng::block_wide(acc, static_cast<const T *>(L.A) + (2 * (int64_t)i + ch) * blk, L.r, L.c,
-                                   buf + L.xbase + (2 * (int64_t)i + ch) * L.c + (int64_t)n0 * ld, ld, L.c, nvc, lane);
+                        for (int ch = 0; ch < 2; ++ch)
+                            Eng::block_wide(acc, A2 + ch * blk, L.r, L.c, x2 + ch * L.c, ld, L.c, nvc, lane);
+                    } else {
+                        // the two children's Ft blocks (r x c each, column-major, adjacent) form
+                        // one r x 2c block over the two adjacent child x^ slots
+                        Eng::block_wide(acc, A2, L.r, 2 * L.c, x2, ld, 2 * L.c, nvc, lane);
+                    }
                 }
                 acc_store(acc, out, ld, L.r, nvc, lane);
             }
