@@ -32,6 +32,13 @@
 namespace h2 {
 
 constexpr unsigned FULL = 0xffffffffu;
+#ifndef H2_SSTAGE_DEFAULT
+#define H2_SSTAGE_DEFAULT 0x7fffffff   // SIMT engines: cp.async-staged transfer sweeps for every
+#endif                                 // level (cfg2 nv = 1: 1.083 -> 1.030 ms)
+#ifndef H2_SSTAGE_MMA_DEFAULT
+#define H2_SSTAGE_MMA_DEFAULT 0        // DMMA engines: never (measured slower at every threshold)
+#endif
+constexpr size_t SWEEP_STAGE_SMEM = 200 * 1024;   // dynamic smem cap of a staged k_sweep CTA
 #ifndef H2_APF
 #define H2_APF 8          // k-steps of L2 prefetch ahead of the DMMA A-fragment loads (0 = off;
                           // the same prefetch in the SIMT streams measured slower)
@@ -770,6 +777,18 @@ struct Simt {
     __device__ static void stream(Acc &acc, const T *A0, int r, int c, int nblk, const Blk *blks,
                                   const Src<T> &src, int nvc, int lane, void *scratch)
     { simt_stream<T, RPL, NVB>(acc, A0, r, c, nblk, blks, src, nvc, lane, (T *)scratch, XCAP_BYTES / (int)sizeof(T)); }
+    // acc += As (r x c, col-major ld r, shared) * xs (c x nvc, ld xld, shared)
+    __device__ static void smem_block(Acc &acc, const T *As, int r, int c, const T *xs, int xld, int nvc, int lane)
+    {
+        acc.each(lane, [&](int row, int n, T &v) {
+            if (row < r && n < nvc) {
+                T s = v;
+#pragma unroll 8
+                for (int j = 0; j < c; ++j) s = fma(As[j * r + row], xs[j + n * xld], s);
+                v = s;
+            }
+        });
+    }
     static constexpr int TSCRATCH = XCAP_BYTES;     // per-warp smem next to the TMA ring
     __device__ static void tstream(Acc &acc, const T *A0, int r, int c, int nblk, const Blk *blks,
                                    const Src<T> &src, int nvc, int lane, TmaRing &rg, void *scratch)
@@ -793,6 +812,9 @@ struct Mma {
     __device__ static void stream(Acc &acc, const double *A0, int r, int c, int nblk, const Blk *blks,
                                   const Src<double> &src, int nvc, int lane, void *scratch, int lda = -1)
     { mma_stream<MT, NT>(acc, A0, r, c, nblk, blks, src, nvc, lane, (MmaDesc *)scratch, lda); }
+    __device__ static void smem_block(Acc &acc, const double *As, int r, int c, const double *xs, int xld, int nvc,
+                                      int lane)
+    { mma_block<MT, NT, false>(acc, As, r, c, xs, xld, c, nvc, lane, r); }
     static constexpr int TSCRATCH = 32 * sizeof(MmaDesc);
     __device__ static void tstream(Acc &acc, const double *A0, int r, int c, int nblk, const Blk *blks,
                                    const Src<double> &src, int nvc, int lane, TmaRing &rg, void *scratch)
@@ -937,14 +959,62 @@ k_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
 // Heap-addressed transfer sweep (see SweepParams): one warp per output node, no descriptor
 // loads -- the A blocks and x operands are computed from the slot index, so a task is a single
 // round of independent loads.  nlev > 1 only with one CTA (barrier between levels).
-template <typename T, typename Eng, int MODE>
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T *dst, const T *src)
+{
+    if constexpr (sizeof(T) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all()
+{
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+template <typename T, typename Eng, int MODE, bool STAGE>
 __global__ void __launch_bounds__(512, 1)
-k_sweep(const __grid_constant__ SweepParams p, T *__restrict__ buf, int64_t ld, int nv)
+k_sweep(const __grid_constant__ SweepParams p, T *__restrict__ buf, int64_t ld, int nv, int wstride)
 {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int lv = 0; lv < p.nlev; ++lv) {
         const SweepLevel L = p.lv[lv];
         const int64_t blk = (int64_t)L.r * L.c;
+        if constexpr (STAGE) {
+            // latency-bound levels: the node's whole operand set (its transfer block(s) and source
+            // x^ slots, r x cc and cc x nvc) is pulled into the warp's shared memory by cp.async
+            // in ONE round of independent copies, then multiplied from shared memory -- one HBM
+            // round trip per node instead of one per pipelined k-step group
+            extern __shared__ __align__(128) unsigned char smem_raw[];
+            T *As = reinterpret_cast<T *>(smem_raw) + (int64_t)wid * wstride;
+            const int cc = MODE == MODE_ACCUM ? L.c : 2 * L.c;
+            T *xs = As + L.r * cc;
+            for (int i = blockIdx.x * nw + wid; i < L.n; i += gridDim.x * nw) {
+                const T *Ag = static_cast<const T *>(L.A) + (MODE == MODE_ACCUM ? (int64_t)i : 2 * (int64_t)i) * blk;
+                const T *xg = buf + L.xbase + (MODE == MODE_ACCUM ? (int64_t)(i >> 1) : 2 * (int64_t)i) * L.c;
+                for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
+                    const int nvc = min(Eng::NV, nv - n0);
+                    T *out = buf + L.obase + (int64_t)i * L.r + (int64_t)n0 * ld;
+                    __syncwarp();
+                    if (n0 == 0)
+                        for (int e = lane; e < L.r * cc; e += 32) cp_async_elem(As + e, Ag + e);
+                    for (int e = lane; e < cc * nvc; e += 32) {
+                        const int n = e / cc, j = e - n * cc;
+                        cp_async_elem(xs + e, xg + j + (int64_t)(n0 + n) * ld);
+                    }
+                    typename Eng::Acc acc;
+                    if (MODE == MODE_ACCUM) acc_load(acc, out, ld, L.r, nvc, lane);
+                    else                    acc_zero(acc, lane);
+                    cp_async_wait_all();
+                    __syncwarp();
+                    Eng::smem_block(acc, As, L.r, cc, xs, cc, nvc, lane);
+                    acc_store(acc, out, ld, L.r, nvc, lane);
+                }
+            }
+            if (p.nlev > 1) __syncthreads();
+            continue;
+        }
         for (int i = blockIdx.x * nw + wid; i < L.n; i += gridDim.x * nw) {
             for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
                 const int nvc = min(Eng::NV, nv - n0);
@@ -1973,11 +2043,46 @@ cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads,
                          int r, cudaStream_t s)
 {
     if (p.nlev == 0 || nctas == 0) return cudaSuccess;
+    // H2_SSTAGE: launches whose levels all have <= this many nodes use the cp.async-staged
+    // variant (default: see DESIGN.md section 5)
+    // (SIMT engines) / H2_SSTAGE_MMA (DMMA engines)
+    static const long stage_simt = getenv("H2_SSTAGE") ? atol(getenv("H2_SSTAGE")) : (long)H2_SSTAGE_DEFAULT;
+    static const long stage_mma = getenv("H2_SSTAGE_MMA") ? atol(getenv("H2_SSTAGE_MMA")) : (long)H2_SSTAGE_MMA_DEFAULT;
+    int maxn = 0, rmax = 0, cmax = 0;
+    for (int l = 0; l < p.nlev; ++l) {
+        maxn = std::max(maxn, (int)p.lv[l].n);
+        rmax = std::max(rmax, (int)p.lv[l].r);
+        cmax = std::max(cmax, (int)p.lv[l].c);
+    }
+    const int cc = mode == MODE_ACCUM ? cmax : 2 * cmax;
+    cudaError_t err = cudaSuccess;
     Dispatch<T>::run(r, nv, [&](auto e) {
         using E = decltype(e);
-        if (mode == MODE_WRITE) launch_pri(k_sweep<T, E, MODE_WRITE>, nctas, threads, 0, s, p, buf, ld, nv);
-        else                    launch_pri(k_sweep<T, E, MODE_ACCUM>, nctas, threads, 0, s, p, buf, ld, nv);
+        const int wstride = ((rmax * cc + cc * E::NV) + 1) & ~1;          // elements, 16-byte multiple
+        const size_t wbytes = (size_t)wstride * sizeof(T);
+        int warps = threads / 32;
+        while (warps > 1 && warps * wbytes > SWEEP_STAGE_SMEM) warps >>= 1;
+        const bool stage = maxn <= (E::MMA ? stage_mma : stage_simt) && warps * wbytes <= SWEEP_STAGE_SMEM;
+        if (stage) {
+            const int ctas = nctas == 1 ? 1 : (int)((maxn + warps - 1) / warps);
+            const size_t sm = warps * wbytes;
+            auto kw = k_sweep<T, E, MODE_WRITE, true>;
+            auto ka = k_sweep<T, E, MODE_ACCUM, true>;
+            static bool attr_set = false;          // once per engine, for both modes
+            if (!attr_set) {
+                err = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SWEEP_STAGE_SMEM);
+                if (err == cudaSuccess)
+                    err = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SWEEP_STAGE_SMEM);
+                attr_set = (err == cudaSuccess);
+            }
+            if (err == cudaSuccess)
+                launch_pri(mode == MODE_WRITE ? kw : ka, ctas, warps * 32, sm, s, p, buf, ld, nv, wstride);
+        } else {
+            if (mode == MODE_WRITE) launch_pri(k_sweep<T, E, MODE_WRITE, false>, nctas, threads, 0, s, p, buf, ld, nv, 0);
+            else                    launch_pri(k_sweep<T, E, MODE_ACCUM, false>, nctas, threads, 0, s, p, buf, ld, nv, 0);
+        }
     });
+    if (err != cudaSuccess) return err;
     return cudaGetLastError();
 }
 
