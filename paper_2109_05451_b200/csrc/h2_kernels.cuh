@@ -978,6 +978,11 @@ __global__ void __launch_bounds__(512, 1)
 k_sweep(const __grid_constant__ SweepParams p, T *__restrict__ buf, int64_t ld, int nv, int wstride)
 {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // programmatic dependent launch: the next level's grid may be scheduled now (its CTAs wait
+    // below for this grid's completion and memory flush), hiding the per-level launch latency;
+    // a no-op when launched without the attribute
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     for (int lv = 0; lv < p.nlev; ++lv) {
         const SweepLevel L = p.lv[lv];
         const int64_t blk = (int64_t)L.r * L.c;
@@ -1698,6 +1703,30 @@ __global__ void k_pack(const PackSeg *__restrict__ segs, int64_t nseg, const T *
 // dispatch: Simt for float or nv <= 4; Mma (DMMA) for double with nv >= 5
 static inline int grid_for(int ntask) { return (ntask + WPB - 1) / WPB; }
 
+// kernel launch with programmatic stream serialization (PDL): the kernel may start before its
+// in-stream predecessor completes and must execute griddepcontrol.wait before reading its output
+template <typename... KArgs, typename... Args>
+static inline void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
+                              Args &&...args)
+{
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na++].val.programmaticStreamSerializationAllowed = 1;
+    if (g_launch_priority != 0) {
+        at[na].id = cudaLaunchAttributePriority;
+        at[na++].val.priority = g_launch_priority;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // kernel<<<grid, block, smem, s>>>(args...) with the per-launch priority g_launch_priority
 template <typename... KArgs, typename... Args>
 static inline void launch_pri(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
@@ -2055,6 +2084,11 @@ cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads,
         cmax = std::max(cmax, (int)p.lv[l].c);
     }
     const int cc = mode == MODE_ACCUM ? cmax : 2 * cmax;
+    static const bool pdl = !(getenv("H2_PDL") && getenv("H2_PDL")[0] == '0');
+    auto launch = [&](auto kern, int grid, int block, size_t sm, int wstride) {
+        if (pdl) launch_pdl(kern, grid, block, sm, s, p, buf, ld, nv, wstride);
+        else     launch_pri(kern, grid, block, sm, s, p, buf, ld, nv, wstride);
+    };
     cudaError_t err = cudaSuccess;
     Dispatch<T>::run(r, nv, [&](auto e) {
         using E = decltype(e);
@@ -2075,11 +2109,10 @@ cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads,
                     err = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SWEEP_STAGE_SMEM);
                 attr_set = (err == cudaSuccess);
             }
-            if (err == cudaSuccess)
-                launch_pri(mode == MODE_WRITE ? kw : ka, ctas, warps * 32, sm, s, p, buf, ld, nv, wstride);
+            if (err == cudaSuccess) launch(mode == MODE_WRITE ? kw : ka, ctas, warps * 32, sm, wstride);
         } else {
-            if (mode == MODE_WRITE) launch_pri(k_sweep<T, E, MODE_WRITE, false>, nctas, threads, 0, s, p, buf, ld, nv, 0);
-            else                    launch_pri(k_sweep<T, E, MODE_ACCUM, false>, nctas, threads, 0, s, p, buf, ld, nv, 0);
+            launch(mode == MODE_WRITE ? k_sweep<T, E, MODE_WRITE, false> : k_sweep<T, E, MODE_ACCUM, false>, nctas,
+                   threads, 0, 0);
         }
     });
     if (err != cudaSuccess) return err;
