@@ -38,7 +38,7 @@ def build(force=False, verbose=False):
     objs = []
     common = ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I" + inc,
                      "-I" + os.path.join(ROOT, "include"),
-                     '-DH2_NCCL_DEFAULT="%s"' % ncclso]
+                     '-DH2_NCCL_DEFAULT="%s"' % ncclso] + os.environ.get("H2_NVCC_DEFS", "").split()
     procs = []
     for src in SOURCES:                       # compile the translation units in parallel
         obj = os.path.join(CSRC, os.path.basename(src) + ".o")

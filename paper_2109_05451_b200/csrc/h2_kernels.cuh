@@ -40,7 +40,7 @@ constexpr unsigned FULL = 0xffffffffu;
 #endif
 constexpr size_t SWEEP_STAGE_SMEM = 200 * 1024;   // dynamic smem cap of a staged k_sweep CTA
 #ifndef H2_APF
-#define H2_APF 8          // k-steps of L2 prefetch ahead of the DMMA A-fragment loads (0 = off;
+#define H2_APF 4          // k-steps of L2 prefetch ahead of the DMMA A-fragment loads (0 = off;
                           // the same prefetch in the SIMT streams measured slower)
 #endif
 constexpr int XCAP_BYTES = 4096;   // per-warp staging of the stacked x in the Simt stream
