@@ -1020,11 +1020,20 @@ k_sweep(const __grid_constant__ SweepParams p, T *__restrict__ buf, int64_t ld, 
             if (p.nlev > 1) __syncthreads();
             continue;
         }
-        for (int i = blockIdx.x * nw + wid; i < L.n; i += gridDim.x * nw) {
-            for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
+        // task = (node, vector chunk) when the grid has a warp for each (nv > Eng::NV): the
+        // chunks of one node run on adjacent warps instead of in series on one warp, which is
+        // what bounds the small levels at large k and nv (cfg3s: ~80 us per level otherwise);
+        // the launch sizes the single-level grid by the chunk count (launch_sweep)
+        const int nch = (nv + Eng::NV - 1) / Eng::NV;
+        const int S = (p.nlev > 1 || (int64_t)L.n * nch <= (int64_t)gridDim.x * nw) ? nch : 1;
+        for (int64_t t = (int64_t)blockIdx.x * nw + wid; t < (int64_t)L.n * S; t += (int64_t)gridDim.x * nw) {
+            const int64_t i = t / S;
+            const int ch0 = S == 1 ? 0 : (int)(t - i * S);
+            const int ch1 = S == 1 ? nch : ch0 + 1;
+            for (int n0 = ch0 * Eng::NV; n0 < ch1 * Eng::NV && n0 < nv; n0 += Eng::NV) {
                 const int nvc = min(Eng::NV, nv - n0);
                 typename Eng::Acc acc;
-                T *out = buf + L.obase + (int64_t)i * L.r + (int64_t)n0 * ld;
+                T *out = buf + L.obase + i * L.r + (int64_t)n0 * ld;
                 if (MODE == MODE_ACCUM) {
                     acc_load(acc, out, ld, L.r, nvc, lane);
                     Eng::block_wide(acc, static_cast<const T *>(L.A) + i * blk, L.r, L.c,
@@ -2111,7 +2120,11 @@ cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads,
             }
             if (err == cudaSuccess) launch(mode == MODE_WRITE ? kw : ka, ctas, warps * 32, sm, wstride);
         } else {
-            launch(mode == MODE_WRITE ? k_sweep<T, E, MODE_WRITE, false> : k_sweep<T, E, MODE_ACCUM, false>, nctas,
+            // single-level launches get a warp per (node, vector chunk); see k_sweep
+            static const bool split = !(getenv("H2_SWEEP_SPLIT") && getenv("H2_SWEEP_SPLIT")[0] == '0');
+            const int nch = (nv + E::NV - 1) / E::NV;
+            const int grid = (p.nlev > 1 || !split) ? nctas : nctas * nch;
+            launch(mode == MODE_WRITE ? k_sweep<T, E, MODE_WRITE, false> : k_sweep<T, E, MODE_ACCUM, false>, grid,
                    threads, 0, 0);
         }
     });

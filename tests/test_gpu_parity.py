@@ -151,3 +151,32 @@ def test_cfg2_full_size_sampled(nv):
     ref = oracle.matvec(h, X, 1.0, 0.0, None, leaf_mask=mask)
     rows = np.concatenate([np.arange(h.leaf_ptr[i], h.leaf_ptr[i + 1]) for i in np.flatnonzero(mask)])
     assert colmax_rel(out[:, rows], ref[:, rows]) <= TOL64
+
+
+def test_cfg3_structure_small():
+    """cfg3's structure (3D Gaussian, k = 4^3 = 64, eta = 1.1; readings R5, R8, R9) at nv = 64 on
+    a 16x16x32 grid (128 leaves): every element against the oracle, alpha and beta nonzero."""
+    h = build_config("cfg3", points=("grid", (16, 16, 32)))
+    assert h.ranks[-1] == 64 and h.dim == 3
+    op = _op(h, nv_max=64)
+    X = make_xy(h.perm, 64, 8, -1.0, 1.0)
+    Y0 = make_xy(h.perm, 64, 8, -1.0, 1.0, stream=1)
+    ref = oracle.matvec(h, X, 0.8, 1.5, Y0)
+    out = gpu_matvec(op, X, 0.8, 1.5, Y0)
+    assert colmax_rel(out, ref) <= TOL64
+
+
+@pytest.mark.slow
+def test_cfg3s_full_size_sampled():
+    """bench.py --config cfg3s at its full size (64^3 points, nv = 64, nv_max = 64): sampled-row
+    oracle on 2% of the leaves, alpha=1, beta=0."""
+    h = build_config("cfg3", points=("grid", (64, 64, 64)))
+    op = _op(h, nv_max=64)
+    X = make_xy(h.perm, 64, 3, 0.0, 1.0)
+    out = gpu_matvec(op, X, 1.0, 0.0, np.zeros_like(X))
+    mask = np.zeros(1 << h.q, dtype=bool)
+    mask[np.random.default_rng(1).choice(mask.size, mask.size // 50, replace=False)] = True
+    mask[[0, -1]] = True
+    ref = oracle.matvec(h, X, 1.0, 0.0, None, leaf_mask=mask)
+    rows = np.concatenate([np.arange(h.leaf_ptr[i], h.leaf_ptr[i + 1]) for i in np.flatnonzero(mask)])
+    assert colmax_rel(out[:, rows], ref[:, rows]) <= TOL64
