@@ -919,15 +919,21 @@ k_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (blockIdx.x * WPB + wid >= ntask) return;
+    // (row, vector chunk) tasks when the launcher sized the grid for them (H2_ROWS_SPLIT):
+    // the chunks of one row run on adjacent warps instead of in series on one warp
+    const int nch = (nv + Eng::NV - 1) / Eng::NV;
+    const int S = (int64_t)ntask * nch <= (int64_t)gridDim.x * WPB ? nch : 1;
+    if (blockIdx.x * WPB + wid >= ntask * S) return;
     unsigned char *wsm = smem_raw + (size_t)wid * (TMA ? warp_tma_bytes<Eng>() : Eng::SCRATCH);
     TmaRing rg{};
     if (TMA) rg = ring_init(wsm, lane);
     void *scratch = TMA ? (void *)(wsm + TMA_RING + 128) : (void *)wsm;
     // grid-stride over tasks (the launcher may cap the grid: persistent bandwidth kernels)
-    for (int task = blockIdx.x * WPB + wid; task < ntask; task += gridDim.x * WPB) {
+    for (int vt = blockIdx.x * WPB + wid; vt < ntask * S; vt += gridDim.x * WPB) {
+    const int task = vt / S;
+    const int ch0 = S == 1 ? 0 : vt - task * S, ch1 = S == 1 ? nch : ch0 + 1;
     const Task tk = tasks[task];
-    for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
+    for (int n0 = ch0 * Eng::NV; n0 < ch1 * Eng::NV && n0 < nv; n0 += Eng::NV) {
         const int nvc = min(Eng::NV, nv - n0);
         typename Eng::Acc acc;
         if (MODE == MODE_ACCUM) acc_load(acc, dst + tk.out + (int64_t)n0 * dst_ld, dst_ld, tk.r, nvc, lane);
@@ -1850,7 +1856,9 @@ cudaError_t launch_rows_t(int mode, const Task *t, int ntask, const Blk *b, cons
             attr_set = (err == cudaSuccess);
         }
         if (err != cudaSuccess) return;
-        const int grid = max_ctas > 0 ? min(grid_for(ntask), max_ctas) : grid_for(ntask);
+        static const bool split = !(getenv("H2_ROWS_SPLIT") && getenv("H2_ROWS_SPLIT")[0] == '0');
+        const int nch = (nv + E::NV - 1) / E::NV;
+        const int grid = max_ctas > 0 ? min(grid_for(ntask), max_ctas) : grid_for(split ? ntask * nch : ntask);
         if (mode == MODE_WRITE)
             launch_pri(kw, grid, WPB * 32, sm, s, t, ntask, b, src, src_ld, dst, dst_ld, nv);
         else
