@@ -1556,7 +1556,12 @@ k_leaf_dense_split(const Task *__restrict__ ltasks, const Task *__restrict__ dta
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     T *zs = reinterpret_cast<T *>(smem_raw) + wid * NV * ZLD;
     void *scratch = smem_raw + (size_t)WPB * NV * ZLD * sizeof(T) + wid * EngH::SCRATCH;
-    for (int task2 = blockIdx.x * WPB + wid; task2 < ntask2; task2 += gridDim.x * WPB) {
+    // (leaf half, vector chunk) tasks when the launcher sized the grid for them (see k_rows)
+    const int nch = (nv + NV - 1) / NV;
+    const int S = (int64_t)ntask2 * nch <= (int64_t)gridDim.x * WPB ? nch : 1;
+    for (int vt = blockIdx.x * WPB + wid; vt < ntask2 * S; vt += gridDim.x * WPB) {
+        const int task2 = vt / S;
+        const int ch0 = S == 1 ? 0 : vt - task2 * S, ch1 = S == 1 ? nch : ch0 + 1;
         const int task = task2 >> 1, half = task2 & 1;
         const Task tk = ltasks[task];
         const Task dk = dtasks[task];
@@ -1564,7 +1569,7 @@ k_leaf_dense_split(const Task *__restrict__ ltasks, const Task *__restrict__ dta
         const Blk bU = blks[tk.blk0 + (hasE ? 1 : 0)];
         const int r0 = 32 * half;
         const int rh = min(32, m - r0);
-        for (int n0 = 0; n0 < nv; n0 += NV) {
+        for (int n0 = ch0 * NV; n0 < ch1 * NV && n0 < nv; n0 += NV) {
             const int nvc = min(NV, nv - n0);
             typename EngK::Acc z;
             acc_load(z, yh + bU.x + (int64_t)n0 * yh_ld, yh_ld, k, nvc, lane);
@@ -1928,9 +1933,11 @@ cudaError_t launch_leaf_dense(const Task *lt, const Task *dt, int ntask, const B
                     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
                     attr_set = (err == cudaSuccess);
                 }
+                static const bool vsplit = !(getenv("H2_LEAF_VSPLIT") && getenv("H2_LEAF_VSPLIT")[0] == '0');
+                const int nch = vsplit ? (nv + EH::NV - 1) / EH::NV : 1;
                 if (err == cudaSuccess)
-                    kern<<<grid_for(2 * ntask), WPB * 32, sm, s>>>(lt, dt, 2 * ntask, b, yh, yh_ld, args, halo, nv,
-                                                                   k, kp, m);
+                    kern<<<grid_for(2 * ntask * nch), WPB * 32, sm, s>>>(lt, dt, 2 * ntask, b, yh, yh_ld, args,
+                                                                         halo, nv, k, kp, m);
             };
             Dispatch<double>::run(k, nv, [&](auto ek) {
                 using EK = decltype(ek);
