@@ -832,13 +832,18 @@ k_up_leaf(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blk
           const CallArgs<T> *__restrict__ args, T *__restrict__ xh, int64_t xh_ld, int nv)
 {
     const int lane = threadIdx.x & 31;
-    const int task = blockIdx.x * WPB + (threadIdx.x >> 5);
-    if (task >= ntask) return;
+    // one warp per (leaf, vector chunk) when the launcher sized the grid for it (see k_rows)
+    const int nch = (nv + Eng::NV - 1) / Eng::NV;
+    const int S = (int64_t)ntask * nch <= (int64_t)gridDim.x * WPB ? nch : 1;
+    const int vt = blockIdx.x * WPB + (threadIdx.x >> 5);
+    if (vt >= ntask * S) return;
+    const int task = vt / S;
+    const int ch0 = S == 1 ? 0 : vt - task * S, ch1 = S == 1 ? nch : ch0 + 1;
     const T *__restrict__ X = args->X;
     const int64_t ldx = args->ldx;
     const Task tk = tasks[task];
     const Blk b = blks[tk.blk0];
-    for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
+    for (int n0 = ch0 * Eng::NV; n0 < ch1 * Eng::NV && n0 < nv; n0 += Eng::NV) {
         const int nvc = min(Eng::NV, nv - n0);
         typename Eng::Acc acc;
         acc_zero(acc, lane);
@@ -1838,7 +1843,9 @@ cudaError_t launch_up_leaf(const Task *t, int ntask, const Blk *b, const CallArg
 {
     if (ntask == 0) return cudaSuccess;
     Dispatch<T>::run(r, nv, [&](auto e) {
-        k_up_leaf<T, decltype(e)><<<grid_for(ntask), WPB * 32, 0, s>>>(t, ntask, b, args, xh, xh_ld, nv);
+        static const bool vsplit = !(getenv("H2_LEAF_VSPLIT") && getenv("H2_LEAF_VSPLIT")[0] == '0');
+        const int nch = vsplit ? (nv + decltype(e)::NV - 1) / decltype(e)::NV : 1;
+        k_up_leaf<T, decltype(e)><<<grid_for(ntask * nch), WPB * 32, 0, s>>>(t, ntask, b, args, xh, xh_ld, nv);
     });
     return cudaGetLastError();
 }
