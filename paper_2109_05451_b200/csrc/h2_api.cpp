@@ -990,9 +990,11 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     //      always for P = 1, and for P > 1 without top-tree couplings)
     {
         // levels with <= TOPN output nodes are fused into one single-CTA launch; one SM streams
-        // only ~1/148 of the HBM bandwidth, so only the tiniest levels are worth fusing
+        // only ~1/148 of the HBM bandwidth, so only the tiniest levels are worth fusing -- and
+        // only while one vector chunk covers nv (nv_max > 16: the (node, chunk) warps of a
+        // level-per-launch sweep win, cfg3s 4.13 -> 4.06 ms; cfg2 keeps 8)
         const char *tn = getenv("H2_TOPN");
-        const int TOPN = tn ? atoi(tn) : 8;
+        const int TOPN = tn ? atoi(tn) : (h->nv_max > 16 ? 0 : 8);
         const char *stv = getenv("H2_SUBTREE");
         h->subtree_on = stv && stv[0] == '1';
         const char *sw = getenv("H2_SWEEP");
