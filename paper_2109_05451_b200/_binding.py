@@ -19,10 +19,11 @@ EXPORTS = ["h2_create", "h2_matvec", "h2_matvec_ld", "h2_matvec_host", "h2_set_s
            "h2_plan_counts", "h2_plan_census", "h2_destroy", "h2_nccl_unique_id", "h2_last_error", "h2_version"]
 PHASES = ["up_leaf", "up_transfer", "exchange_top", "coupling_diag", "coupling_offdiag",
           "down_transfer", "leaf_u", "dense", "coupling_leaf"]
-KERNEL_OF_PHASE = {"up_leaf": "k_up_leaf (or k_mega_up: leaf projection + upsweep + coupling)", "up_transfer": "k_tree<WRITE>", "exchange_top": "k_pack",
+KERNEL_OF_PHASE = {"up_leaf": "k_up_leaf", "up_transfer": "k_sweep<WRITE>", "exchange_top": "k_pack + k_tree",
                    "coupling_diag": "k_rows<WRITE>", "coupling_offdiag": "k_rows<ACCUM>",
-                   "down_transfer": "k_tree<ACCUM>", "leaf_u": "k_leaf_dense / k_mega_down (downsweep + leaf expansion + dense near field + epilogue)", "dense": "k_dense",
-                   "coupling_leaf": "k_rows<WRITE>"}
+                   "down_transfer": "k_sweep<ACCUM>",
+                   "leaf_u": "k_leaf_dense (last transfer + leaf expansion + dense near field + epilogue)",
+                   "dense": "k_leaf_dense", "coupling_leaf": "k_rows<WRITE>"}
 
 
 class H2Error(RuntimeError):
@@ -194,27 +195,75 @@ class H2Operator:
                              C.byref(h)))
         self.handle = h
         self._keep = ds.keep if ds.device else []   # host arrays were copied by h2_create
+        self.device_index = None
+        try:
+            import torch
+            if torch.cuda.is_available():
+                self.device_index = torch.cuda.current_device()
+        except Exception:
+            pass
 
     # -- calls
     def set_stream(self, stream_ptr):
         _check(self._lib.h2_set_stream(self.handle, C.c_void_p(int(stream_ptr))))
 
+    def _check_vectors(self, X, Y, want_cuda):
+        """Shape / dtype / device / layout checks before raw pointers cross the C ABI."""
+        want = "torch.float64" if self.dtype == H2_F64 else "torch.float32"
+        nv = X.shape[0] if len(X.shape) == 2 else -1
+        if len(X.shape) != 2 or tuple(X.shape) != (nv, self.n_local) or tuple(Y.shape) != tuple(X.shape):
+            raise ValueError(f"X, Y must both have shape (nv, n_local={self.n_local})")
+        if not 1 <= nv <= self.nv_max:
+            raise ValueError(f"nv must be in [1, nv_max={self.nv_max}]")
+        for name, a in (("X", X), ("Y", Y)):
+            if _is_torch(a):
+                if str(a.dtype) != want:
+                    raise ValueError(f"{name} must be {want} (handle dtype)")
+                if not a.is_contiguous():
+                    raise ValueError(f"{name} must be contiguous")
+                if a.is_cuda != want_cuda:
+                    raise ValueError(f"{name} must be a {'CUDA' if want_cuda else 'host'} tensor")
+                if want_cuda and self.device_index is not None and a.device.index != self.device_index:
+                    raise ValueError(f"{name} is on cuda:{a.device.index}, the handle on cuda:{self.device_index}")
+            else:
+                if want_cuda:
+                    raise ValueError(f"{name} must be a CUDA tensor")
+                if a.dtype != self.np_dtype or not a.flags["C_CONTIGUOUS"]:
+                    raise ValueError(f"{name} must be a C-contiguous {np.dtype(self.np_dtype).name} array")
+                if name == "Y" and not a.flags["WRITEABLE"]:
+                    raise ValueError("Y must be writeable")
+        return nv
+
     def matvec(self, X, Y, alpha=1.0, beta=0.0, stream=None):
         """Y := alpha A X + beta Y.  X, Y: CUDA tensors of shape (nv, n_local) (contiguous ==
         n_local x nv column-major).  Asynchronous on `stream` (default: torch's current stream)."""
         import torch
-        nv = X.shape[0]
-        if X.shape != (nv, self.n_local) or Y.shape != X.shape or not (X.is_contiguous() and Y.is_contiguous()):
-            raise ValueError("X, Y must be contiguous (nv, n_local)")
+        nv = self._check_vectors(X, Y, True)
         st = stream if stream is not None else torch.cuda.current_stream(X.device)
         self.set_stream(st.cuda_stream)
         _check(self._lib.h2_matvec(self.handle, float(alpha), X.data_ptr(), float(beta), Y.data_ptr(), nv))
         return Y
 
+    def matvec_ld(self, X, ldx, Y, ldy, nv, alpha=1.0, beta=0.0, stream=None):
+        """h2_matvec_ld: X, Y are 1-D CUDA tensors holding nv columns of n_local rows with leading
+        dimensions ldx, ldy (>= n_local): column n of X starts at element n * ldx."""
+        import torch
+        want = torch.float64 if self.dtype == H2_F64 else torch.float32
+        for name, a, ld in (("X", X, ldx), ("Y", Y, ldy)):
+            if not (_is_torch(a) and a.is_cuda and a.dtype == want and a.is_contiguous()):
+                raise ValueError(f"{name} must be a contiguous CUDA {want} tensor")
+            if ld < self.n_local or a.numel() < (nv - 1) * ld + self.n_local:
+                raise ValueError(f"{name} too small for nv={nv}, ld={ld}")
+        st = stream if stream is not None else torch.cuda.current_stream(X.device)
+        self.set_stream(st.cuda_stream)
+        _check(self._lib.h2_matvec_ld(self.handle, float(alpha), X.data_ptr(), int(ldx), float(beta),
+                                      Y.data_ptr(), int(ldy), int(nv)))
+        return Y
+
     def matvec_host(self, X, Y, alpha=1.0, beta=0.0, stream=None):
         """End-to-end: X, Y host arrays (nv, n_local) (numpy or pinned CPU torch tensors)."""
         ptr = lambda a: a.data_ptr() if _is_torch(a) else a.ctypes.data
-        nv = X.shape[0]
+        nv = self._check_vectors(X, Y, False)
         if stream is not None:
             self.set_stream(stream.cuda_stream)
         _check(self._lib.h2_matvec_host(self.handle, float(alpha), ptr(X), float(beta), ptr(Y), nv))

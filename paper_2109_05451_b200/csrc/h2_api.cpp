@@ -148,6 +148,9 @@ int validate(const h2_desc *d, int nv_max, Layout &L)
         const int64_t rows = L.held(l);
         if (!rp) return fail(H2_ERR_ARG, "S_rowptr[l] is NULL");
         if (rp[0] != 0) return fail(H2_ERR_STRUCT, "S_rowptr[l][0] must be 0");
+        for (int64_t i = 0; i < rows; ++i)
+            if (rp[i + 1] < rp[i]) return fail(H2_ERR_STRUCT, "S_rowptr not monotone");
+        if (rp[rows] > 0 && !col) return fail(H2_ERR_ARG, "S_col[l] is NULL but level has blocks");
         for (int64_t i = 0; i < rows; ++i) {
             if (rp[i + 1] < rp[i]) return fail(H2_ERR_STRUCT, "S_rowptr not monotone");
             for (int64_t b = rp[i]; b < rp[i + 1]; ++b) {
@@ -166,6 +169,9 @@ int validate(const h2_desc *d, int nv_max, Layout &L)
     {
         const int64_t *rp = d->D_rowptr;
         if (rp[0] != 0) return fail(H2_ERR_STRUCT, "D_rowptr[0] must be 0");
+        for (int64_t i = 0; i < nleaf; ++i)
+            if (rp[i + 1] < rp[i]) return fail(H2_ERR_STRUCT, "D_rowptr not monotone");
+        if (rp[nleaf] > 0 && !d->D_col) return fail(H2_ERR_ARG, "D_col is NULL but there are dense blocks");
         for (int64_t i = 0; i < nleaf; ++i) {
             if (rp[i + 1] < rp[i]) return fail(H2_ERR_STRUCT, "D_rowptr not monotone");
             for (int64_t b = rp[i]; b < rp[i + 1]; ++b) {
@@ -238,13 +244,10 @@ struct h2_ctx {
     bool has_top = false;            // P > 1 and the top tree (levels < C) holds couplings
     cudaStream_t stream = nullptr;   // caller's stream (default legacy)
     cudaStream_t s_comm = nullptr;
-    cudaStream_t s_dense = nullptr;  // low-priority stream of the dense near field
     cudaStream_t s_leafc = nullptr;  // leaf-level coupling, concurrent with the upsweep transfers
     cudaEvent_t ev_packed = nullptr, ev_recv = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_dense = nullptr, ev_halo = nullptr;
-    cudaEvent_t ev_upleaf = nullptr, ev_leafc = nullptr, ev_cu = nullptr;
-    int sched = 0;                   // H2_SCHED: 0 fused leaf+dense kernel (default), 1 dense on its own
-                                     // stream from t = 0, 2 dense paired with the downsweep
+    cudaEvent_t ev_fork = nullptr, ev_halo = nullptr;
+    cudaEvent_t ev_upleaf = nullptr, ev_leafc = nullptr;
     std::vector<void *> owned;       // device allocations to free
     // operator (device)
     const void *U = nullptr, *Vt = nullptr, *D = nullptr;
@@ -264,29 +267,11 @@ struct h2_ctx {
     std::vector<Phase> up_lv, top_up_lv, coup_diag, coup_leaf, down_lv;
     struct Stage { TreeStage st; int nctas; int r; };
     std::vector<Stage> up_stages, top_stages, down_stages;
-    // dependency-driven single-launch sweeps (k_chain): task ranges, their deps, the flags
-    // persistent scheduled kernels (k_mega_up / k_mega_down), see h2_internal.h
-    bool use_mega = false;
-    MegaParams mp{};
-    SchedEntry *d_sched = nullptr;
-    int nsched_up = 0, nsched_dn = 0;
-    int mega_r = 1, mega_grid = 0;
-    int32_t *d_counters = nullptr;
     // heap-addressed sweeps (k_sweep): bottom levels one launch each, small top levels fused
     bool use_sweep = false;
-    bool subtree_on = false;         // H2_SUBTREE=1: leaf projection fused with the first levels
-                                     // (measured neutral / slower on cfg2 in round 1)
     std::vector<SweepParams> up_sweeps, dn_sweeps;
     std::vector<int> up_sweep_ctas, dn_sweep_ctas;
     int sweep_r_up = 1, sweep_r_dn = 1;
-    PrefetchList top_pf{};           // top-level F^T / E blocks prefetched into L2 every call
-    bool use_chain = true;
-    int chain_ctas = 0;
-    int64_t up_c0 = 0, dn_c0 = 0;
-    int up_cn = 0, dn_cn = 0, up_cr = 1, dn_cr = 1;
-    ChainDep *d_deps = nullptr;      // [up_cn + dn_cn]
-    int32_t *d_flags = nullptr;
-    int64_t nflags = 0;
     std::vector<int> up_lv_level, top_up_level, down_level;
     int64_t nseg_x = 0, nseg_h = 0, seg_x0 = 0, seg_h0 = 0;
     struct Peer {
@@ -301,13 +286,6 @@ struct h2_ctx {
     void *dX = nullptr, *dY = nullptr;
     // per-call arguments (device CallArgs<T>) and the captured graphs, one per nv
     void *dargs = nullptr;
-    bool use_graph = true;
-    int tma_mode = 0;                // H2_TMA: 0 never, 1 always, 2 for nv <= 4 only
-    int bw_ctas = 0;                 // grid cap of the side-stream bandwidth kernels (H2_BW_CTAS)
-    bool one_side = false;           // leaf-level coupling queued behind the dense kernel (H2_ONE_SIDE)
-    bool leafc_serial = false;       // leaf-level coupling on the main stream (H2_LEAFC_SERIAL=1)
-    int prio_lo = 0, prio_hi = 0;    // per-launch priorities (H2_PRIO=1): side bandwidth / sweep chain
-    bool tma_on(int nv) const { return tma_mode == 1 || (tma_mode == 2 && nv <= 4); }
     cudaStream_t cap_stream = nullptr;
     cudaStream_t last_stream = nullptr;
     bool last_stream_set = false;
@@ -373,9 +351,8 @@ int release(h2_ctx *h)
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     if (h->s_comm) cudaStreamDestroy(h->s_comm);
-    if (h->s_dense) cudaStreamDestroy(h->s_dense);
     if (h->s_leafc) cudaStreamDestroy(h->s_leafc);
-    for (cudaEvent_t e : {h->ev_packed, h->ev_recv, h->ev_fork, h->ev_dense, h->ev_halo, h->ev_upleaf, h->ev_leafc, h->ev_cu})
+    for (cudaEvent_t e : {h->ev_packed, h->ev_recv, h->ev_fork, h->ev_halo, h->ev_upleaf, h->ev_leafc})
         if (e) cudaEventDestroy(e);
     delete h;
     return H2_OK;
@@ -494,34 +471,14 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         H2_TRYC(cudaMemset(h->dargs, 0, sizeof(CallArgs<double>)));
         int least = 0, greatest = 0;
         H2_TRYC(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-        // the tree chain (captured on cap_stream) gets the highest priority, the bandwidth
-        // kernels on the side streams the lowest (PAPER.md:509 low-priority stream)
+        // the tree sweeps (captured on cap_stream) get the highest priority, the leaf-level
+        // coupling on its side stream the lowest (PAPER.md:509 low-priority stream)
         H2_TRYC(cudaStreamCreateWithPriority(&h->cap_stream, cudaStreamNonBlocking, greatest));
-        H2_TRYC(cudaStreamCreateWithPriority(&h->s_dense, cudaStreamNonBlocking, least));
         H2_TRYC(cudaStreamCreateWithPriority(&h->s_leafc, cudaStreamNonBlocking, least));
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_upleaf, cudaEventDisableTiming));
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_leafc, cudaEventDisableTiming));
-        H2_TRYC(cudaEventCreateWithFlags(&h->ev_cu, cudaEventDisableTiming));
-        const char *sc = getenv("H2_SCHED");
-        h->sched = sc ? atoi(sc) : 0;
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
-        H2_TRYC(cudaEventCreateWithFlags(&h->ev_dense, cudaEventDisableTiming));
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
-        const char *g = getenv("H2_GRAPH");
-        h->use_graph = !(g && g[0] == '0');
-        const char *tm = getenv("H2_TMA");
-        h->tma_mode = tm ? atoi(tm) : 0;
-        int dev = 0, nsm = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        const char *bc = getenv("H2_BW_CTAS");      // per SM; default 0 = uncapped grid
-        h->bw_ctas = (bc ? atoi(bc) : 0) * nsm;
-        const char *pr = getenv("H2_PRIO");
-        if (pr && pr[0] == '1') { h->prio_lo = least; h->prio_hi = greatest; }
-        const char *ls = getenv("H2_LEAFC_SERIAL");
-        h->leafc_serial = ls && ls[0] == '1';
-        const char *os = getenv("H2_ONE_SIDE");
-        h->one_side = os && os[0] == '1';
     }
     // ---- operator arrays on the device; V and F re-laid out as V^T, F^T (operand order)
     const int kq = k[q];
@@ -821,7 +778,6 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     //     (PAPER.md:328-331, 496); every held row gets a task (empty rows write 0)
     std::vector<Task> offd_tasks[3];
     std::vector<Blk> offd_blks[3];
-    std::vector<std::pair<int64_t, int>> coup_task_level;   // (task index, level) of diagonal coupling rows
     {
         // classes: engine class ci (0..2) for the levels above the leaves, 3 + ci for the leaf
         // level (its coupling only needs x^ of the leaves: it runs on its own stream right after
@@ -878,7 +834,6 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
                 Task t = cls[cj][o];
                 t.blk0 = (int64_t)blks.size();
                 blks.insert(blks.end(), cls_blk[cj][o].begin(), cls_blk[cj][o].end());
-                coup_task_level.push_back({(int64_t)tasks.size(), cls_lvl[cj][o]});
                 tasks.push_back(t);
             }
             if (ph.n) (cj < 3 ? h->coup_diag : h->coup_leaf).push_back(ph);
@@ -993,12 +948,8 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         // only ~1/148 of the HBM bandwidth, so only the tiniest levels are worth fusing -- and
         // only while one vector chunk covers nv (nv_max > 16: the (node, chunk) warps of a
         // level-per-launch sweep win, cfg3s 4.13 -> 4.06 ms; cfg2 keeps 8)
-        const char *tn = getenv("H2_TOPN");
-        const int TOPN = tn ? atoi(tn) : (h->nv_max > 16 ? 0 : 8);
-        const char *stv = getenv("H2_SUBTREE");
-        h->subtree_on = stv && stv[0] == '1';
-        const char *sw = getenv("H2_SWEEP");
-        h->use_sweep = !h->has_top && !(sw && sw[0] == '0');
+        const int TOPN = h->nv_max > 16 ? 0 : 8;
+        h->use_sweep = !h->has_top;
         auto lvl_up = [&](int lc) {              // parents at lc - 1, children at lc
             SweepLevel v{h->Ft[lc], h->xh_base[lc], h->xh_base[lc - 1], (int32_t)L.held(lc - 1),
                          (int16_t)k[lc - 1], (int16_t)k[lc]};
@@ -1009,16 +960,6 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
                          (int16_t)k[l - 1]};
             return v;
         };
-        // L2 prefetch list: F^T and E of the levels with <= 1024 held nodes (opt-in H2_PREFETCH=1:
-        // shortens the top sweep levels but measured net-neutral on cfg2)
-        const char *pf = getenv("H2_PREFETCH");
-        if (pf && pf[0] == '1')
-            for (int l = 1; l <= q && h->top_pf.n + 2 <= PREFETCH_MAX; ++l) {
-                if (L.held(l) > 1024) break;
-                const int64_t bytes = L.held(l) * k[l] * k[l - 1] * (int64_t)h->esz;
-                h->top_pf.ptr[h->top_pf.n] = h->Ft[l]; h->top_pf.bytes[h->top_pf.n++] = bytes;
-                h->top_pf.ptr[h->top_pf.n] = h->E[l]; h->top_pf.bytes[h->top_pf.n++] = bytes;
-            }
         if (h->use_sweep) {
             SweepParams top{};
             for (int lc : h->up_lv_level) {
@@ -1054,121 +995,6 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             h->dn_sweeps.insert(h->dn_sweeps.end(), dbot.begin(), dbot.end());
             h->dn_sweep_ctas.insert(h->dn_sweep_ctas.end(), dbot_ctas.begin(), dbot_ctas.end());
         }
-    }
-    // ---- persistent scheduled sweeps (valid under the same conditions as the sweeps)
-    {
-        // opt-in (H2_MEGA=1): measured slower than the staged launches on cfg2 in round 1
-        const char *me = getenv("H2_MEGA");
-        h->use_mega = h->use_sweep && (me && me[0] == '1') && q >= 1 && q + 1 <= SWEEP_MAXLEV;
-        if (h->use_mega) {
-            MegaParams &mp = h->mp;
-            mp.q = q;
-            mp.k = k[q];
-            mp.kp = k[q - 1];
-            int64_t fb = 0;
-            for (int l = 0; l <= q; ++l) { mp.fbase[l] = fb; fb += L.held(l); mp.nodes[l] = (int32_t)L.held(l); }
-            mp.fbase[q + 1] = fb;
-            for (int lc = C + 1; lc <= q; ++lc)
-                mp.up[lc] = SweepLevel{h->Ft[lc], h->xh_base[lc], h->xh_base[lc - 1], (int32_t)L.held(lc - 1),
-                                       (int16_t)k[lc - 1], (int16_t)k[lc]};
-            mp.dn_first = h->down_level.empty() ? q : h->down_level.front();
-            for (int l : h->down_level)
-                mp.dn[l] = SweepLevel{h->E[l], h->yh_base[l - 1], h->yh_base[l], (int32_t)L.held(l), (int16_t)k[l],
-                                      (int16_t)k[l - 1]};
-            // coupling tasks per level, longest rows first (already sorted within a class)
-            std::vector<std::vector<int64_t>> coup_by_level(q + 1);
-            for (auto &tl : coup_task_level) coup_by_level[tl.second].push_back(tl.first);
-            for (auto &v : coup_by_level)
-                std::stable_sort(v.begin(), v.end(), [&](int64_t x, int64_t y) { return tasks[x].nblk > tasks[y].nblk; });
-            std::vector<SchedEntry> sch;
-            for (int64_t s = 0; s < nleaf; ++s) sch.push_back({ST_UPLEAF, (int16_t)q, (int32_t)(h->up_leaf.t0 + s)});
-            // interleave: up(lc) producing level lc-1, then the coupling of level lc (complete)
-            for (int lc = q; lc >= C + 1; --lc) {
-                for (int64_t i = 0; i < L.held(lc - 1); ++i) sch.push_back({ST_UP, (int16_t)lc, (int32_t)i});
-                for (int64_t ti : coup_by_level[lc]) sch.push_back({ST_COUP, (int16_t)lc, (int32_t)ti});
-            }
-            for (int l = C; l >= 0; --l)
-                for (int64_t ti : coup_by_level[l]) sch.push_back({ST_COUP, (int16_t)l, (int32_t)ti});
-            h->nsched_up = (int)sch.size();
-            for (int l : h->down_level)
-                for (int64_t c = 0; c < L.held(l); ++c) sch.push_back({ST_DOWN, (int16_t)l, (int32_t)c});
-            for (int64_t t = 0; t < nleaf; ++t) sch.push_back({ST_LEAF, (int16_t)q, (int32_t)t});
-            h->nsched_dn = (int)sch.size() - h->nsched_up;
-            for (int l = 0; l <= q; ++l) h->mega_r = std::max(h->mega_r, k[l]);
-            mp.kmax = h->mega_r;
-            cudaError_t err;
-            h->d_sched = (SchedEntry *)dalloc(h, sch.size() * sizeof(SchedEntry), err);
-            h->d_counters = (int32_t *)dalloc(h, (size_t)(q + 1) * sizeof(int32_t), err);
-            if (!h->d_sched || !h->d_counters) H2_TRY(cuda_fail(h, err, "cudaMalloc(schedule)"));
-            H2_TRYC(cudaMemcpy(h->d_sched, sch.data(), sch.size() * sizeof(SchedEntry), cudaMemcpyHostToDevice));
-            H2_TRYC(cudaMemset(h->d_counters, 0, (size_t)(q + 1) * sizeof(int32_t)));
-            int dev = 0, nsm = 148;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            const char *mg = getenv("H2_MEGA_CTAS");
-            h->mega_grid = (mg ? atoi(mg) : 2) * nsm;
-        }
-    }
-    // ---- chain sweeps: flat flag index per held node; deps on children (up) / parent (down)
-    std::vector<ChainDep> cdeps;
-    {
-        std::vector<int64_t> fbase(q + 2, 0);
-        for (int l = 0; l <= q; ++l) fbase[l + 1] = fbase[l] + L.held(l);
-        if (!h->up_lv.empty()) {
-            h->up_c0 = h->up_lv.front().t0;
-            for (size_t u = 0; u < h->up_lv.size(); ++u) {
-                const Phase &ph = h->up_lv[u];
-                const int lc = h->up_lv_level[u];          // children level; parents at lc - 1
-                if (ph.t0 != h->up_c0 + h->up_cn) { h->use_chain = false; break; }
-                for (int64_t i = 0; i < ph.n; ++i) {
-                    ChainDep dp{(int32_t)(fbase[lc - 1] + i), -1, -1, 0};
-                    if (lc <= q - 1) {                     // children computed by the chain too
-                        dp.dep0 = (int32_t)(fbase[lc] + 2 * i);
-                        dp.dep1 = (int32_t)(fbase[lc] + 2 * i + 1);
-                    }
-                    cdeps.push_back(dp);
-                }
-                h->up_cn += ph.n;
-                h->up_cr = std::max(h->up_cr, ph.r);
-            }
-        }
-        if (!h->down_lv.empty()) {
-            h->dn_c0 = h->down_lv.front().t0;
-            for (size_t u = 0; u < h->down_lv.size() && h->use_chain; ++u) {
-                const Phase &ph = h->down_lv[u];
-                const int l = h->down_level[u];
-                if (ph.t0 != h->dn_c0 + h->dn_cn) { h->use_chain = false; break; }
-                const bool parent_in_chain = u > 0 && h->down_level[u - 1] == l - 1;
-                for (int64_t c = 0; c < ph.n; ++c) {
-                    ChainDep dp{(int32_t)(fbase[l] + c), -1, -1, 0};
-                    if (parent_in_chain) {
-                        const int64_t gp = (L.g0(l) + c) >> 1;
-                        dp.dep0 = (int32_t)(fbase[l - 1] + gp - L.g0(l - 1));
-                    }
-                    cdeps.push_back(dp);
-                }
-                h->dn_cn += ph.n;
-                h->dn_cr = std::max(h->dn_cr, ph.r);
-            }
-        }
-        // default: staged launches (measured faster on B200 for cfg2); H2_CHAIN=1 enables
-        const char *ce = getenv("H2_CHAIN");
-        if (!(ce && ce[0] == '1')) h->use_chain = false;
-        int dev = 0, nsm = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        const char *cc = getenv("H2_CHAIN_CTAS");
-        h->chain_ctas = (cc ? atoi(cc) : 2) * nsm;
-        cudaError_t err;
-        // two flag sets: x^ nodes (upsweep chain) and y^ nodes (downsweep chain)
-        h->nflags = fbase[q + 1];
-        h->d_flags = (int32_t *)dalloc(h, (size_t)2 * fbase[q + 1] * sizeof(int32_t), err);
-        if (!h->d_flags) H2_TRY(cuda_fail(h, err, "cudaMalloc(flags)"));
-        H2_TRYC(cudaMemset(h->d_flags, 0, (size_t)2 * fbase[q + 1] * sizeof(int32_t)));
-        h->d_deps = (ChainDep *)dalloc(h, (cdeps.size() + 1) * sizeof(ChainDep), err);
-        if (!h->d_deps) H2_TRY(cuda_fail(h, err, "cudaMalloc(deps)"));
-        if (!cdeps.empty())
-            H2_TRYC(cudaMemcpy(h->d_deps, cdeps.data(), cdeps.size() * sizeof(ChainDep), cudaMemcpyHostToDevice));
     }
     // ---- contiguity of every task's block run (TF_ACONTIG): A_b == A_0 + b r c
     for (Task &t : tasks) {
@@ -1208,21 +1034,13 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     for (auto &kv : need_h) hr += (int64_t)kv.second.size();
     int64_t c8[8] = {n_diag, n_off, n_root, nd_diag, nd_off, peers_n, xr, hr};
     memcpy(h->counts, c8, sizeof(c8));
-    int launches = 2 + (h->top_pf.n > 0) + (int)(h->use_sweep ? h->up_sweeps.size() : h->up_stages.size()) +
+    int launches = 2 + (int)(h->use_sweep ? h->up_sweeps.size() : h->up_stages.size()) +
                    (int)h->coup_diag.size() + (int)h->coup_leaf.size() +
                    (int)(h->use_sweep ? h->dn_sweeps.size() : h->down_stages.size()) + 2;
     if (P > 1) {
         launches += 2;   // pack x^, pack halo
         for (int ci = 0; ci < 3; ++ci) launches += h->coup_off[ci].n ? 1 : 0;
         if (h->has_top) launches += (int)h->top_stages.size();
-    }
-    if (h->use_mega) {
-        launches = 2 + (L.P > 1 ? 1 + (h->coup_off[0].n > 0) + (h->coup_off[1].n > 0) + (h->coup_off[2].n > 0) + 1 : 0);
-        int32_t nc = q + 1;
-        size_t off_c = h->dtype == H2_F64 ? offsetof(CallArgs<double>, counters) : offsetof(CallArgs<float>, counters);
-        size_t off_n = h->dtype == H2_F64 ? offsetof(CallArgs<double>, ncounters) : offsetof(CallArgs<float>, ncounters);
-        H2_TRYC(cudaMemcpy((char *)h->dargs + off_c, &h->d_counters, sizeof(int32_t *), cudaMemcpyHostToDevice));
-        H2_TRYC(cudaMemcpy((char *)h->dargs + off_n, &nc, sizeof(int32_t), cudaMemcpyHostToDevice));
     }
     h->launches_per_call = launches;
     *out = h;
@@ -1245,7 +1063,7 @@ extern "C" int h2_create(const h2_desc *d, int nv_max, const void *nccl_unique_i
 namespace {
 
 // phase marker: records event `i` (0..NEV-1) of the current call when profiling is on
-constexpr int NEV = 13;
+constexpr int NEV = 10;
 int mark(h2_ctx *h, int i, cudaStream_t st)
 {
     if (!h->prof) return H2_OK;
@@ -1258,6 +1076,9 @@ int mark(h2_ctx *h, int i, cudaStream_t st)
     H2_CUDA(h, cudaEventRecord(h->ev_pool[idx], st));
     return H2_OK;
 }
+// phase -> (start marker, end marker) of a call (see enqueue); index H2_NPHASE = whole call
+const int kPhaseSpan[H2_NPHASE + 1][2] = {{0, 1}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7},
+                                          {8, 9}, {9, 9}, {1, 2}, {0, 9}};
 
 // Enqueue one matvec for nv vectors on `st`; X, Y, alpha, beta come from the device CallArgs
 // (written by k_set_args before), so the same sequence can be captured once as a CUDA graph.
@@ -1272,16 +1093,14 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     int rc;
 #define H2_MARK(i) if ((rc = mark(h, i, st)) != H2_OK) return rc
     ncclDataType_t ty = nccl_type(h->dtype);
-    // profiling serializes the side streams onto the main one so every phase's events bracket
+    // profiling serializes the side stream onto the main one so every phase's events bracket
     // only its own kernels (clean per-kernel durations for the roofline)
-    cudaStream_t s_dense = h->prof ? st : h->s_dense;
-    cudaStream_t s_leafc = (h->prof || h->leafc_serial) ? st : (h->one_side ? h->s_dense : h->s_leafc);
-    // 0. fork: the dense near field runs on its own low-priority stream from the start, in
-    //    parallel with the tree phases; for P > 1 the x-leaf halo it needs is
-    //    exchanged first on the comm stream (X is an input, so it can start at t = 0)
-    H2_CUDA(h, cudaEventRecord(h->ev_fork, st));
-    if (h->sched != 0) H2_CUDA(h, cudaStreamWaitEvent(s_dense, h->ev_fork, 0));
+    cudaStream_t s_leafc = h->prof ? st : h->s_leafc;
+    H2_MARK(0);
+    // 0. x-leaf halo for the off-process dense blocks (P > 1): X is an input, so the exchange
+    //    starts at t = 0 on the comm stream
     if (L.P > 1) {
+        H2_CUDA(h, cudaEventRecord(h->ev_fork, st));
         H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_fork, 0));
         H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_h0, h->nseg_h, (const T *)nullptr, 0, args, (T *)h->hsend, nv, h->s_comm));
         H2_NCCL(h, g_nccl.GroupStart());
@@ -1291,112 +1110,32 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
         }
         H2_NCCL(h, g_nccl.GroupEnd());
         H2_CUDA(h, cudaEventRecord(h->ev_halo, h->s_comm));
-        if (h->sched != 0) H2_CUDA(h, cudaStreamWaitEvent(s_dense, h->ev_halo, 0));
     }
-    auto dense_now = [&]() -> int {
-        int rc2;
-        if ((rc2 = mark(h, 9, s_dense)) != H2_OK) return rc2;
-        H2_CUDA(h, launch_dense<T>(T0(h->dense), h->dense.n, h->d_blks, args, (const T *)h->hrecv, nv, h->dense.r,
-                                   h->tma_on(nv), h->bw_ctas, s_dense));
-        if ((rc2 = mark(h, 10, s_dense)) != H2_OK) return rc2;
-        H2_CUDA(h, cudaEventRecord(h->ev_dense, s_dense));
-        return H2_OK;
-    };
-    // schedule 0: dense from t = 0; schedule 1 (H2_SCHED=1): dense paired with the latency-bound
-    // downsweep (starts when the upper-level coupling is done), the leaf-level coupling paired
-    // with the upsweep transfers
-    if (h->sched == 1 && (rc = dense_now()) != H2_OK) return rc;
-    H2_CUDA(h, launch_prefetch_l2(h->top_pf, st));
-    H2_MARK(0);
-    if (h->use_mega && h->sched == 0) {
-        // persistent scheduled kernels: (leaf projection + upsweep + diagonal coupling) and
-        // (downsweep + leaf expansion + dense + epilogue), one launch each
-        H2_CUDA(h, launch_mega_up<T>(h->d_sched, h->nsched_up, h->mp, h->d_tasks, h->d_blks, h->d_tasks, xh,
-                                     h->xh_plane, yh, h->yh_plane, h->d_flags, h->d_counters,
-                                     (CallArgs<T> *)h->dargs, nv, h->mega_r, h->mega_grid, st));
-        for (int mk : {11, 12, 1, 2})
-            if ((rc = mark(h, mk, st)) != H2_OK) return rc;
-        if (L.P > 1) {
-            H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_x0, h->nseg_x, xh, h->xh_plane, args, (T *)h->xsend, nv, st));
-            H2_CUDA(h, cudaEventRecord(h->ev_packed, st));
-            H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_packed, 0));
-            H2_NCCL(h, g_nccl.GroupStart());
-            for (const auto &pr : h->peers) {
-                if (pr.xs_cnt) H2_NCCL(h, g_nccl.Send((T *)h->xsend + pr.xs_off, pr.xs_cnt * nv, ty, pr.rank, h->comm, h->s_comm));
-                if (pr.xr_cnt) H2_NCCL(h, g_nccl.Recv((T *)h->xrecv + pr.xr_off, pr.xr_cnt * nv, ty, pr.rank, h->comm, h->s_comm));
-            }
-            H2_NCCL(h, g_nccl.GroupEnd());
-            H2_CUDA(h, cudaEventRecord(h->ev_recv, h->s_comm));
-        }
-        for (int mk : {3, 4})
-            if ((rc = mark(h, mk, st)) != H2_OK) return rc;
-        if (L.P > 1) {
-            H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_recv, 0));
-            for (int ci = 0; ci < 3; ++ci) {
-                const Phase &ph = h->coup_off[ci];
-                H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(ph), ph.n, h->d_blks, (const T *)h->xrecv, 0, yh,
-                                          h->yh_plane, nv, ph.r, false, 0, st));
-            }
-            H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_halo, 0));
-        }
-        for (int mk : {5, 6, 7, 9, 10})
-            if ((rc = mark(h, mk, st)) != H2_OK) return rc;
-        H2_CUDA(h, launch_mega_down<T>(h->d_sched + h->nsched_up, h->nsched_dn, h->mp, T0(h->leaf), T0(h->dense),
-                                       h->d_blks, yh, h->yh_plane, (const T *)h->hrecv, h->d_flags + h->nflags,
-                                       (CallArgs<T> *)h->dargs, nv, L.m, h->mega_grid, st));
-        H2_MARK(8);
-        if (h->prof) h->ev_used += NEV;
-        return H2_OK;
-    }
-    // 1. upsweep of the local branch (PAPER.md:281 / alg:upsweep2): the leaf projection fused
-    //    with the first J transfer levels (warp-level subtrees), when those are standard levels
-    int J = 0;
-    if (h->use_sweep && h->subtree_on) {
-        const int want = nv <= 4 ? 2 : 1;
-        bool ok = (int)h->up_sweeps.size() >= want && (h->nleaf % (1 << want)) == 0;
-        for (int u = 0; ok && u < want; ++u) ok = h->up_sweeps[u].nlev == 1 && h->up_sweep_ctas[u] > 1;
-        if (ok) J = want;
-    }
-    if (J > 0) {
-        SweepParams sp{};
-        sp.nlev = J;
-        int rmax = h->up_leaf.r;
-        for (int u = 0; u < J; ++u) { sp.lv[u] = h->up_sweeps[u].lv[0]; rmax = std::max(rmax, (int)sp.lv[u].r); }
-        H2_CUDA(h, launch_up_subtree<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv, rmax, J,
-                                        sp, st));
-    } else {
-        H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
-                                     h->up_leaf.r, st));
-    }
+    // 1. leaf projection (alg:upsweep2 line 3)
+    H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
+                                 h->up_leaf.r, st));
+    H2_MARK(1);
     // 1b. leaf-level coupling (diagonal part) as soon as x^ of the leaves exists (alg:mult's
     //     levels are independent), on its own stream
     H2_CUDA(h, cudaEventRecord(h->ev_upleaf, st));
     H2_CUDA(h, cudaStreamWaitEvent(s_leafc, h->ev_upleaf, 0));
-    if ((rc = mark(h, 11, s_leafc)) != H2_OK) return rc;
-    g_launch_priority = h->prio_lo;
     for (const Phase &ph : h->coup_leaf)
         H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
-                                  nv, ph.r, h->tma_on(nv), h->bw_ctas, s_leafc));
-    g_launch_priority = 0;
-    if ((rc = mark(h, 12, s_leafc)) != H2_OK) return rc;
+                                  nv, ph.r, s_leafc));
     H2_CUDA(h, cudaEventRecord(h->ev_leafc, s_leafc));
-    H2_MARK(1);
-    g_launch_priority = h->prio_hi;
+    H2_MARK(2);
+    // 1c. upsweep transfers of the local branch
     if (h->use_sweep) {
-        for (size_t u = J; u < h->up_sweeps.size(); ++u)
+        for (size_t u = 0; u < h->up_sweeps.size(); ++u)
             H2_CUDA(h, launch_sweep<T>(MODE_WRITE, h->up_sweeps[u], h->up_sweep_ctas[u],
                                        h->up_sweep_ctas[u] == 1 && h->up_sweeps[u].nlev > 1 ? 512 : WPB * 32,
                                        xh, h->xh_plane, nv, h->sweep_r_up, st));
-    } else if (h->use_chain)
-        H2_CUDA(h, launch_chain<T>(MODE_WRITE, h->d_tasks + h->up_c0, h->d_deps, h->up_cn, h->d_blks, xh,
-                                   h->xh_plane, nv, h->up_cr, h->d_flags, (CallArgs<T> *)h->dargs, 0,
-                                   h->chain_ctas, st));
-    else
+    } else {
         for (const auto &sg : h->up_stages)
             H2_CUDA(h, launch_tree<T>(MODE_WRITE, sg.st, sg.nctas, h->d_tasks, h->d_blks, xh, h->xh_plane, nv,
                                       sg.r, st));
-    g_launch_priority = 0;
-    H2_MARK(2);
+    }
+    H2_MARK(3);
     // 2. exchange (P > 1): pack my x^ nodes that peers need, one NCCL group on the comm stream,
     //    overlapped with the diagonal multiply (alg:optimized_dist_mult)
     if (L.P > 1) {
@@ -1425,17 +1164,12 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
                                           nv, sg.r, st));
         }
     }
-    H2_MARK(3);
-    // 3. coupling multiply, diagonal part (all levels) (alg:mult)
+    H2_MARK(4);
+    // 3. coupling multiply, diagonal part of the levels above the leaves (alg:mult)
     for (const Phase &ph : h->coup_diag)
         H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
-                                  nv, ph.r, h->tma_on(nv), 0, st));
-    H2_MARK(4);
-    if (h->sched == 2) {
-        H2_CUDA(h, cudaEventRecord(h->ev_cu, st));
-        H2_CUDA(h, cudaStreamWaitEvent(s_dense, h->ev_cu, 0));
-        if ((rc = dense_now()) != H2_OK) return rc;
-    }
+                                  nv, ph.r, st));
+    H2_MARK(5);
     // 4. off-diagonal part after the exchange (waitAll, alg:optimized_dist_mult line 11-12);
     //    it accumulates into leaf-level rows too, so the leaf coupling stream joins first
     if (L.P > 1) {
@@ -1444,43 +1178,31 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
         for (int ci = 0; ci < 3; ++ci) {
             const Phase &ph = h->coup_off[ci];
             H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(ph), ph.n, h->d_blks, (const T *)h->xrecv, 0, yh,
-                                      h->yh_plane, nv, ph.r, h->tma_on(nv), 0, st));
+                                      h->yh_plane, nv, ph.r, st));
         }
     }
-    H2_MARK(5);
+    H2_MARK(6);
     // 5. downsweep transfers (alg:downsweep)
     if (h->use_sweep) {
         for (size_t u = 0; u < h->dn_sweeps.size(); ++u)
             H2_CUDA(h, launch_sweep<T>(MODE_ACCUM, h->dn_sweeps[u], h->dn_sweep_ctas[u],
                                        h->dn_sweep_ctas[u] == 1 && h->dn_sweeps[u].nlev > 1 ? 512 : WPB * 32,
                                        yh, h->yh_plane, nv, h->sweep_r_dn, st));
-    } else if (h->use_chain)
-        H2_CUDA(h, launch_chain<T>(MODE_ACCUM, h->d_tasks + h->dn_c0, h->d_deps + h->up_cn, h->dn_cn, h->d_blks,
-                                   yh, h->yh_plane, nv, h->dn_cr, h->d_flags + h->nflags, (CallArgs<T> *)h->dargs, 1,
-                                   h->chain_ctas, st));
-    else
+    } else {
         for (const auto &sg : h->down_stages)
             H2_CUDA(h, launch_tree<T>(MODE_ACCUM, sg.st, sg.nctas, h->d_tasks, h->d_blks, yh, h->yh_plane, nv,
                                       sg.r, st));
-    H2_MARK(6);
-    // 6. leaves: last transfer + U expansion (+ the dense near field in the fused schedule),
-    //    after the side streams joined
-    if (h->sched != 0) H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_dense, 0));
-    else if (L.P > 1) H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_halo, 0));   // fused kernel reads the halo
-    H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_leafc, 0));
-    H2_MARK(7);
-    if (h->sched == 0) {                     // fused schedule: the dense phase is inside phase 6
-        if ((rc = mark(h, 9, st)) != H2_OK) return rc;
-        if ((rc = mark(h, 10, st)) != H2_OK) return rc;
     }
-    const int kq = L.k[q], kp = q >= 1 ? L.k[q - 1] : 1;
-    if (h->sched == 0)
-        H2_CUDA(h, launch_leaf_dense<T>(T0(h->leaf), T0(h->dense), h->leaf.n, h->d_blks, yh, h->yh_plane, args,
-                                        (const T *)h->hrecv, nv, kq, kp, h->leaf.r, st));
-    else
-        H2_CUDA(h, launch_leaf_u<T>(T0(h->leaf), h->leaf.n, h->d_blks, yh, h->yh_plane, args, nv, kq, kp,
-                                    h->leaf.r, st));
+    H2_MARK(7);
+    // 6. leaves: last transfer + U expansion + dense near field + epilogue in one kernel (Y
+    //    written once, reading R11/R18), after the side streams joined
+    if (L.P > 1) H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_halo, 0));   // the kernel reads the x halo
+    H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_leafc, 0));
     H2_MARK(8);
+    const int kq = L.k[q], kp = q >= 1 ? L.k[q - 1] : 1;
+    H2_CUDA(h, launch_leaf_dense<T>(T0(h->leaf), T0(h->dense), h->leaf.n, h->d_blks, yh, h->yh_plane, args,
+                                    (const T *)h->hrecv, nv, kq, kp, h->leaf.r, st));
+    H2_MARK(9);
     if (h->prof) h->ev_used += NEV;
 #undef H2_MARK
     return H2_OK;
@@ -1500,7 +1222,7 @@ int run_matvec(h2_ctx *h, T alpha, const T *X, int64_t ldx, T beta, T *Y, int64_
     }
     H2_DBG("rank %d: matvec nv=%d warm=%d graph=%d", h->L.p, nv, (int)h->warm[nv], (int)(h->graph[nv] != nullptr));
     H2_CUDA(h, launch_set_args<T>((CallArgs<T> *)h->dargs, X, ldx, Y, ldy, alpha, beta, st));
-    if (h->prof || !h->use_graph || !h->warm[nv]) {
+    if (h->prof || !h->warm[nv]) {
         h->warm[nv] = true;            // first call per nv runs eagerly (sets kernel attributes)
         return enqueue<T>(h, nv, st);
     }
@@ -1610,19 +1332,13 @@ extern "C" int h2_phase_times(h2_handle h, double ms[H2_NPHASE + 1], int64_t *nc
     if (!h || !ms) return fail(H2_ERR_ARG, "NULL argument");
     for (int i = 0; i <= H2_NPHASE; ++i) ms[i] = 0;
     int64_t calls = h->ev_used / NEV;
-    // phase -> (start event, end event) of a call; see enqueue()
-    static const int span[H2_NPHASE + 1][2] = {{0, 11}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6},
-                                               {7, 8}, {9, 10}, {11, 12}, {9, 8}};
-    int sp[H2_NPHASE + 1][2];
-    memcpy(sp, span, sizeof(sp));
-    if (h->sched == 0) { sp[H2_NPHASE][0] = 0; }     // fused: the call starts at marker 0
     if (calls) {
         H2_CUDA(h, cudaDeviceSynchronize());
         for (int64_t c = 0; c < calls; ++c) {
             cudaEvent_t *e = &h->ev_pool[c * NEV];
             for (int i = 0; i <= H2_NPHASE; ++i) {
                 float t = 0;
-                H2_CUDA(h, cudaEventElapsedTime(&t, e[sp[i][0]], e[sp[i][1]]));
+                H2_CUDA(h, cudaEventElapsedTime(&t, e[kPhaseSpan[i][0]], e[kPhaseSpan[i][1]]));
                 ms[i] += t;
             }
         }
@@ -1639,15 +1355,10 @@ extern "C" int h2_phase_stats(h2_handle h, int nv, double bytes[H2_NPHASE + 1], 
     double tb = 0, tf = 0;
     double ops[H2_NPHASE], vec[H2_NPHASE];
     for (int i = 0; i < H2_NPHASE; ++i) { ops[i] = h->ph_ops[i]; vec[i] = h->ph_vec[i]; }
-    if (h->sched == 0) {      // fused leaf + dense kernel: one phase (6), Y written once
-        ops[6] += ops[7];
-        vec[6] += vec[7] - 2.0 * h->n_local;    // Y read+write of k_leaf_u replaced by one write
-        ops[7] = vec[7] = 0;
-    }
-    if (h->use_mega && h->sched == 0) {   // k_mega_up = phases 0+1+3+8, k_mega_down = 5+6
-        for (int i : {1, 3, 8}) { ops[0] += ops[i]; vec[0] += vec[i]; ops[i] = vec[i] = 0; }
-        ops[6] += ops[5]; vec[6] += vec[5]; ops[5] = vec[5] = 0;
-    }
+    // fused leaf + dense kernel: one phase (6), Y written once
+    ops[6] += ops[7];
+    vec[6] += vec[7] - 2.0 * h->n_local;    // Y read+write of a separate U pass replaced by one write
+    ops[7] = vec[7] = 0;
     for (int i = 0; i < H2_NPHASE; ++i) {
         double b = (double)h->esz * (ops[i] + nv * vec[i]);
         double f = 2.0 * nv * ops[i];

@@ -9,6 +9,6 @@ namespace h2 {
     template cudaError_t launch_transpose<T>(const T *, T *, int64_t, int, int, cudaStream_t);
     template cudaError_t launch_pack<T>(const PackSeg *, int64_t, const T *, int64_t, const CallArgs<T> *, T *, int, cudaStream_t);
     template cudaError_t launch_sweep<T>(int, const SweepParams &, int, int, T *, int64_t, int, int, cudaStream_t);
-    template cudaError_t launch_up_subtree<T>(const Task *, int, const Blk *, const CallArgs<T> *, T *, int64_t, int, int, int, const SweepParams &, cudaStream_t);
+    template cudaError_t launch_tree<T>(int, const TreeStage &, int, const Task *, const Blk *, T *, int64_t, int, int, cudaStream_t);
 #undef T
 }  // namespace h2

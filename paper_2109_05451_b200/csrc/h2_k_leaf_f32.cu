@@ -4,7 +4,5 @@
 namespace h2 {
 #define T float
     template cudaError_t launch_leaf_dense<T>(const Task *, const Task *, int, const Blk *, const T *, int64_t, const CallArgs<T> *, const T *, int, int, int, int, cudaStream_t);
-    template cudaError_t launch_leaf_u<T>(const Task *, int, const Blk *, const T *, int64_t, const CallArgs<T> *, int, int, int, int, cudaStream_t);
-    template cudaError_t launch_dense<T>(const Task *, int, const Blk *, const CallArgs<T> *, const T *, int, int, bool, int, cudaStream_t);
 #undef T
 }  // namespace h2

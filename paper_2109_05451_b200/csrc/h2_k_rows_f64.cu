@@ -3,6 +3,6 @@
 
 namespace h2 {
 #define T double
-    template cudaError_t launch_rows<T>(int, const Task *, int, const Blk *, const T *, int64_t, T *, int64_t, int, int, bool, int, cudaStream_t);
+    template cudaError_t launch_rows<T>(int, const Task *, int, const Blk *, const T *, int64_t, T *, int64_t, int, int, cudaStream_t);
 #undef T
 }  // namespace h2

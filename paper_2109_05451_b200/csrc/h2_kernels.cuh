@@ -32,21 +32,12 @@
 namespace h2 {
 
 constexpr unsigned FULL = 0xffffffffu;
-#ifndef H2_SSTAGE_DEFAULT
-#define H2_SSTAGE_DEFAULT 0x7fffffff   // SIMT engines: cp.async-staged transfer sweeps for every
-#endif                                 // level (cfg2 nv = 1: 1.083 -> 1.030 ms)
-#ifndef H2_SSTAGE_MMA_DEFAULT
-#define H2_SSTAGE_MMA_DEFAULT 0        // DMMA engines: never (measured slower at every threshold)
-#endif
 constexpr size_t SWEEP_STAGE_SMEM = 200 * 1024;   // dynamic smem cap of a staged k_sweep CTA
 #ifndef H2_APF
 #define H2_APF 4          // k-steps of L2 prefetch ahead of the DMMA A-fragment loads (0 = off;
                           // the same prefetch in the SIMT streams measured slower)
 #endif
 constexpr int XCAP_BYTES = 4096;   // per-warp staging of the stacked x in the Simt stream
-#ifndef H2_SPLIT_MINB
-#define H2_SPLIT_MINB 2
-#endif
 constexpr int ZLD = KMAX + 4;   // smem leading dimension of the z hand-over (2 wavefronts per
                                 // DMMA B-fragment load: no extra bank conflicts)
 
@@ -462,277 +453,9 @@ __device__ __forceinline__ void mma_stream(MmaAcc<MT, NT> &acc, const double *__
     }
 }
 
-// =========================================================================== TMA-bulk row stream
-// The contiguous A run of a task (coupling row, dense leaf row) is pulled into a warp-private
-// shared-memory ring by cp.async.bulk (SASS UBLKCP) completing on mbarriers: the loads are
-// asynchronous and independent of registers, so a few warps keep the HBM pipe full.  The ring is
-// a circular buffer of the byte stream (RING bytes, NST stages of STB bytes); element e of the
-// run sits at ring[(shift + e * esz) & (RING - 1)].  The consumer of chunk c processes every
-// column whose last byte lies in chunk c (chunk c-1 is still resident), then releases chunk c-1
-// and issues chunk c + NST - 1 into its stage.
-constexpr int TMA_STB = 4096;
-constexpr int TMA_NST = 4;
-constexpr int TMA_RING = TMA_STB * TMA_NST;
-
-struct TmaRing {
-    unsigned char *ring;     // TMA_RING bytes, 128-byte aligned
-    uint64_t *mbar;          // TMA_NST mbarriers
-    uint32_t seq;            // running chunk sequence number (warp-uniform)
-};
-
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, int count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
-{
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
-{
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async()
-{
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
-
-// one warp-private ring (called once per warp at kernel start)
-__device__ __forceinline__ TmaRing ring_init(unsigned char *base, int lane)
-{
-    TmaRing r;
-    r.ring = base;
-    r.mbar = reinterpret_cast<uint64_t *>(base + TMA_RING);
-    r.seq = 0;
-    if (lane == 0) {
-        for (int i = 0; i < TMA_NST; ++i) mbar_init(&r.mbar[i], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        fence_proxy_async();
-    }
-    __syncwarp();
-    return r;
-}
-
-// geometry of one contiguous byte run [a0, a0 + nbytes) in the ring
-struct RunGeo {
-    const unsigned char *g0;   // a0 rounded down to 16
-    uint32_t shift;            // a0 - g0
-    int64_t bulk;              // bytes copied by bulk copies: floor16(a0 + nbytes) - g0
-    uint32_t tail;             // remaining bytes (< 16) copied by lane 0
-    int nch;                   // chunks
-};
-
-__device__ __forceinline__ RunGeo run_geo(const void *a0, int64_t nbytes)
-{
-    RunGeo gq;
-    const uintptr_t a = reinterpret_cast<uintptr_t>(a0);
-    const uintptr_t g0 = a & ~uintptr_t(15), e = a + nbytes, eb = e & ~uintptr_t(15);
-    gq.g0 = reinterpret_cast<const unsigned char *>(g0);
-    gq.shift = (uint32_t)(a - g0);
-    gq.bulk = (int64_t)(eb - g0);
-    gq.tail = (uint32_t)(e - eb);
-    const int64_t span = (int64_t)(e - g0);
-    gq.nch = (int)((span + TMA_STB - 1) / TMA_STB);
-    return gq;
-}
-
-// lane 0: issue chunk ci of the run into stage (seq + ci) % NST
-__device__ __forceinline__ void ring_issue(TmaRing &rg, const RunGeo &gq, int ci, int lane)
-{
-    if (lane != 0 || ci >= gq.nch) return;
-    const uint32_t st = (rg.seq + ci) % TMA_NST;
-    const int64_t off = (int64_t)ci * TMA_STB;
-    const int64_t bytes = gq.bulk - off < TMA_STB ? gq.bulk - off : TMA_STB;
-    unsigned char *dst = rg.ring + st * TMA_STB;
-    if (gq.tail && gq.bulk >= off && gq.bulk < off + TMA_STB) {
-        // the (< 16 byte) tail after the last 16-byte boundary: plain copy, made visible by the
-        // release semantics of the mbarrier arrive below
-        const int64_t toff = gq.bulk - off;
-        for (uint32_t b = 0; b < gq.tail; b += 4)
-            *reinterpret_cast<uint32_t *>(dst + toff + b) = *reinterpret_cast<const uint32_t *>(gq.g0 + gq.bulk + b);
-    }
-    if (bytes > 0) {
-        mbar_expect_tx(&rg.mbar[st], (uint32_t)bytes);
-        bulk_g2s(dst, gq.g0 + off, (uint32_t)bytes, &rg.mbar[st]);
-    } else {
-        mbar_expect_tx(&rg.mbar[st], 0);
-    }
-}
-
-__device__ __forceinline__ void ring_wait(TmaRing &rg, int ci)
-{
-    const uint32_t q = rg.seq + ci;
-    mbar_wait(&rg.mbar[q % TMA_NST], (q / TMA_NST) & 1);
-}
-
-template <typename T>
-__device__ __forceinline__ T ring_ld(const TmaRing &rg, uint32_t byte_pos)
-{
-    return *reinterpret_cast<const T *>(rg.ring + (byte_pos & (TMA_RING - 1)));
-}
-
-// Simt consumer: acc += A_run (r x K) * xs (K x nvc, smem, ld K)
-template <typename T, int RPL, int NVB>
-__device__ __forceinline__ void simt_tma_run(SimtAcc<T, RPL, NVB> &acc, TmaRing &rg, const T *A0, int r, int K,
-                                             const T *xs, int lane)
-{
-    const RunGeo gq = run_geo(A0, (int64_t)K * r * sizeof(T));
-    for (int ci = 0; ci < TMA_NST - 1; ++ci) ring_issue(rg, gq, ci, lane);
-    const int colb = r * (int)sizeof(T);
-    // chunk ci lives in stage (seq + ci) % NST: ring byte of run byte p = base + p (mod RING)
-    const uint32_t base = (rg.seq % TMA_NST) * TMA_STB + gq.shift;
-    int J = 0;
-    for (int ci = 0; ci < gq.nch; ++ci) {
-        ring_wait(rg, ci);
-        int64_t lim = ((int64_t)(ci + 1) * TMA_STB - gq.shift) / colb;
-        const int J1 = (ci == gq.nch - 1 || lim > K) ? K : (int)lim;
-#pragma unroll 8
-        for (; J < J1; ++J) {
-            const uint32_t pos0 = base + (uint32_t)J * colb;
-            T a[RPL];
-#pragma unroll
-            for (int ri = 0; ri < RPL; ++ri) {
-                const int i = lane + 32 * ri;
-                a[ri] = (i < r) ? ring_ld<T>(rg, pos0 + i * (uint32_t)sizeof(T)) : T(0);
-            }
-#pragma unroll
-            for (int n = 0; n < NVB; ++n) {
-                const T xv = xs[J + n * K];
-#pragma unroll
-                for (int ri = 0; ri < RPL; ++ri) acc.v[ri][n] = fma(a[ri], xv, acc.v[ri][n]);
-            }
-        }
-        __syncwarp();
-        fence_proxy_async();
-        ring_issue(rg, gq, ci + TMA_NST - 1, lane);
-    }
-    rg.seq += gq.nch;
-}
-
-template <typename T, int RPL, int NVB>
-__device__ __forceinline__ void simt_tma_stream(SimtAcc<T, RPL, NVB> &acc, const T *__restrict__ A0, int r,
-                                                int c, int nblk, const Blk *__restrict__ blks,
-                                                const Src<T> &src, int nvc, int lane, TmaRing &rg, T *xs,
-                                                int xcap)
-{
-    int per = xcap / (c * NVB);
-    per = per < 1 ? 1 : (per > 32 ? 32 : per);
-    for (int b0 = 0; b0 < nblk; b0 += per) {
-        const int nb = min(per, nblk - b0);
-        const int K = nb * c;
-        int64_t xo = 0;
-        int xr = 0, xl = 0;
-        if (lane < nb) {
-            const Blk b = blks[b0 + lane];
-            xo = b.x; xr = b.xrows; xl = b.xld;
-        }
-        __syncwarp();
-        for (int e0 = 0; e0 < K; e0 += 32) {
-            const int e = e0 + lane;
-            const int bb = min(e / c, nb - 1), j = e - bb * c;
-            const int64_t bxo = __shfl_sync(FULL, xo, bb);
-            const int bxr = __shfl_sync(FULL, xr, bb), bxl = __shfl_sync(FULL, xl, bb);
-            if (e < K) {
-                int64_t ld;
-                const T *p = resolve(src, bxo, bxl, ld);
-#pragma unroll
-                for (int n = 0; n < NVB; ++n) xs[e + n * K] = (j < bxr && n < nvc) ? p[j + n * ld] : T(0);
-            }
-        }
-        __syncwarp();
-        simt_tma_run<T, RPL, NVB>(acc, rg, A0 + (int64_t)b0 * r * c, r, K, xs, lane);
-        __syncwarp();
-    }
-}
-
-// DMMA consumer over the TMA ring: A fragments from shared memory, B from the x sources
-template <int MT, int NT>
-__device__ __forceinline__ void mma_tma_stream(MmaAcc<MT, NT> &acc, const double *__restrict__ A0, int r, int c,
-                                               int nblk, const Blk *__restrict__ blks, const Src<double> &src,
-                                               int nvc, int lane, TmaRing &rg, MmaDesc *ds)
-{
-    const int g = lane >> 2, t = lane & 3;
-    for (int b0 = 0; b0 < nblk; b0 += 32) {
-        const int nb = min(32, nblk - b0);
-        const int K = nb * c;
-        __syncwarp();
-        if (lane < nb) {
-            const Blk b = blks[b0 + lane];
-            int64_t ld;
-            const double *p = resolve(src, b.x, b.xld, ld);
-            ds[lane] = MmaDesc{p, ld, b.xrows, 0};
-        }
-        __syncwarp();
-        const double *A = A0 + (int64_t)b0 * r * c;
-        const RunGeo gq = run_geo(A, (int64_t)K * r * 8);
-        for (int ci = 0; ci < TMA_NST - 1; ++ci) ring_issue(rg, gq, ci, lane);
-        int bb = 0, j = t;
-        while (j >= c) { j -= c; ++bb; }
-        MmaDesc d = ds[min(bb, nb - 1)];
-        const int ksn = (K + 3) >> 2;
-        const int colb = r * 8;
-        const uint32_t base = (rg.seq % TMA_NST) * TMA_STB + gq.shift;   // see simt_tma_run
-        int ks = 0;
-        for (int ci = 0; ci < gq.nch; ++ci) {
-            ring_wait(rg, ci);
-            // k-steps whose last column ends in chunk ci
-            const int64_t lim = ((int64_t)(ci + 1) * TMA_STB - gq.shift) / colb;   // full columns
-            const int ks1 = (ci == gq.nch - 1 || lim >= K) ? ksn : (int)(lim >> 2);
-#pragma unroll 2
-            for (; ks < ks1; ++ks) {
-                const int col = ks * 4 + t;
-                double a[MT], b[NT];
-#pragma unroll
-                for (int mt = 0; mt < MT; ++mt) {
-                    const int row = mt * 8 + g;
-                    a[mt] = (row < r && col < K) ? ring_ld<double>(rg, base + (uint32_t)(col * r + row) * 8u) : 0.0;
-                }
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {
-                    const int n = nt * 8 + g;
-                    b[nt] = (col < K && j < d.xrows && n < nvc) ? d.p[j + n * d.ld] : 0.0;
-                }
-#pragma unroll
-                for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) dmma(acc.v[mt][nt], a[mt], b[nt]);
-                j += 4;
-                if (j >= c) {
-                    do { j -= c; ++bb; } while (j >= c);
-                    d = ds[min(bb, nb - 1)];
-                }
-            }
-            __syncwarp();
-            fence_proxy_async();
-            ring_issue(rg, gq, ci + TMA_NST - 1, lane);
-        }
-        rg.seq += gq.nch;
-    }
+    return (uint32_t)__cvta_generic_to_shared(p);
 }
 
 // =========================================================================== common helpers
@@ -789,10 +512,6 @@ struct Simt {
             }
         });
     }
-    static constexpr int TSCRATCH = XCAP_BYTES;     // per-warp smem next to the TMA ring
-    __device__ static void tstream(Acc &acc, const T *A0, int r, int c, int nblk, const Blk *blks,
-                                   const Src<T> &src, int nvc, int lane, TmaRing &rg, void *scratch)
-    { simt_tma_stream<T, RPL, NVB>(acc, A0, r, c, nblk, blks, src, nvc, lane, rg, (T *)scratch, XCAP_BYTES / (int)sizeof(T)); }
 };
 
 template <int MT, int NT>
@@ -815,14 +534,7 @@ struct Mma {
     __device__ static void smem_block(Acc &acc, const double *As, int r, int c, const double *xs, int xld, int nvc,
                                       int lane)
     { mma_block<MT, NT, false>(acc, As, r, c, xs, xld, c, nvc, lane, r); }
-    static constexpr int TSCRATCH = 32 * sizeof(MmaDesc);
-    __device__ static void tstream(Acc &acc, const double *A0, int r, int c, int nblk, const Blk *blks,
-                                   const Src<double> &src, int nvc, int lane, TmaRing &rg, void *scratch)
-    { mma_tma_stream<MT, NT>(acc, A0, r, c, nblk, blks, src, nvc, lane, rg, (MmaDesc *)scratch); }
 };
-
-template <typename Eng>
-__host__ __device__ constexpr int warp_tma_bytes() { return TMA_RING + 128 + Eng::TSCRATCH; }
 
 // ---------------------------------------------------------------------------------------
 // Upsweep leaves: x^_s (k x nv) = Vt_s (k x m) x_s (m x nv), Vt = V^T re-laid out at create.
@@ -853,87 +565,23 @@ k_up_leaf(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blk
     }
 }
 
-// Leaf projection fused with the first J upsweep levels: one warp owns a
-// subtree of 2^J sibling leaves, computes their x^ (written for the coupling), and sweeps the J
-// levels above in warp shared memory -- no launch and no global round trip for those levels.
-// Heap addressing: leaf slots g 2^J .. (g+1) 2^J - 1; level (q-j) slots g 2^(J-j) ...
-template <typename T, typename Eng, int J>
-__global__ void __launch_bounds__(WPB * 32, Eng::MINB < 2 ? Eng::MINB : 2)
-k_up_subtree(const Task *__restrict__ leaf_tasks, int ngroups, const Blk *__restrict__ blks,
-             const CallArgs<T> *__restrict__ args, T *__restrict__ xh, int64_t xh_ld, int nv, int SLD,
-             const __grid_constant__ SweepParams lv)     // lv.lv[j-1]: level produced at step j
-{
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    constexpr int NV = Eng::NV;
-    constexpr int NODES = 1 << J;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int grp = blockIdx.x * WPB + wid;
-    if (grp >= ngroups) return;
-    // warp smem: NODES node slots of (SLD x NV), SLD = max rank + 1 (odd: fewer bank conflicts)
-    T *sm = reinterpret_cast<T *>(smem_raw) + (size_t)wid * NODES * NV * SLD;
-    const T *__restrict__ X = args->X;
-    const int64_t ldx = args->ldx;
-    for (int n0 = 0; n0 < nv; n0 += NV) {
-        const int nvc = min(NV, nv - n0);
-        // leaves
-        for (int u = 0; u < NODES; ++u) {
-            const Task tk = leaf_tasks[grp * NODES + u];
-            const Blk b = blks[tk.blk0];
-            typename Eng::Acc acc;
-            acc_zero(acc, lane);
-            Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.c, X + b.x + (int64_t)n0 * ldx, ldx, b.xrows,
-                       nvc, lane);
-            acc_store(acc, xh + tk.out + (int64_t)n0 * xh_ld, xh_ld, tk.r, nvc, lane);
-            __syncwarp();
-            acc_store(acc, sm + (size_t)u * NV * SLD, (int64_t)SLD, tk.r, nvc, lane);
-        }
-        // J levels up, in shared memory (children of slot i are slots 2i, 2i+1; results reuse slot 2i)
-#pragma unroll
-        for (int j = 1; j <= J; ++j) {
-            const SweepLevel L = lv.lv[j - 1];
-            const int64_t blk = (int64_t)L.r * L.c;
-            const int np = NODES >> j;
-            for (int i = 0; i < np; ++i) {
-                const int pslot = grp * np + i;            // parent slot within its level
-                typename Eng::Acc acc;
-                acc_zero(acc, lane);
-                __syncwarp();
-#pragma unroll
-                for (int ch = 0; ch < 2; ++ch) {
-                    const int cs = (2 * i + ch) << (j - 1);  // smem slot holding child 2i+ch
-                    Eng::block(acc, static_cast<const T *>(L.A) + (2 * (int64_t)pslot + ch) * blk, L.r, L.c,
-                               sm + (size_t)cs * NV * SLD, (int64_t)SLD, L.c, nvc, lane);
-                }
-                acc_store(acc, xh + L.obase + (int64_t)pslot * L.r + (int64_t)n0 * xh_ld, xh_ld, L.r, nvc, lane);
-                __syncwarp();
-                acc_store(acc, sm + (size_t)((2 * i) << (j - 1)) * NV * SLD, (int64_t)SLD, L.r, nvc, lane);
-            }
-        }
-        __syncwarp();
-    }
-}
-
 // ---------------------------------------------------------------------------------------
 // Generic row tasks whose x operands and output live in the x^/y^ workspaces:
 //   MODE_WRITE  out  = sum_b A_b x_b    (upsweep transfers, coupling multiply)
 //   MODE_ACCUM  out += sum_b A_b x_b    (downsweep transfers, off-diagonal coupling pass)
-template <typename T, typename Eng, int MODE, bool TMA>
-__global__ void __launch_bounds__(WPB * 32, TMA ? 1 : Eng::MINB)
+template <typename T, typename Eng, int MODE>
+__global__ void __launch_bounds__(WPB * 32, Eng::MINB)
 k_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
        const T *__restrict__ src, int64_t src_ld, T *__restrict__ dst, int64_t dst_ld, int nv)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    // (row, vector chunk) tasks when the launcher sized the grid for them (H2_ROWS_SPLIT):
+    // (row, vector chunk) tasks when the launcher sized the grid for them:
     // the chunks of one row run on adjacent warps instead of in series on one warp
     const int nch = (nv + Eng::NV - 1) / Eng::NV;
     const int S = (int64_t)ntask * nch <= (int64_t)gridDim.x * WPB ? nch : 1;
     if (blockIdx.x * WPB + wid >= ntask * S) return;
-    unsigned char *wsm = smem_raw + (size_t)wid * (TMA ? warp_tma_bytes<Eng>() : Eng::SCRATCH);
-    TmaRing rg{};
-    if (TMA) rg = ring_init(wsm, lane);
-    void *scratch = TMA ? (void *)(wsm + TMA_RING + 128) : (void *)wsm;
-    // grid-stride over tasks (the launcher may cap the grid: persistent bandwidth kernels)
+    void *scratch = smem_raw + (size_t)wid * Eng::SCRATCH;
     for (int vt = blockIdx.x * WPB + wid; vt < ntask * S; vt += gridDim.x * WPB) {
     const int task = vt / S;
     const int ch0 = S == 1 ? 0 : vt - task * S, ch1 = S == 1 ? nch : ch0 + 1;
@@ -946,12 +594,8 @@ k_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
         if ((tk.flags & TF_ACONTIG) && tk.nblk > 0) {
             const Blk b0 = blks[tk.blk0];
             const Src<T> sr{src, src_ld, nullptr, n0};
-            if (TMA)
-                Eng::tstream(acc, static_cast<const T *>(b0.A), tk.r, tk.c, tk.nblk, blks + tk.blk0, sr, nvc,
-                             lane, rg, scratch);
-            else
-                Eng::stream(acc, static_cast<const T *>(b0.A), tk.r, tk.c, tk.nblk, blks + tk.blk0, sr, nvc,
-                            lane, scratch);
+            Eng::stream(acc, static_cast<const T *>(b0.A), tk.r, tk.c, tk.nblk, blks + tk.blk0, sr, nvc, lane,
+                        scratch);
             acc_store(acc, dst + tk.out + (int64_t)n0 * dst_ld, dst_ld, tk.r, nvc, lane);
             continue;
         }
@@ -1070,19 +714,6 @@ k_sweep(const __grid_constant__ SweepParams p, T *__restrict__ buf, int64_t ld, 
     }
 }
 
-#ifdef H2_TU_COMMON
-__global__ void k_prefetch_l2(const PrefetchList pl)
-{
-    // one CTA per range: L2 prefetch (evict_last) of the small top-level transfer blocks, read
-    // late by latency-bound sweep levels (PAPER.md:263, 408 top of the trees)
-    if (blockIdx.x >= pl.n) return;
-    const char *p = static_cast<const char *>(pl.ptr[blockIdx.x]);
-    const int64_t bytes = pl.bytes[blockIdx.x];
-    for (int64_t o = (int64_t)threadIdx.x * 128; o < bytes; o += (int64_t)blockDim.x * 128)
-        asm volatile("prefetch.global.L2::evict_last [%0];\n" ::"l"(p + o));
-}
-#endif
-
 // ---------------------------------------------------------------------------------------
 // Fused tree stage: one CTA owns a subtree and runs `nlev` consecutive transfer levels of it,
 // level by level, with a CTA barrier between levels (the upsweep levels q-1 .. 0 or the
@@ -1123,128 +754,6 @@ k_tree(TreeStage st, const Task *__restrict__ tasks, const Blk *__restrict__ blk
             }
         }
         __syncthreads();   // level lv complete (global writes visible to the CTA) before lv + 1
-    }
-}
-
-// ---------------------------------------------------------------------------------------
-// Dependency-driven tree sweep in ONE launch (upsweep transfers bottom-up, or downsweep transfers
-// top-down): warps take tasks in topological order from an atomic
-// ticket, wait until the task's tree neighbours (children for the upsweep, the parent for the
-// downsweep) have published this call's epoch in their completion flags, compute, and publish
-// their own flag.  A parent starts as soon as its own children are done -- no per-level launch
-// or grid barrier.  Tickets are handed out in order and every dependency has a smaller ticket
-// held by a running warp, so the waits cannot deadlock.
-__device__ __forceinline__ int ld_acquire(const int32_t *p)
-{
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_release(int32_t *p, int v)
-{
-    asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-
-template <typename T, typename Eng, int MODE>
-__global__ void __launch_bounds__(WPB * 32, Eng::MINB)
-k_chain(const Task *__restrict__ tasks, const ChainDep *__restrict__ deps, int ntask,
-        const Blk *__restrict__ blks, T *__restrict__ buf, int64_t ld, int nv, int32_t *flags,
-        CallArgs<T> *args, int which)
-{
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    void *scratch = smem_raw + wid * Eng::SCRATCH;
-    const int epoch = *((volatile int32_t *)&args->epoch);
-    unsigned *ticket = &args->ticket[which];
-    for (;;) {
-        int t = 0;
-        if (lane == 0) t = (int)atomicAdd(ticket, 1u);
-        t = __shfl_sync(FULL, t, 0);
-        if (t >= ntask) break;
-        const ChainDep dp = deps[t];
-        if (lane == 0) {
-            if (dp.dep0 >= 0) while (ld_acquire(flags + dp.dep0) != epoch) __nanosleep(20);
-            if (dp.dep1 >= 0) while (ld_acquire(flags + dp.dep1) != epoch) __nanosleep(20);
-            __threadfence();           // (CCTL.IVALL) no stale L1 lines of the producers' outputs
-        }
-        __syncwarp();
-        const Task tk = tasks[t];
-        for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
-            const int nvc = min(Eng::NV, nv - n0);
-            typename Eng::Acc acc;
-            if (MODE == MODE_ACCUM) acc_load(acc, buf + tk.out + (int64_t)n0 * ld, ld, tk.r, nvc, lane);
-            else acc_zero(acc, lane);
-            if (tk.flags & TF_ACONTIG) {
-                const Src<T> sr{buf, ld, nullptr, n0};
-                Eng::stream(acc, static_cast<const T *>(blks[tk.blk0].A), tk.r, tk.c, tk.nblk, blks + tk.blk0,
-                            sr, nvc, lane, scratch);
-            } else {
-                for (int bi = 0; bi < tk.nblk; ++bi) {
-                    const Blk b = blks[tk.blk0 + bi];
-                    Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.c, buf + b.x + (int64_t)n0 * ld, ld,
-                               b.xrows, nvc, lane);
-                }
-            }
-            acc_store(acc, buf + tk.out + (int64_t)n0 * ld, ld, tk.r, nvc, lane);
-        }
-        __syncwarp();
-        if (lane == 0) {
-            __threadfence();
-            st_release(flags + dp.self, epoch);
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------------------
-// Leaf kernel: last downsweep transfer + leaf expansion, added into Y:
-//   z_t = y^_t + E_t y^_parent ;  Y_t += alpha U_t z_t
-// blocks: [E_t (if TF_HAS_E), x = parent y^ offset] [U_t, x = own y^ offset].  k_dense has
-// already written Y = alpha A_de X + beta Y on the dense stream (reading R11).
-// EngK computes z (rows k), EngM the leaf rows (m); z is handed over through warp smem.
-template <typename T, typename EngK, typename EngM>
-__global__ void __launch_bounds__(WPB * 32, (EngM::MINB < EngK::MINB ? EngM::MINB : EngK::MINB) < 3 ? (EngM::MINB < EngK::MINB ? EngM::MINB : EngK::MINB) : 3)
-k_leaf_u(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
-         const T *__restrict__ yh, int64_t yh_ld, const CallArgs<T> *__restrict__ args, int nv, int k,
-         int kp)
-{
-    T *__restrict__ Y = args->Y;
-    const int64_t ldy = args->ldy;
-    const T alpha = args->alpha;
-    static_assert(EngK::NV == EngM::NV, "engines must agree on the vector chunk");
-    constexpr int NV = EngM::NV;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int task = blockIdx.x * WPB + wid;
-    if (task >= ntask) return;
-    T *zs = reinterpret_cast<T *>(smem_raw) + wid * NV * ZLD;
-    const Task tk = tasks[task];
-    const bool hasE = tk.flags & TF_HAS_E;
-    const Blk bU = blks[tk.blk0 + (hasE ? 1 : 0)];
-    for (int n0 = 0; n0 < nv; n0 += NV) {
-        const int nvc = min(NV, nv - n0);
-        typename EngK::Acc z;
-        acc_load(z, yh + bU.x + (int64_t)n0 * yh_ld, yh_ld, k, nvc, lane);
-        if (hasE) {
-            const Blk bE = blks[tk.blk0];
-            EngK::block(z, static_cast<const T *>(bE.A), k, kp, yh + bE.x + (int64_t)n0 * yh_ld, yh_ld,
-                        bE.xrows, nvc, lane);
-        }
-        __syncwarp();
-        acc_store(z, zs, (int64_t)ZLD, k, nvc, lane);
-        __syncwarp();
-        typename EngM::Acc acc;
-        acc_zero(acc, lane);
-        EngM::block(acc, static_cast<const T *>(bU.A), tk.r, k, zs, (int64_t)ZLD, k, nvc, lane);
-        T *Yb = Y + tk.out + (int64_t)n0 * ldy;
-        const int rows = tk.rows;
-        acc.each(lane, [&](int row, int n, auto &v) {
-            if (row < rows && n < nvc) {
-                T *p = Yb + row + n * ldy;
-                *p = fma(alpha, (T)v, *p);
-            }
-        });
-        __syncwarp();
     }
 }
 
@@ -1315,238 +824,11 @@ k_leaf_dense(const Task *__restrict__ ltasks, const Task *__restrict__ dtasks, i
     }
 }
 
-// ---------------------------------------------------------------------------------------
-// Scheduled upsweep + coupling (one persistent launch): entries in topological order
-//   ST_UPLEAF s  : x^_s = V_s^T x_s                          -> flag(q, s), counter[q]++
-//   ST_UP (lc,i) : wait flags of children (lc,2i),(lc,2i+1); x^_i = sum F^T x^_c -> flag, counter
-//   ST_COUP t    : wait counter[level] == nodes[level]; y^_t = sum_s S_ts x^_s  (alg:mult)
-// The schedule interleaves the levels (up q-1, coupling q, up q-2, coupling q-1, ...), so the
-// latency-bound tree levels run while other warps stream coupling blocks.
-__device__ __forceinline__ void wait_flag(const int32_t *f, int epoch)
-{
-    while (ld_acquire(f) != epoch) __nanosleep(32);
-}
-
-__device__ __forceinline__ void wait_count(const int32_t *c, int target)
-{
-    while (ld_acquire(c) < target) __nanosleep(64);
-}
-
-template <typename T, typename Eng>
-__global__ void __launch_bounds__(WPB * 32, Eng::MINB < 2 ? Eng::MINB : 2)
-k_mega_up(const SchedEntry *__restrict__ sched, int nsched, const __grid_constant__ MegaParams mp,
-          const Task *__restrict__ tasks, const Blk *__restrict__ blks, const Task *__restrict__ upleaf,
-          T *__restrict__ xh, int64_t xh_ld, T *__restrict__ yh, int64_t yh_ld, int32_t *flags,
-          int32_t *counters, CallArgs<T> *args, int nv)
-{
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    void *scratch = smem_raw + wid * Eng::SCRATCH;
-    const int epoch = *((volatile int32_t *)&args->epoch);
-    const T *__restrict__ X = args->X;
-    const int64_t ldx = args->ldx;
-    unsigned *ticket = &args->ticket[2];
-    int next = 0;
-    if (lane == 0) next = (int)atomicAdd(ticket, 1u);
-    for (;;) {
-        const int t = __shfl_sync(FULL, next, 0);
-        if (t >= nsched) break;
-        if (lane == 0) next = (int)atomicAdd(ticket, 1u);     // prefetch the next ticket
-        const SchedEntry e = sched[t];
-        int32_t *done_flag = nullptr;
-        int32_t *done_cnt = nullptr;
-        if (e.type == ST_UPLEAF) {
-            const Task tk = upleaf[e.idx];
-            const Blk b = blks[tk.blk0];
-            for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
-                const int nvc = min(Eng::NV, nv - n0);
-                typename Eng::Acc acc;
-                acc_zero(acc, lane);
-                Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.c, X + b.x + (int64_t)n0 * ldx, ldx, b.xrows,
-                           nvc, lane);
-                acc_store(acc, xh + tk.out + (int64_t)n0 * xh_ld, xh_ld, tk.r, nvc, lane);
-            }
-            done_flag = flags + mp.fbase[mp.q] + e.idx;
-            done_cnt = counters + mp.q;
-        } else if (e.type == ST_UP) {
-            const int lc = e.level, i = e.idx;
-            if (lane == 0) {
-                wait_flag(flags + mp.fbase[lc] + 2 * i, epoch);
-                wait_flag(flags + mp.fbase[lc] + 2 * i + 1, epoch);
-                __threadfence();
-            }
-            __syncwarp();
-            const SweepLevel Lv = mp.up[lc];
-            const int64_t blk = (int64_t)Lv.r * Lv.c;
-            for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
-                const int nvc = min(Eng::NV, nv - n0);
-                typename Eng::Acc acc;
-                acc_zero(acc, lane);
-#pragma unroll
-                for (int ch = 0; ch < 2; ++ch)
-                    Eng::block(acc, static_cast<const T *>(Lv.A) + (2 * (int64_t)i + ch) * blk, Lv.r, Lv.c,
-                               xh + Lv.xbase + (2 * (int64_t)i + ch) * Lv.c + (int64_t)n0 * xh_ld, xh_ld, Lv.c, nvc,
-                               lane);
-                acc_store(acc, xh + Lv.obase + (int64_t)i * Lv.r + (int64_t)n0 * xh_ld, xh_ld, Lv.r, nvc, lane);
-            }
-            done_flag = flags + mp.fbase[lc - 1] + i;
-            done_cnt = counters + (lc - 1);
-        } else {   // ST_COUP
-            if (lane == 0) {
-                wait_count(counters + e.level, mp.nodes[e.level]);
-                __threadfence();
-            }
-            __syncwarp();
-            const Task tk = tasks[e.idx];
-            for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
-                const int nvc = min(Eng::NV, nv - n0);
-                typename Eng::Acc acc;
-                acc_zero(acc, lane);
-                if ((tk.flags & TF_ACONTIG) && tk.nblk > 0) {
-                    const Src<T> sr{xh, xh_ld, nullptr, n0};
-                    Eng::stream(acc, static_cast<const T *>(blks[tk.blk0].A), tk.r, tk.c, tk.nblk, blks + tk.blk0, sr,
-                                nvc, lane, scratch);
-                } else {
-                    for (int bi = 0; bi < tk.nblk; ++bi) {
-                        const Blk b = blks[tk.blk0 + bi];
-                        const int64_t ld = b.xld ? (int64_t)b.xld : xh_ld;
-                        Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.c, xh + b.x + (int64_t)n0 * ld, ld,
-                                   b.xrows, nvc, lane);
-                    }
-                }
-                acc_store(acc, yh + tk.out + (int64_t)n0 * yh_ld, yh_ld, tk.r, nvc, lane);
-            }
-        }
-        if (done_flag) {
-            __syncwarp();
-            if (lane == 0) {
-                __threadfence();
-                st_release(done_flag, epoch);
-                atomicAdd(done_cnt, 1);
-            }
-        }
-    }
-}
-
-// Scheduled downsweep + leaves (one persistent launch):
-//   ST_DOWN (l,c): wait flag(l-1, c/2) (if computed here); y^_c += E_c y^_parent -> flag(l, c)
-//   ST_LEAF t    : dense row first (needs only X), then wait flag(q-1, t/2), z = y^_t + E_t y^_p,
-//                  Y_t = alpha (U_t z + sum D x) + beta Y_t
-template <typename T, typename EngK, typename EngM>
-__global__ void __launch_bounds__(WPB * 32, (EngM::MINB < EngK::MINB ? EngM::MINB : EngK::MINB) < 2 ? (EngM::MINB < EngK::MINB ? EngM::MINB : EngK::MINB) : 2)
-k_mega_down(const SchedEntry *__restrict__ sched, int nsched, const __grid_constant__ MegaParams mp,
-            const Task *__restrict__ ltasks, const Task *__restrict__ dtasks, const Blk *__restrict__ blks,
-            T *__restrict__ yh, int64_t yh_ld, const T *__restrict__ halo, int32_t *flags, CallArgs<T> *args, int nv)
-{
-    static_assert(EngK::NV == EngM::NV, "engines must agree on the vector chunk");
-    constexpr int NV = EngM::NV;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    T *zs = reinterpret_cast<T *>(smem_raw) + wid * NV * ZLD;
-    void *scratch = smem_raw + (size_t)WPB * NV * ZLD * sizeof(T) + wid * EngM::SCRATCH;
-    const int epoch = *((volatile int32_t *)&args->epoch);
-    const T *__restrict__ X = args->X;
-    T *__restrict__ Y = args->Y;
-    const int64_t ldx = args->ldx, ldy = args->ldy;
-    const T alpha = args->alpha, beta = args->beta;
-    unsigned *ticket = &args->ticket[3];
-    const int q = mp.q;
-    int next = 0;
-    if (lane == 0) next = (int)atomicAdd(ticket, 1u);
-    for (;;) {
-        const int t = __shfl_sync(FULL, next, 0);
-        if (t >= nsched) break;
-        if (lane == 0) next = (int)atomicAdd(ticket, 1u);
-        const SchedEntry e = sched[t];
-        if (e.type == ST_DOWN) {
-            const int l = e.level, c = e.idx;
-            if (l - 1 >= mp.dn_first) {
-                if (lane == 0) {
-                    wait_flag(flags + mp.fbase[l - 1] + (c >> 1), epoch);
-                    __threadfence();
-                }
-                __syncwarp();
-            }
-            const SweepLevel Lv = mp.dn[l];
-            const int64_t blk = (int64_t)Lv.r * Lv.c;
-            for (int n0 = 0; n0 < nv; n0 += NV) {
-                const int nvc = min(NV, nv - n0);
-                typename EngK::Acc acc;
-                T *out = yh + Lv.obase + (int64_t)c * Lv.r + (int64_t)n0 * yh_ld;
-                acc_load(acc, out, yh_ld, Lv.r, nvc, lane);
-                EngK::block(acc, static_cast<const T *>(Lv.A) + c * blk, Lv.r, Lv.c,
-                            yh + Lv.xbase + (int64_t)(c >> 1) * Lv.c + (int64_t)n0 * yh_ld, yh_ld, Lv.c, nvc, lane);
-                acc_store(acc, out, yh_ld, Lv.r, nvc, lane);
-            }
-            __syncwarp();
-            if (lane == 0) {
-                __threadfence();
-                st_release(flags + mp.fbase[l] + c, epoch);
-            }
-            continue;
-        }
-        // ST_LEAF
-        const Task tk = ltasks[e.idx];
-        const Task dk = dtasks[e.idx];
-        const bool hasE = tk.flags & TF_HAS_E;
-        const Blk bU = blks[tk.blk0 + (hasE ? 1 : 0)];
-        bool waited = false;
-        for (int n0 = 0; n0 < nv; n0 += NV) {
-            const int nvc = min(NV, nv - n0);
-            typename EngM::Acc acc;
-            acc_zero(acc, lane);
-            if ((dk.flags & TF_ACONTIG) && dk.nblk > 0) {
-                const Src<T> sr{X, ldx, halo, n0};
-                EngM::stream(acc, static_cast<const T *>(blks[dk.blk0].A), dk.r, dk.c, dk.nblk, blks + dk.blk0, sr,
-                             nvc, lane, scratch);
-            } else {
-                for (int bi = 0; bi < dk.nblk; ++bi) {
-                    const Blk b = blks[dk.blk0 + bi];
-                    const T *src;
-                    int64_t ld;
-                    if (b.x >= 0) { src = X + b.x; ld = ldx; }
-                    else          { src = halo + (-b.x - 1); ld = b.xld; }
-                    EngM::block(acc, static_cast<const T *>(b.A), dk.r, dk.c, src + (int64_t)n0 * ld, ld, b.xrows,
-                                nvc, lane);
-                }
-            }
-            if (!waited && hasE && q - 1 >= mp.dn_first) {
-                if (lane == 0) {
-                    wait_flag(flags + mp.fbase[q - 1] + (e.idx >> 1), epoch);
-                    __threadfence();
-                }
-                __syncwarp();
-                waited = true;
-            }
-            typename EngK::Acc z;
-            acc_load(z, yh + bU.x + (int64_t)n0 * yh_ld, yh_ld, mp.k, nvc, lane);
-            if (hasE) {
-                const Blk bE = blks[tk.blk0];
-                EngK::block(z, static_cast<const T *>(bE.A), mp.k, mp.kp, yh + bE.x + (int64_t)n0 * yh_ld, yh_ld,
-                            bE.xrows, nvc, lane);
-            }
-            __syncwarp();
-            acc_store(z, zs, (int64_t)ZLD, mp.k, nvc, lane);
-            __syncwarp();
-            EngM::block(acc, static_cast<const T *>(bU.A), tk.r, mp.k, zs, (int64_t)ZLD, mp.k, nvc, lane);
-            T *Yb = Y + tk.out + (int64_t)n0 * ldy;
-            const int rows = tk.rows;
-            acc.each(lane, [&](int row, int n, auto &v) {
-                if (row < rows && n < nvc) {
-                    T *p = Yb + row + n * ldy;
-                    *p = (beta == T(0)) ? alpha * v : fma(alpha, (T)v, beta * *p);
-                }
-            });
-            __syncwarp();
-        }
-    }
-}
-
 // Row-split fused leaf kernel for the DMMA path with m > 32 (nv >= 5): two warps per leaf, each
 // owning 32 rows of U_t and of the dense row (lda = m), so the accumulator is Mma<4,NT> instead
 // of Mma<8,NT> (no register spills, twice the warps in flight).  z_t is computed by both.
 template <typename T, typename EngK, typename EngH>
-__global__ void __launch_bounds__(WPB * 32, H2_SPLIT_MINB)
+__global__ void __launch_bounds__(WPB * 32, 2)
 k_leaf_dense_split(const Task *__restrict__ ltasks, const Task *__restrict__ dtasks, int ntask2,
                    const Blk *__restrict__ blks, const T *__restrict__ yh, int64_t yh_ld,
                    const CallArgs<T> *__restrict__ args, const T *__restrict__ halo, int nv, int k, int kp, int m)
@@ -1617,69 +899,10 @@ k_leaf_dense_split(const Task *__restrict__ ltasks, const Task *__restrict__ dta
     }
 }
 
-// Dense near field + epilogue (reading R12), on its own low-priority stream
-// concurrent with the tree phases:  Y_t = alpha sum_s D_ts x_s + beta Y_t  (beta == 0: Y is
-// write-only).  Every leaf has a task (rows without dense blocks still apply beta).
-template <typename T, typename Eng, bool TMA>
-__global__ void __launch_bounds__(WPB * 32, TMA ? 1 : Eng::MINB)
-k_dense(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
-        const CallArgs<T> *__restrict__ args, const T *__restrict__ halo, int nv)
-{
-    const T *__restrict__ X = args->X;
-    T *__restrict__ Y = args->Y;
-    const int64_t ldx = args->ldx, ldy = args->ldy;
-    const T alpha = args->alpha, beta = args->beta;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (blockIdx.x * WPB + wid >= ntask) return;
-    unsigned char *wsm = smem_raw + (size_t)wid * (TMA ? warp_tma_bytes<Eng>() : Eng::SCRATCH);
-    TmaRing rg{};
-    if (TMA) rg = ring_init(wsm, lane);
-    void *scratch = TMA ? (void *)(wsm + TMA_RING + 128) : (void *)wsm;
-    for (int task = blockIdx.x * WPB + wid; task < ntask; task += gridDim.x * WPB) {
-    const Task tk = tasks[task];
-    for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
-        const int nvc = min(Eng::NV, nv - n0);
-        typename Eng::Acc acc;
-        acc_zero(acc, lane);
-        if ((tk.flags & TF_ACONTIG) && tk.nblk > 0) {
-            const Src<T> sr{X, ldx, halo, n0};
-            if (TMA)
-                Eng::tstream(acc, static_cast<const T *>(blks[tk.blk0].A), tk.r, tk.c, tk.nblk, blks + tk.blk0,
-                             sr, nvc, lane, rg, scratch);
-            else
-                Eng::stream(acc, static_cast<const T *>(blks[tk.blk0].A), tk.r, tk.c, tk.nblk, blks + tk.blk0,
-                            sr, nvc, lane, scratch);
-        } else {
-            for (int bi = 0; bi < tk.nblk; ++bi) {
-                const Blk b = blks[tk.blk0 + bi];
-                const T *src;
-                int64_t ld;
-                if (b.x >= 0) { src = X + b.x; ld = ldx; }
-                else          { src = halo + (-b.x - 1); ld = b.xld; }
-                Eng::block(acc, static_cast<const T *>(b.A), tk.r, tk.c, src + (int64_t)n0 * ld, ld,
-                           b.xrows, nvc, lane);
-            }
-        }
-        T *Yb = Y + tk.out + (int64_t)n0 * ldy;
-        const int rows = tk.rows;
-        acc.each(lane, [&](int row, int n, auto &v) {
-            if (row < rows && n < nvc) {
-                T *p = Yb + row + n * ldy;
-                *p = (beta == T(0)) ? alpha * v : fma(alpha, (T)v, beta * *p);
-            }
-        });
-    }
-    }
-}
-
 template <typename T>
 __global__ void k_set_args(CallArgs<T> *a, const T *X, int64_t ldx, T *Y, int64_t ldy, T alpha, T beta)
 {
     a->X = X; a->ldx = ldx; a->Y = Y; a->ldy = ldy; a->alpha = alpha; a->beta = beta;
-    a->epoch = a->epoch + 1;
-    for (int i = 0; i < 4; ++i) a->ticket[i] = 0;
-    for (int i = 0; i < a->ncounters; ++i) a->counters[i] = 0;
 }
 
 template <typename T>
@@ -1739,39 +962,20 @@ static inline void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[2];
-    int na = 0;
-    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[na++].val.programmaticStreamSerializationAllowed = 1;
-    if (g_launch_priority != 0) {
-        at[na].id = cudaLaunchAttributePriority;
-        at[na++].val.priority = g_launch_priority;
-    }
-    cfg.attrs = at;
-    cfg.numAttrs = na;
-    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-}
-
-// kernel<<<grid, block, smem, s>>>(args...) with the per-launch priority g_launch_priority
-template <typename... KArgs, typename... Args>
-static inline void launch_pri(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
-                              Args &&...args)
-{
-    if (g_launch_priority == 0) {
-        kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
-        return;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(block);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
     cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributePriority;
-    at[0].val.priority = g_launch_priority;
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// dynamic shared memory opt-in, once per kernel instantiation
+template <typename K>
+static inline cudaError_t smem_opt_in(K kern, size_t bytes)
+{
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 template <typename T>
@@ -1837,44 +1041,40 @@ cudaError_t launch_set_args(CallArgs<T> *a, const T *X, int64_t ldx, T *Y, int64
     return cudaGetLastError();
 }
 
+// Grids of the warp-task kernels carry one warp per (task, vector chunk): when nv exceeds the
+// engine's chunk, the chunks of one task run on adjacent warps instead of in series on one warp
+// (the repeated block reads then hit L2).
 template <typename T>
 cudaError_t launch_up_leaf(const Task *t, int ntask, const Blk *b, const CallArgs<T> *args,
                            T *xh, int64_t xh_ld, int nv, int r, cudaStream_t s)
 {
     if (ntask == 0) return cudaSuccess;
     Dispatch<T>::run(r, nv, [&](auto e) {
-        static const bool vsplit = !(getenv("H2_LEAF_VSPLIT") && getenv("H2_LEAF_VSPLIT")[0] == '0');
-        const int nch = vsplit ? (nv + decltype(e)::NV - 1) / decltype(e)::NV : 1;
+        const int nch = (nv + decltype(e)::NV - 1) / decltype(e)::NV;
         k_up_leaf<T, decltype(e)><<<grid_for(ntask * nch), WPB * 32, 0, s>>>(t, ntask, b, args, xh, xh_ld, nv);
     });
     return cudaGetLastError();
 }
 
-template <typename T, bool TMA>
-cudaError_t launch_rows_t(int mode, const Task *t, int ntask, const Blk *b, const T *src,
-                          int64_t src_ld, T *dst, int64_t dst_ld, int nv, int r, int max_ctas, cudaStream_t s)
+template <typename T>
+cudaError_t launch_rows(int mode, const Task *t, int ntask, const Blk *b, const T *src, int64_t src_ld, T *dst,
+                        int64_t dst_ld, int nv, int r, cudaStream_t s)
 {
     if (ntask == 0) return cudaSuccess;
     cudaError_t err = cudaSuccess;
     Dispatch<T>::run(r, nv, [&](auto e) {
         using E = decltype(e);
-        const size_t sm = (size_t)WPB * (TMA ? warp_tma_bytes<E>() : E::SCRATCH);
-        auto kw = k_rows<T, E, MODE_WRITE, TMA>;
-        auto ka = k_rows<T, E, MODE_ACCUM, TMA>;
-        static bool attr_set = false;
-        if (!attr_set) {
-            err = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            if (err == cudaSuccess) err = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            attr_set = (err == cudaSuccess);
-        }
-        if (err != cudaSuccess) return;
-        static const bool split = !(getenv("H2_ROWS_SPLIT") && getenv("H2_ROWS_SPLIT")[0] == '0');
+        const size_t sm = (size_t)WPB * E::SCRATCH;
+        auto kw = k_rows<T, E, MODE_WRITE>;
+        auto ka = k_rows<T, E, MODE_ACCUM>;
+        static cudaError_t attr = [&] {
+            cudaError_t e1 = smem_opt_in(kw, sm);
+            return e1 == cudaSuccess ? smem_opt_in(ka, sm) : e1;
+        }();
+        if ((err = attr) != cudaSuccess) return;
         const int nch = (nv + E::NV - 1) / E::NV;
-        const int grid = max_ctas > 0 ? min(grid_for(ntask), max_ctas) : grid_for(split ? ntask * nch : ntask);
-        if (mode == MODE_WRITE)
-            launch_pri(kw, grid, WPB * 32, sm, s, t, ntask, b, src, src_ld, dst, dst_ld, nv);
-        else
-            launch_pri(ka, grid, WPB * 32, sm, s, t, ntask, b, src, src_ld, dst, dst_ld, nv);
+        if (mode == MODE_WRITE) kw<<<grid_for(ntask * nch), WPB * 32, sm, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv);
+        else                    ka<<<grid_for(ntask * nch), WPB * 32, sm, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv);
     });
     if (err != cudaSuccess) return err;
     return cudaGetLastError();
@@ -1897,54 +1097,24 @@ cudaError_t launch_tree(int mode, const TreeStage &st, int nctas, const Task *t,
 }
 
 template <typename T>
-cudaError_t launch_leaf_u(const Task *t, int ntask, const Blk *b, const T *yh, int64_t yh_ld,
-                          const CallArgs<T> *args, int nv, int k, int kp, int m, cudaStream_t s)
-{
-    if (ntask == 0) return cudaSuccess;
-    cudaError_t err = cudaSuccess;
-    Dispatch<T>::run2(k, m, nv, [&](auto ek, auto em) {
-        using EK = decltype(ek);
-        using EM = decltype(em);
-        auto kern = k_leaf_u<T, EK, EM>;
-        const size_t sm = (size_t)WPB * EM::NV * ZLD * sizeof(T);
-        if (sm > 48 * 1024) {
-            static bool attr_set = false;       // once per instantiation
-            if (!attr_set) {
-                err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-                attr_set = (err == cudaSuccess);
-            }
-        }
-        if (err == cudaSuccess)
-            kern<<<grid_for(ntask), WPB * 32, sm, s>>>(t, ntask, b, yh, yh_ld, args, nv, k, kp);
-    });
-    if (err != cudaSuccess) return err;
-    return cudaGetLastError();
-}
-
-template <typename T>
 cudaError_t launch_leaf_dense(const Task *lt, const Task *dt, int ntask, const Blk *b, const T *yh, int64_t yh_ld,
                               const CallArgs<T> *args, const T *halo, int nv, int k, int kp, int m, cudaStream_t s)
 {
     if (ntask == 0) return cudaSuccess;
     cudaError_t err = cudaSuccess;
     if constexpr (std::is_same<T, double>::value) {
-        static const bool split_on = !(getenv("H2_SPLIT") && getenv("H2_SPLIT")[0] == '0');
-        if (split_on && nv >= 5 && m > 32) {
+        if (nv >= 5 && m > 32) {
+            // DMMA path with 64-row leaves: two warps per leaf (k_leaf_dense_split)
             auto go = [&](auto ek, auto eh) {
                 using EK = decltype(ek);
                 using EH = decltype(eh);
                 auto kern = k_leaf_dense_split<double, EK, EH>;
                 const size_t sm = (size_t)WPB * (EH::NV * ZLD * sizeof(double) + EH::SCRATCH);
-                static bool attr_set = false;
-                if (!attr_set) {
-                    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-                    attr_set = (err == cudaSuccess);
-                }
-                static const bool vsplit = !(getenv("H2_LEAF_VSPLIT") && getenv("H2_LEAF_VSPLIT")[0] == '0');
-                const int nch = vsplit ? (nv + EH::NV - 1) / EH::NV : 1;
-                if (err == cudaSuccess)
-                    kern<<<grid_for(2 * ntask * nch), WPB * 32, sm, s>>>(lt, dt, 2 * ntask, b, yh, yh_ld, args,
-                                                                         halo, nv, k, kp, m);
+                static cudaError_t attr = smem_opt_in(kern, sm);
+                if ((err = attr) != cudaSuccess) return;
+                const int nch = (nv + EH::NV - 1) / EH::NV;
+                kern<<<grid_for(2 * ntask * nch), WPB * 32, sm, s>>>(lt, dt, 2 * ntask, b, yh, yh_ld, args, halo,
+                                                                     nv, k, kp, m);
             };
             Dispatch<double>::run(k, nv, [&](auto ek) {
                 using EK = decltype(ek);
@@ -1960,154 +1130,22 @@ cudaError_t launch_leaf_dense(const Task *lt, const Task *dt, int ntask, const B
         using EM = decltype(em);
         auto kern = k_leaf_dense<T, EK, EM>;
         const size_t sm = (size_t)WPB * (EM::NV * ZLD * sizeof(T) + EM::SCRATCH);
-        static bool attr_set = false;
-        if (!attr_set) {
-            err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            attr_set = (err == cudaSuccess);
-        }
-        if (err == cudaSuccess)
-            kern<<<grid_for(ntask), WPB * 32, sm, s>>>(lt, dt, ntask, b, yh, yh_ld, args, halo, nv, k, kp);
+        static cudaError_t attr = smem_opt_in(kern, sm);
+        if ((err = attr) != cudaSuccess) return;
+        kern<<<grid_for(ntask), WPB * 32, sm, s>>>(lt, dt, ntask, b, yh, yh_ld, args, halo, nv, k, kp);
     });
     if (err != cudaSuccess) return err;
     return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t launch_mega_up(const SchedEntry *sched, int n, const MegaParams &mp, const Task *tasks, const Blk *blks,
-                           const Task *upleaf_tasks, T *xh, int64_t xh_ld, T *yh, int64_t yh_ld, int32_t *flags,
-                           int32_t *counters, CallArgs<T> *args, int nv, int r, int grid, cudaStream_t s)
-{
-    if (n == 0) return cudaSuccess;
-    Dispatch<T>::run(r, nv, [&](auto e) {
-        using E = decltype(e);
-        const size_t sm = (size_t)WPB * E::SCRATCH;
-        k_mega_up<T, E><<<grid, WPB * 32, sm, s>>>(sched, n, mp, tasks, blks, upleaf_tasks, xh, xh_ld, yh, yh_ld, flags,
-                                                   counters, args, nv);
-    });
-    return cudaGetLastError();
-}
-
-template <typename T>
-cudaError_t launch_mega_down(const SchedEntry *sched, int n, const MegaParams &mp, const Task *ltasks,
-                             const Task *dtasks, const Blk *blks, T *yh, int64_t yh_ld, const T *halo,
-                             int32_t *flags, CallArgs<T> *args, int nv, int m, int grid, cudaStream_t s)
-{
-    if (n == 0) return cudaSuccess;
-    cudaError_t err = cudaSuccess;
-    Dispatch<T>::run2(mp.kmax, m, nv, [&](auto ek, auto em) {
-        using EK = decltype(ek);
-        using EM = decltype(em);
-        auto kern = k_mega_down<T, EK, EM>;
-        const size_t sm = (size_t)WPB * (EM::NV * ZLD * sizeof(T) + EM::SCRATCH);
-        static bool attr_set = false;
-        if (!attr_set) {
-            err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            attr_set = (err == cudaSuccess);
-        }
-        if (err == cudaSuccess)
-            kern<<<grid, WPB * 32, sm, s>>>(sched, n, mp, ltasks, dtasks, blks, yh, yh_ld, halo, flags, args, nv);
-    });
-    if (err != cudaSuccess) return err;
-    return cudaGetLastError();
-}
-
-template <typename T, bool TMA>
-cudaError_t launch_dense_t(const Task *t, int ntask, const Blk *b, const CallArgs<T> *args, const T *halo,
-                           int nv, int m, int max_ctas, cudaStream_t s)
-{
-    if (ntask == 0) return cudaSuccess;
-    cudaError_t err = cudaSuccess;
-    Dispatch<T>::run(m, nv, [&](auto e) {
-        using E = decltype(e);
-        const size_t sm = (size_t)WPB * (TMA ? warp_tma_bytes<E>() : E::SCRATCH);
-        auto kd = k_dense<T, E, TMA>;
-        static bool attr_set = false;
-        if (!attr_set) {
-            err = cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            attr_set = (err == cudaSuccess);
-        }
-        if (err != cudaSuccess) return;
-        const int grid = max_ctas > 0 ? min(grid_for(ntask), max_ctas) : grid_for(ntask);
-        kd<<<grid, WPB * 32, sm, s>>>(t, ntask, b, args, halo, nv);
-    });
-    if (err != cudaSuccess) return err;
-    return cudaGetLastError();
-}
-
-template <typename T>
-cudaError_t launch_up_subtree(const Task *leaf_tasks, int nleaf, const Blk *b, const CallArgs<T> *args, T *xh,
-                              int64_t xh_ld, int nv, int r, int J, const SweepParams &lv, cudaStream_t s)
-{
-    if (nleaf == 0) return cudaSuccess;
-    cudaError_t err = cudaSuccess;
-    Dispatch<T>::run(r, nv, [&](auto e) {
-        using E = decltype(e);
-        auto go = [&](auto jc) {
-            constexpr int JJ = decltype(jc)::value;
-            auto kern = k_up_subtree<T, E, JJ>;
-            const int sld = r | 1;
-            const size_t sm = (size_t)WPB * (1 << JJ) * E::NV * sld * sizeof(T);
-            static bool attr_set = false;       // sized once for the largest rank (KMAX + 1)
-            if (!attr_set) {
-                const size_t smax = (size_t)WPB * (1 << JJ) * E::NV * (KMAX + 1) * sizeof(T);
-                err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
-                attr_set = (err == cudaSuccess);
-            }
-            const int ng = nleaf >> JJ;
-            if (err == cudaSuccess)
-                kern<<<grid_for(ng), WPB * 32, sm, s>>>(leaf_tasks, ng, b, args, xh, xh_ld, nv, sld, lv);
-        };
-        if (J == 2) go(std::integral_constant<int, 2>{});
-        else go(std::integral_constant<int, 1>{});
-    });
-    if (err != cudaSuccess) return err;
-    return cudaGetLastError();
-}
-
-template <typename T>
-cudaError_t launch_rows(int mode, const Task *t, int ntask, const Blk *b, const T *src, int64_t src_ld, T *dst,
-                        int64_t dst_ld, int nv, int r, bool tma, int max_ctas, cudaStream_t s)
-{
-    return tma ? launch_rows_t<T, true>(mode, t, ntask, b, src, src_ld, dst, dst_ld, nv, r, max_ctas, s)
-               : launch_rows_t<T, false>(mode, t, ntask, b, src, src_ld, dst, dst_ld, nv, r, max_ctas, s);
-}
-
-template <typename T>
-cudaError_t launch_dense(const Task *t, int ntask, const Blk *b, const CallArgs<T> *args, const T *halo,
-                         int nv, int m, bool tma, int max_ctas, cudaStream_t s)
-{
-    return tma ? launch_dense_t<T, true>(t, ntask, b, args, halo, nv, m, max_ctas, s)
-               : launch_dense_t<T, false>(t, ntask, b, args, halo, nv, m, max_ctas, s);
-}
-
-template <typename T>
-cudaError_t launch_chain(int mode, const Task *t, const ChainDep *deps, int ntask, const Blk *b, T *buf,
-                         int64_t ld, int nv, int r, int32_t *flags, CallArgs<T> *args, int which,
-                         int max_ctas, cudaStream_t s)
-{
-    if (ntask == 0) return cudaSuccess;
-    Dispatch<T>::run(r, nv, [&](auto e) {
-        using E = decltype(e);
-        const size_t sm = (size_t)WPB * E::SCRATCH;
-        const int grid = max_ctas > 0 ? min(grid_for(ntask), max_ctas) : grid_for(ntask);
-        if (mode == MODE_WRITE)
-            k_chain<T, E, MODE_WRITE><<<grid, WPB * 32, sm, s>>>(t, deps, ntask, b, buf, ld, nv, flags, args, which);
-        else
-            k_chain<T, E, MODE_ACCUM><<<grid, WPB * 32, sm, s>>>(t, deps, ntask, b, buf, ld, nv, flags, args, which);
-    });
-    return cudaGetLastError();
-}
-
+// Heap-addressed transfer sweep launch (k_sweep).  SIMT engines stage every node's operands
+// with cp.async (one round of copies per node); DMMA engines read them straight from L2.
+// Consecutive sweep launches overlap through programmatic dependent launch.
 template <typename T>
 cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads, T *buf, int64_t ld, int nv,
                          int r, cudaStream_t s)
 {
     if (p.nlev == 0 || nctas == 0) return cudaSuccess;
-    // H2_SSTAGE: launches whose levels all have <= this many nodes use the cp.async-staged
-    // variant (default: see DESIGN.md section 5)
-    // (SIMT engines) / H2_SSTAGE_MMA (DMMA engines)
-    static const long stage_simt = getenv("H2_SSTAGE") ? atol(getenv("H2_SSTAGE")) : (long)H2_SSTAGE_DEFAULT;
-    static const long stage_mma = getenv("H2_SSTAGE_MMA") ? atol(getenv("H2_SSTAGE_MMA")) : (long)H2_SSTAGE_MMA_DEFAULT;
     int maxn = 0, rmax = 0, cmax = 0;
     for (int l = 0; l < p.nlev; ++l) {
         maxn = std::max(maxn, (int)p.lv[l].n);
@@ -2115,11 +1153,6 @@ cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads,
         cmax = std::max(cmax, (int)p.lv[l].c);
     }
     const int cc = mode == MODE_ACCUM ? cmax : 2 * cmax;
-    static const bool pdl = !(getenv("H2_PDL") && getenv("H2_PDL")[0] == '0');
-    auto launch = [&](auto kern, int grid, int block, size_t sm, int wstride) {
-        if (pdl) launch_pdl(kern, grid, block, sm, s, p, buf, ld, nv, wstride);
-        else     launch_pri(kern, grid, block, sm, s, p, buf, ld, nv, wstride);
-    };
     cudaError_t err = cudaSuccess;
     Dispatch<T>::run(r, nv, [&](auto e) {
         using E = decltype(e);
@@ -2127,41 +1160,31 @@ cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads,
         const size_t wbytes = (size_t)wstride * sizeof(T);
         int warps = threads / 32;
         while (warps > 1 && warps * wbytes > SWEEP_STAGE_SMEM) warps >>= 1;
-        const bool stage = maxn <= (E::MMA ? stage_mma : stage_simt) && warps * wbytes <= SWEEP_STAGE_SMEM;
+        const bool stage = !E::MMA && warps * wbytes <= SWEEP_STAGE_SMEM;
         if (stage) {
             const int ctas = nctas == 1 ? 1 : (int)((maxn + warps - 1) / warps);
             const size_t sm = warps * wbytes;
             auto kw = k_sweep<T, E, MODE_WRITE, true>;
             auto ka = k_sweep<T, E, MODE_ACCUM, true>;
-            static bool attr_set = false;          // once per engine, for both modes
-            if (!attr_set) {
-                err = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SWEEP_STAGE_SMEM);
-                if (err == cudaSuccess)
-                    err = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SWEEP_STAGE_SMEM);
-                attr_set = (err == cudaSuccess);
-            }
-            if (err == cudaSuccess) launch(mode == MODE_WRITE ? kw : ka, ctas, warps * 32, sm, wstride);
+            static cudaError_t attr = [&] {
+                cudaError_t e1 = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SWEEP_STAGE_SMEM);
+                return e1 == cudaSuccess
+                           ? cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SWEEP_STAGE_SMEM)
+                           : e1;
+            }();
+            if ((err = attr) != cudaSuccess) return;
+            launch_pdl(mode == MODE_WRITE ? kw : ka, ctas, warps * 32, sm, s, p, buf, ld, nv, wstride);
         } else {
             // single-level launches get a warp per (node, vector chunk); see k_sweep
-            static const bool split = !(getenv("H2_SWEEP_SPLIT") && getenv("H2_SWEEP_SPLIT")[0] == '0');
             const int nch = (nv + E::NV - 1) / E::NV;
-            const int grid = (p.nlev > 1 || !split) ? nctas : nctas * nch;
-            launch(mode == MODE_WRITE ? k_sweep<T, E, MODE_WRITE, false> : k_sweep<T, E, MODE_ACCUM, false>, grid,
-                   threads, 0, 0);
+            const int grid = p.nlev > 1 ? nctas : nctas * nch;
+            launch_pdl(mode == MODE_WRITE ? k_sweep<T, E, MODE_WRITE, false> : k_sweep<T, E, MODE_ACCUM, false>, grid,
+                       threads, 0, s, p, buf, ld, nv, 0);
         }
     });
     if (err != cudaSuccess) return err;
     return cudaGetLastError();
 }
-
-#ifdef H2_TU_COMMON
-cudaError_t launch_prefetch_l2(const PrefetchList &pl, cudaStream_t s)
-{
-    if (pl.n <= 0) return cudaSuccess;
-    k_prefetch_l2<<<pl.n, 256, 0, s>>>(pl);
-    return cudaGetLastError();
-}
-#endif
 
 template <typename T>
 cudaError_t launch_scale(T *Y, int64_t ldy, int64_t n, int nv, T beta, cudaStream_t s)
