@@ -19,7 +19,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 def build(force=False):
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-shared", "-fPIC",
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-fopenmp", "-shared", "-fPIC",
                                "-o", _LIB, _SRC])
     return _LIB
 
@@ -48,7 +48,18 @@ def _load():
                                     C.c_double, C.c_void_p, C.c_void_p]
         _lib.h2o_trees.restype = C.c_int
         _lib.h2o_trees.argtypes = [C.POINTER(_Input), C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.h2o_set_threads.restype = C.c_int
+        _lib.h2o_set_threads.argtypes = [C.c_int]
     return _lib
+
+
+def set_threads(n=0):
+    """OpenMP threads of later oracle calls (n < 1: all host cores the process may use).
+    Returns the count in effect.  The result does not depend on it (fixed per-output order)."""
+    import os
+    if n is None or n < 1:
+        n = len(os.sched_getaffinity(0))
+    return _load().h2o_set_threads(int(n))
 
 
 def _ptr(a):

@@ -8,7 +8,11 @@
  * CUDA path (paper_2109_05451_b200/) and includes none of its headers.
  *
  * It follows the paper's algorithm step by step, by direct recursion over a pointer tree it
- * builds itself from the flat input arrays, in FP64, single-threaded, fixed order:
+ * builds itself from the flat input arrays, in FP64, in a fixed per-output order.  OpenMP runs
+ * independent subtrees (tasks) and independent rows (parallel loops) concurrently; every output
+ * value is still computed by one thread in the same order as the sequential recursion, so the
+ * result is bitwise identical for any thread count (SURVEY.md §8(c) "OpenMP is allowed over
+ * independent subtrees and rows with a fixed per-output order"; pinned by a test):
  *   1. forward(s)   upsweep      PAPER.md:239-254 (sec. "Distributed Upsweep", alg:upsweep2):
  *                   leaf: xh_s = V_s^T x_s ; inner: xh_s = F_{s1}^T xh_{s1} + F_{s2}^T xh_{s2}
  *   2. couplings    PAPER.md:328-329 ("Distributed Intermediate Multiplication"):
@@ -27,6 +31,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 typedef struct {
     int64_t N;
@@ -63,6 +70,7 @@ typedef struct {
     const double *X;
     double *y;                          /* N x nv accumulator for y = A~ X */
     node **level_nodes;                 /* [q+1] arrays of 2^l nodes       */
+    int par_levels;                     /* spawn subtree tasks above this level */
 } ctx;
 
 /* ---------------------------------------------------------------- tree construction */
@@ -164,9 +172,13 @@ static void forward(ctx *c, node *s)
             }
         return;
     }
+    /* the two child subtrees are independent: recurse concurrently, then accumulate in order */
+    #pragma omp task if (s->level < c->par_levels)
+    forward(c, s->child[0]);
+    forward(c, s->child[1]);
+    #pragma omp taskwait
     for (int ci = 0; ci < 2; ci++) {            /* inner: xh_s = sum_c F_c^T xh_c */
         node *ch = s->child[ci];
-        forward(c, ch);
         int kc = ch->k;
         for (int n = 0; n < nv; n++)
             for (int b = 0; b < k; b++) {
@@ -225,8 +237,10 @@ static void backward(ctx *c, node *t)
             }
         return;
     }
+    #pragma omp task if (t->level < c->par_levels)
     backward(c, t->child[0]);
     backward(c, t->child[1]);
+    #pragma omp taskwait
 }
 
 /* ---------------------------------------------------------------- 4. dense near field */
@@ -267,20 +281,29 @@ int h2o_matvec(const h2o_input *in, int nv, double alpha, const double *X, doubl
     if (alpha != 0.0) {
         node **levels = NULL;
         node *root = build_tree(in, nv, &levels);
-        ctx c = { in, nv, X, y, levels };
+        ctx c = { in, nv, X, y, levels, q < 12 ? q : 12 };
         for (int64_t i = 0; i < nleaf; i++) {
             if (leaf_mask && !leaf_mask[i]) continue;
             for (node *t = &levels[q][i]; t; t = t->parent) t->needed = 1;
         }
+        #pragma omp parallel
+        #pragma omp single
         forward(&c, root);                                       /* 1 */
-        for (int l = 0; l <= q; l++)                             /* 2 */
-            for (int64_t i = 0; i < ((int64_t)1 << l); i++)
+        for (int l = 0; l <= q; l++) {                           /* 2 */
+            int64_t n = (int64_t)1 << l;
+            #pragma omp parallel for schedule(dynamic, 16)
+            for (int64_t i = 0; i < n; i++)
                 if (levels[l][i].needed) couple(&c, &levels[l][i]);
+        }
+        #pragma omp parallel
+        #pragma omp single
         backward(&c, root);                                      /* 3 */
+        #pragma omp parallel for schedule(dynamic, 16)
         for (int64_t i = 0; i < nleaf; i++)                      /* 4 */
             if (levels[q][i].needed) dense(&c, &levels[q][i]);
         free_tree(in, levels);
     }
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < nleaf; i++) {                        /* 5 */
         if (leaf_mask && !leaf_mask[i]) continue;
         for (int n = 0; n < nv; n++)
@@ -304,11 +327,15 @@ int h2o_trees(const h2o_input *in, int nv, const double *X, double *xh_out, doub
     if (!y) return -1;
     node **levels = NULL;
     node *root = build_tree(in, nv, &levels);
-    ctx c = { in, nv, X, y, levels };
+    ctx c = { in, nv, X, y, levels, q < 12 ? q : 12 };
+    #pragma omp parallel
+    #pragma omp single
     forward(&c, root);
-    for (int l = 0; l <= q; l++)
-        for (int64_t i = 0; i < ((int64_t)1 << l); i++) couple(&c, &levels[l][i]);
-    (void)root;
+    for (int l = 0; l <= q; l++) {
+        int64_t n = (int64_t)1 << l;
+        #pragma omp parallel for schedule(dynamic, 16)
+        for (int64_t i = 0; i < n; i++) couple(&c, &levels[l][i]);
+    }
     size_t off = 0;
     for (int l = 0; l <= q; l++)
         for (int64_t i = 0; i < ((int64_t)1 << l); i++) {
@@ -320,4 +347,17 @@ int h2o_trees(const h2o_input *in, int nv, const double *X, double *xh_out, doub
     free_tree(in, levels);
     free(y);
     return 0;
+}
+
+/* Threads used by the OpenMP regions of later calls (n < 1: the OpenMP default); returns the
+ * thread count in effect (1 when built without OpenMP). */
+int h2o_set_threads(int n)
+{
+#ifdef _OPENMP
+    if (n >= 1) omp_set_num_threads(n);
+    return omp_get_max_threads();
+#else
+    (void)n;
+    return 1;
+#endif
 }

@@ -201,3 +201,27 @@ def test_paper_accuracy_3d_order(golden):
     err = np.linalg.norm(y[0, rows] - ref) / np.linalg.norm(ref)
     v = golden["accuracy_3d"]["value"]
     assert v / 30 < err < v * 30, err
+
+
+def test_openmp_threads_bitwise_equal():
+    """The OpenMP oracle keeps a fixed per-output order: 1 thread and all host
+    threads give bitwise-identical results, in the full and in the sampled-row mode."""
+    h = small_random(3000, 16, seed=21)
+    X = make_xy(h.perm, 5, 21, -1.0, 1.0)
+    Y0 = make_xy(h.perm, 5, 22, -1.0, 1.0, stream=1)
+    mask = (np.arange(1 << h.q) % 3) == 0
+    try:
+        oracle.set_threads(1)
+        a = oracle.matvec(h, X, -0.7, 0.3, Y0)
+        am = oracle.matvec(h, X, -0.7, 0.3, Y0, leaf_mask=mask)
+        ta = oracle.trees(h, X)
+        n = oracle.set_threads(max(4, len(__import__("os").sched_getaffinity(0))))
+        assert n >= 2
+        b = oracle.matvec(h, X, -0.7, 0.3, Y0)
+        bm = oracle.matvec(h, X, -0.7, 0.3, Y0, leaf_mask=mask)
+        tb = oracle.trees(h, X)
+    finally:
+        oracle.set_threads(0)
+    assert np.array_equal(a, b) and np.array_equal(am, bm)
+    for u, v in zip(ta[0] + ta[1], tb[0] + tb[1]):
+        assert np.array_equal(u, v)
