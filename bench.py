@@ -1,14 +1,23 @@
 #!/usr/bin/env python
-"""bench.py — H² matvec throughput on B200 (driver contract).
+"""bench.py — H² matvec throughput on B200 (driver contract; DESIGN.md §"Measurement").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config suite]
 
-One STEP = one pass of the whole hot path (upsweep, coupling, downsweep, dense, epilogue) for
-every nv the workload names (cfg2: nv=1 and nv=16), on inputs already resident in HBM.
-N=1: BASELINE.json configs[1] (cfg2, 1M points, FP64).  N>1 (torchrun): weak scaling, each rank
-holds a 1M-point branch of an N x 1M-point grid; the off-diagonal x^ / x halo exchange runs
-over NCCL inside every matvec.  Timing: CUDA events on the launching stream, barrier + device
-sync on both sides, max over ranks.  Rank 0 prints one JSON line.
+A workload LEG is one BASELINE.json config in one precision with its vector counts; one STEP of a
+leg is one pass of the whole hot path (upsweep, coupling, downsweep, dense near field, epilogue)
+for every nv of the leg, on inputs already resident in HBM.
+
+--config suite (default) times
+  * the PRIMARY leg cfg2 (BASELINE configs[1]: 2D exp kernel, 1M points per GPU, nv = 1 and 16,
+    FP64; weak scaling at N > 1): `value`, `ms_per_step`, `per_nv`, `roofline`, `e2e`;
+  * cfg3 (configs[2]: 3D Gaussian, 2M points, k = 64, nv = 64, FP64; STRONG scaling: the same 2M
+    points split over the N GPUs) and cfg1 (configs[0]: N = 4096, latency, warm / cold L2) as
+    extra legs under `per_config`, each with its own roofline, e2e and CPU baseline.
+--config cfg2|cfg3|cfg3s|cfg4|cfg5|cfg1: that workload alone as the primary leg (cfg5 = FP64 and
+    FP32 legs).
+Timing: CUDA events on the launching stream, barrier + device sync on both sides, max over ranks;
+the timed loop runs the product path (one CUDA graph per call, concurrent side stream); per-phase
+times come from a separate profiled pass afterwards.  Rank 0 prints one JSON line.
 """
 import argparse
 import json
@@ -25,46 +34,33 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "H2 matvec GFLOP/s per GPU and ms/matvec (nv=1,16,64) at 1/2/4/8 B200"
-WORKLOADS = {
-    "cfg2": dict(desc="2D exp-covariance kernel, N=1M points, leaf 64, rank 25, nv=1 and nv=16, FP64",
-                 base=(1024, 1024), m=64, p=5, eta=0.9, kernel=("exp", 0.1), nvs=(1, 16), dtype="f64"),
-    "cfg1": dict(desc="2D exp-covariance kernel, N=4096 uniform points, leaf 32, Chebyshev rank 16, nv=1, FP64",
-                 base=None, m=32, p=4, eta=0.9, kernel=("exp", 0.1), nvs=(1,), dtype="f64"),
-    # cfg3's structure (3D Gaussian, leaf 64, k = 4^3 = 64, eta = 1.1, nv = 64; reading R5/R9) on a
-    # 64^3 grid: the compute-bound regime on one GPU without the 37 GB operator of the 128^3 case
-    "cfg3s": dict(desc="3D Gaussian kernel (cfg3 structure), N=64^3=262144 grid points, leaf 64, rank 64, "
-                       "eta 1.1, nv=64, FP64",
-                  base=(64, 64, 64), m=64, p=4, eta=1.1, kernel=("gaussian", 0.2), nvs=(64,), dtype="f64"),
+SUITES = {
+    "suite": (["cfg2"], ["cfg3", "cfg1"]),
+    "cfg1": (["cfg1"], []), "cfg2": (["cfg2"], []), "cfg3": (["cfg3"], []), "cfg3s": (["cfg3s"], []),
+    "cfg4": (["cfg4"], []), "cfg5": (["cfg5"], []),
 }
+CPU_BUDGET_S = 12.0          # oracle seconds per leg for the cpu_baseline sample
 
 
-def grid_for(base, P):
-    """Weak-scaling grid: P x base points, doubling the shorter side (longest side = 1)."""
-    dims = list(base)
-    n = P
-    while n > 1:
-        i = int(np.argmin(dims))
-        dims[i] *= 2
-        n //= 2
-    return tuple(dims)
-
-
-def fp64_peak():
-    """Measured FP64 DMMA ceiling: cuBLAS DGEMM 8192^3 on this pool's B200 (profiles/peaks_b200_r01.json)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "peaks_b200_r01.json")) as f:
-            return float(json.load(f)["gemm_float64_tflops"]), "measured cuBLAS DGEMM (profiles/peaks_b200_r01.json)"
-    except Exception:
-        return 40.0, "nominal B200 FP64 tensor 40 TFLOP/s"
-
-
-def peaks():
+# ------------------------------------------------------------------------------------------ helpers
+def fp_peaks():
+    """Measured peaks: HBM copy bandwidth (MEASURED_PEAKS.json), FP64 / FP32 GEMM rates (cuBLAS
+    DGEMM / SGEMM 8192^3 measured on this pool's B200, profiles/peaks_b200_r01.json)."""
+    out = {"hbm": (6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"), "f64": (40.0, "nominal FP64 40 TFLOP/s"),
+           "f32": (80.0, "nominal FP32 80 TFLOP/s")}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            pk = json.load(f)
-        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+            out["hbm"] = (float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)")
     except Exception:
-        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+        pass
+    try:
+        with open(os.path.join(ROOT, "profiles", "peaks_b200_r01.json")) as f:
+            pk = json.load(f)
+        out["f64"] = (float(pk["gemm_float64_tflops"]), "measured cuBLAS DGEMM 8192^3 (profiles/peaks_b200_r01.json)")
+        out["f32"] = (float(pk["gemm_float32_tflops"]), "measured cuBLAS SGEMM 8192^3 (profiles/peaks_b200_r01.json)")
+    except Exception:
+        pass
+    return out
 
 
 class ClockSampler:
@@ -77,6 +73,7 @@ class ClockSampler:
     def __init__(self, gpu_index):
         self.idx = gpu_index
         self.proc = None
+        self.lines = []
 
     def __enter__(self):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
@@ -93,95 +90,360 @@ class ClockSampler:
         if self.proc:
             self.proc.terminate()
             self.proc.wait()
-
-    def summary(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.f.seek(0)
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.f.read().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                smax = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
+            self.f.seek(0)
+            self.lines = self.f.read().splitlines()
+        self.f.close()
         os.unlink(self.f.name)
-        busy = [s for s in sm if smax and s > 0.5 * smax] or sm
-        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def clock_summary(samplers):
+    lines = [ln for s in samplers for ln in s.lines]
+    if not any(s.proc for s in samplers):
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+    sm, smax, reasons = [], None, set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in lines:
+        parts = [x.strip() for x in line.split(",")]
+        if len(parts) < 8:
+            continue
+        try:
+            sm.append(float(parts[1]))
+            smax = float(parts[2])
+        except ValueError:
+            continue
+        for nm, v in zip(names, parts[4:8]):
+            if v.lower() == "active":
+                reasons.add(nm)
+    busy = [s for s in sm if smax and s > 0.5 * smax] or sm
+    return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": smax,
+            "reasons": sorted(reasons), "samples": len(sm)}
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rk = int(os.environ.get("RANK", "0"))
-    lr = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rk, lr
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def build_problem(wl, P, rank, with_global):
-    from h2gen import build_cluster_tree, dual_traversal, SEED
-    from h2gen.kernels import Kernel
-    from h2gen.tree import grid_points, uniform_points
-    from h2gen.shard import build_h2_shard
+def legs_of(name):
+    """[(config, dtype, nvs)] of one workload (cfg5: one leg per precision)."""
+    from h2gen.configs import CONFIGS
+    c = CONFIGS[name]
+    return [(name, dt, tuple(c["nvs"])) for dt in c["dtypes"]]
+
+
+def leg_key(leg):
+    name, dt, nvs = leg
+    return f"{name}/{dt}/nv={'+'.join(map(str, nvs))}"
+
+
+def config_dict(args, P, legs_primary, legs_extra, N_global, n_local):
+    from h2gen.configs import CONFIGS
+    prim = legs_primary[0][0]
+    scal = CONFIGS[prim]["scaling"]
+    return {"workload": "; ".join(f"{leg_key(lg)}: {CONFIGS[lg[0]]['desc']}" for lg in legs_primary),
+            "extra_legs": [leg_key(lg) for lg in legs_extra],
+            "N_global": N_global, "N_per_gpu": n_local,
+            "parallelism": f"block rows x{P} ({scal} scaling)" if P > 1 else "single GPU",
+            "l2": "inputs larger than L2 (operators of 5-40 GB streamed per matvec; L2 126 MB); cfg1 (L2-resident) "
+                  "reported warm and cold (256 MB scrub between reps)",
+            "timing": "CUDA events on the launching stream, barrier+sync both sides, max over ranks; product path "
+                      "(CUDA graph); phase split from a separate profiled pass"}
+
+
+# ---------------------------------------------------------------------------------- problem setup
+def build_leg_problem(name, P, rank, with_global):
+    """(tree, host operator kwargs for this rank, (r0, r1), global H2Data or None)."""
+    from h2gen.configs import build_structure
     from h2gen.h2data import build_h2
-    if wl["base"] is None:
-        pts = uniform_points(4096, 2, SEED)
-    else:
-        pts = grid_points(grid_for(wl["base"], P))
-    tree = build_cluster_tree(pts, wl["m"])
-    st = dual_traversal(tree, wl["eta"])
-    kern = Kernel(wl["kernel"][0], ell=wl["kernel"][1])
-    if with_global:
-        h = build_h2(tree, st, kern, wl["p"])
+    from h2gen.shard import build_h2_shard
+    tree, st, kern, c = build_structure(name, P)
+    if with_global or P == 1:
         from paper_2109_05451_b200.operator import shard_arrays
+        h = build_h2(tree, st, kern, c["p"])
         kw, rows = shard_arrays(h, rank, P)
-        return tree, st, h, kw, rows
-    kw, rows = build_h2_shard(tree, st, kern, wl["p"], rank, P)
-    return tree, st, None, kw, rows
+        return tree, kw, rows, h, c
+    kw, rows = build_h2_shard(tree, st, kern, c["p"], rank, P)
+    return tree, kw, rows, None, c
 
 
-def run_reference(args, wl, emit):
-    """--impl reference: the CPU oracle (oracle/, plain C FP64, single thread) on the same
-    workload, one full step (every nv) per timed step; rank 0 only."""
+def cast_kw(kw, dtype):
+    if dtype == "f64":
+        return kw
+    kw = dict(kw)
+    f = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float32)
+    for key in ("U_leaf", "V_leaf", "D"):
+        kw[key] = f(kw[key])
+    for key in ("E", "F", "S"):
+        kw[key] = [f(a) for a in kw[key]]
+    return kw
+
+
+# ------------------------------------------------------------------------------ CPU oracle leg
+def oracle_work(h, mask):
+    """Scalar multiply-adds per vector the oracle performs with leaf mask `mask` (None = all):
+    full upsweep, couplings / downsweep on the ancestors of the masked leaves, their dense rows.
+    Used only to scale a sampled oracle time to the whole workload."""
+    q = h.q
+    rows = np.diff(np.asarray(h.leaf_ptr))
+    need = [None] * (q + 1)
+    need[q] = np.ones(1 << q, dtype=bool) if mask is None else np.asarray(mask, dtype=bool)
+    for l in range(q - 1, -1, -1):
+        need[l] = need[l + 1][0::2] | need[l + 1][1::2]
+    k = h.ranks
+    w = float(rows.sum()) * k[q] + sum(float(1 << l) * k[l] * k[l - 1] for l in range(1, q + 1))
+    for l in range(q + 1):
+        nb = np.diff(np.asarray(h.S_rowptr[l]))
+        w += float(nb[need[l]].sum()) * k[l] * k[l]
+        if l >= 1:
+            w += float(need[l].sum()) * k[l] * k[l - 1]
+    w += float(rows[need[q]].sum()) * k[q]
+    drp = np.asarray(h.D_rowptr)
+    trow = np.repeat(np.arange(1 << q), np.diff(drp))
+    sel = need[q][trow]
+    w += float((rows[trow[sel]] * rows[np.asarray(h.D_col)[sel]]).sum())
+    return w
+
+
+def oracle_mask(h, nvs, budget_s, cores):
+    """Leaf sample sized for ~budget_s of oracle time (assumed ~2.5 GFLOP/s per core; the rate only
+    sizes the sample, the reported value is measured)."""
+    full = oracle_work(h, None) * 2.0 * sum(nvs)
+    frac = min(1.0, budget_s * 2.5e9 * cores / max(full, 1.0))
+    if frac >= 1.0:
+        return None, 1.0
+    rng = np.random.default_rng(12345)
+    mask = rng.random(1 << h.q) < max(frac, 1.0 / (1 << h.q))
+    return mask, oracle_work(h, mask) / oracle_work(h, None)
+
+
+def time_oracle(h, Xs, nvs, mask, flops_model, frac):
+    import oracle
+    prep = oracle.prepare(h)
+    t0 = time.perf_counter()
+    for nv in nvs:
+        oracle.matvec(h, Xs[nv], 1.0, 0.0, None, leaf_mask=mask, prepared=prep)
+    sec = time.perf_counter() - t0
+    return sec, flops_model * frac / sec / 1e9
+
+
+def run_reference(args, emit):
+    """--impl reference: the CPU oracle (oracle/, plain C FP64 + OpenMP over the host cores) on the
+    primary legs of the same workload, rank 0 only; each step = every matvec of the legs on a
+    bounded leaf sample sized so the whole --steps/--warmup run stays within a few minutes."""
     ws, rk, _ = dist_env()
     if rk != 0:
         return
     import oracle
     from h2gen import make_xy, SEED
-    _, _, h, _, _ = build_problem(wl, 1, 0, True)
-    prep = oracle.prepare(h)
-    Xs = {nv: make_xy(h.perm, nv, SEED) for nv in wl["nvs"]}
-    flops = sum(h.flops(nv) for nv in wl["nvs"])
+    cores = oracle.set_threads(0)
+    prim, extra = SUITES[args.config]
+    legs = [lg for nm in prim for lg in legs_of(nm)]
+    parts, flops_step, sample = [], 0.0, []
+    for name, dt, nvs in legs:
+        _, _, _, h, c = build_leg_problem(name, ws, 0, True)
+        hh = h if dt == "f64" else h.astype(np.float32).astype(np.float64)
+        Xs = {nv: make_xy(h.perm, nv, SEED) for nv in nvs}
+        fl = sum(h.flops(nv) for nv in nvs)
+        budget = 150.0 / (args.steps + args.warmup) / len(legs)
+        mask, frac = oracle_mask(h, nvs, budget, cores)
+        parts.append((hh, Xs, nvs, mask, fl, frac))
+        flops_step += fl
+        sample.append(f"{leg_key((name, dt, nvs))}: {frac * 100:.1f}% of the oracle work (leaf sample, full upsweep)")
 
     def step():
-        for nv in wl["nvs"]:
-            oracle.matvec(h, Xs[nv], 1.0, 0.0, None, prepared=prep)
+        return sum(time_oracle(hh, Xs, nvs, mask, fl, frac)[0] / frac for hh, Xs, nvs, mask, fl, frac in parts)
     for _ in range(args.warmup):
         step()
-    t = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        step()
-        t.append(time.perf_counter() - t0)
+    t = [step() for _ in range(args.steps)]          # each step's time scaled to the full step
     sec = sum(t) / len(t)
-    val = flops / sec / 1e9
+    val = flops_step / sec / 1e9
+    from h2gen.configs import CONFIGS
+    P = ws
+    n_first = int(parts[0][0].N) if CONFIGS[legs[0][0]]["scaling"] == "weak" else int(parts[0][0].N)
+    # per-GPU rows of rank 0 = its branch at the C-level (the same rows the GPU arm reports)
+    C = P.bit_length() - 1
+    lp = np.asarray(parts[0][0].leaf_ptr)
+    n_rank0 = int(lp[1 << (parts[0][0].q - C)]) if P > 1 else n_first
+    ours_cfg = config_dict(args, ws, legs, [lg for nm in extra for lg in legs_of(nm)], n_first, n_rank0)
     out = {"metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": wl["dtype"], "data": "synthetic",
-           "config": {"workload": f"{args.config}: {wl['desc']}", "N": int(h.N), "nvs": list(wl["nvs"])},
-           "impl": "reference",
-           "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
-                            "sample": f"one full step ({'+'.join('nv=%d' % v for v in wl['nvs'])} matvecs) "
-                                      f"of {args.config} at full size per timed step, single-threaded C oracle"},
+           "scaling": CONFIGS[legs[0][0]]["scaling"], "vs_baseline": None, "dtype": legs[0][1], "data": "synthetic",
+           "config": ours_cfg, "impl": "reference",
+           "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                            "sample": "; ".join(sample) + "; time scaled by the work fraction"},
            "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(out)
+
+
+# ------------------------------------------------------------------------------------ GPU legs
+def run_leg(leg, args, P, rank, dev, pkg, torch, dist, want_cpu, samplers, latency=False):
+    from h2gen import make_xy, SEED
+    name, dtype, nvs = leg
+    t_gen = time.perf_counter()
+    tree, kw, (r0, r1), hglob, cfg = build_leg_problem(name, P, rank, want_cpu)
+    t_gen = time.perf_counter() - t_gen
+    nccl_id = None
+    if P > 1:
+        from paper_2109_05451_b200.operator import broadcast_nccl_id
+        nccl_id = broadcast_nccl_id(dev)
+    op = pkg.H2Operator(dtype=dtype, nv_max=max(nvs), nccl_id=nccl_id, **cast_kw(kw, dtype))
+    del kw
+    n_local = int(op.n_local)
+    perm_local = tree.perm[r0:r1]
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    esz = 8 if dtype == "f64" else 4
+    X = {nv: torch.from_numpy(make_xy(perm_local, nv, SEED)).to(dev, tdt) for nv in nvs}
+    Y = {nv: torch.zeros(nv, n_local, dtype=tdt, device=dev) for nv in nvs}
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if P > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        for nv in nvs:
+            op.matvec(X[nv], Y[nv], 1.0, 0.0, stream)
+    barrier()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in nvs]
+          for _ in range(args.steps)]
+    scrub = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if latency else None
+    cold = []
+    gidx = torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else dev.index
+    sampler = ClockSampler(gidx) if not args.profile_only else None
+    with (sampler if sampler else _Null()):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(args.steps):
+            for i, nv in enumerate(nvs):
+                ev[s][i][0].record(stream)
+                op.matvec(X[nv], Y[nv], 1.0, 0.0, stream)
+                ev[s][i][1].record(stream)
+        e1.record(stream)
+        barrier()
+        if latency:                         # cold L2: a 256 MB scrub before every call
+            for s in range(args.steps):
+                for i, nv in enumerate(nvs):
+                    scrub.add_(1)
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    op.matvec(X[nv], Y[nv], 1.0, 0.0, stream)
+                    b.record(stream)
+                    cold.append((a, b))
+            barrier()
+    if sampler:
+        samplers.append(sampler)
+    per_nv_ms = [sum(ev[s][i][0].elapsed_time(ev[s][i][1]) for s in range(args.steps)) for i in range(len(nvs))]
+    t = torch.tensor([e0.elapsed_time(e1)] + per_nv_ms, dtype=torch.float64, device=dev)
+    if P > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t[0]) / args.steps
+    per_nv_ms = {nv: float(t[i + 1]) / args.steps for i, nv in enumerate(nvs)}
+    fl = torch.tensor([op.stats(nv)["flops"] for nv in nvs], dtype=torch.float64, device=dev)
+    if P > 1:
+        dist.all_reduce(fl)
+    flops = {nv: float(fl[i]) for i, nv in enumerate(nvs)}
+    flops_step = sum(flops.values())
+    launches = op.stats(1)["launches"]
+    # per-phase times: a separate profiled pass (side stream serialised; events between phases)
+    per_nv_ph = {}
+    for nv in nvs:
+        op.set_profiling(True)
+        op.phase_times()
+        for _ in range(3):
+            op.matvec(X[nv], Y[nv], 1.0, 0.0, stream)
+        per_nv_ph[nv], _ = op.phase_times()
+        op.set_profiling(False)
+    # e2e through the public API with pinned host buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e and not args.profile_only:
+        Xh = {nv: torch.from_numpy(make_xy(perm_local, nv, SEED)).to(tdt).pin_memory() for nv in nvs}
+        Yh = {nv: torch.zeros(nv, n_local, dtype=tdt).pin_memory() for nv in nvs}
+        for nv in nvs:
+            op.matvec_host(Xh[nv], Yh[nv], 1.0, 0.0, stream)
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            for nv in nvs:
+                op.matvec_host(Xh[nv], Yh[nv], 1.0, 0.0, stream)
+        b.record(stream)
+        barrier()
+        te = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        if P > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = float(te[0]) / args.steps
+        e2e = {"value": flops_step / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": sum(n_local * nv * esz for nv in nvs),
+               "d2h_bytes_per_step": sum(n_local * nv * esz for nv in nvs)}
+        del Xh, Yh
+    # roofline of the leg's dominant kernel (largest summed phase time)
+    pk = fp_peaks()
+    kof = pkg._binding.KERNEL_OF_PHASE
+    step_ph = {k: sum(per_nv_ph[nv].get(k, 0.0) for nv in nvs) for k in pkg.PHASES}
+    groups = {}
+    for k in pkg.PHASES:
+        groups.setdefault(kof.get(k, k), []).append(k)
+    dom_k = max(groups, key=lambda g: sum(step_ph[k] for k in groups[g]))
+    dom_phases = groups[dom_k]
+    bytes_dom = sum(op.phase_stats(nv)[0][k] for nv in nvs for k in dom_phases)
+    flops_dom = sum(op.phase_stats(nv)[1][k] for nv in nvs for k in dom_phases)
+    ms_dom = sum(step_ph[k] for k in dom_phases)
+    hbm, hbm_src = pk["hbm"]
+    fpk, fpk_src = pk[dtype]
+    gbs = bytes_dom / (ms_dom * 1e-3) / 1e9
+    if flops_dom / (fpk * 1e12) > bytes_dom / (hbm * 1e9):
+        tf = flops_dom / (ms_dom * 1e-3) / 1e12
+        roof = {"bound": "tensor" if dtype == "f64" else "alu", "achieved": tf, "peak": fpk, "unit": "TFLOP/s",
+                "frac": tf / fpk, "peak_source": fpk_src, "algorithmic_flops_per_step": flops_dom,
+                "hbm_frac": gbs / hbm}
+    else:
+        roof = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                "peak_source": hbm_src}
+    roof.update({"kernel": dom_k, "phase": "+".join(dom_phases), "algorithmic_bytes_per_step": bytes_dom,
+                 "ms_per_step": ms_dom, "traffic": ncu_traffic(leg_key(leg), "+".join(dom_phases))})
+    out = {"leg": leg_key(leg), "desc": cfg["desc"], "dtype": dtype, "N_global": int(tree.N), "N_per_gpu": n_local,
+           "scaling": cfg["scaling"], "ms_per_step": ms_step, "gflops": flops_step / (ms_step * 1e-3) / 1e9,
+           "gflops_per_gpu": flops_step / (ms_step * 1e-3) / 1e9 / P, "flops_step": flops_step,
+           "per_nv": {str(nv): {"ms_per_matvec": per_nv_ms[nv],
+                                "gflops": flops[nv] / (per_nv_ms[nv] * 1e-3) / 1e9,
+                                "gflops_per_gpu": flops[nv] / (per_nv_ms[nv] * 1e-3) / 1e9 / P,
+                                "path_frac_of_hbm": op.stats(nv)["bytes"] / (per_nv_ms[nv] * 1e-3) / 1e9 / hbm,
+                                "phases_ms": {k: round(v, 5) for k, v in per_nv_ph[nv].items()}} for nv in nvs},
+           "roofline": roof, "e2e": e2e, "launches_per_matvec": launches,
+           "gpu_launches": launches * len(nvs) * args.steps, "gen_seconds": round(t_gen, 1)}
+    if latency:
+        cold_us = sorted(a.elapsed_time(b) * 1e3 for a, b in cold)
+        warm_us = sorted(ev[s][i][0].elapsed_time(ev[s][i][1]) * 1e3 for s in range(args.steps) for i in range(len(nvs)))
+        out["latency_us"] = {"warm_median": warm_us[len(warm_us) // 2], "warm_min": warm_us[0],
+                             "cold_median": cold_us[len(cold_us) // 2], "cold_min": cold_us[0],
+                             "launches_per_matvec": launches}
+    # CPU oracle beside it (rank 0, N = 1): bounded leaf sample on all host cores
+    if want_cpu and hglob is not None:
+        import oracle
+        cores = oracle.set_threads(0)
+        hh = hglob if dtype == "f64" else hglob.astype(np.float32).astype(np.float64)
+        Xc = {nv: X[nv].double().cpu().numpy() for nv in nvs}
+        mask, frac = oracle_mask(hglob, nvs, CPU_BUDGET_S, cores)
+        sec, val = time_oracle(hh, Xc, nvs, mask, flops_step, frac)
+        out["cpu_baseline"] = {"value": val, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                               "sample": f"{leg_key(leg)}: {frac * 100:.1f}% of the oracle work per step (random "
+                                         f"leaf sample, full upsweep), {sec:.1f} s, OpenMP on {cores} host threads; "
+                                         "scaled by the work fraction"}
+    op.close()
+    del X, Y, op, hglob
+    torch.cuda.empty_cache()
+    return out
+
+
+def ncu_traffic(key, phases):
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        return tr.get(key, {}).get(phases)
+    except Exception:
+        return None
 
 
 def main():
@@ -195,20 +457,19 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="suite", choices=sorted(SUITES))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="primary legs only")
     ap.add_argument("--profile-only", action="store_true", help="no clocks / e2e / cpu (for ncu runs)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
-    wl = WORKLOADS[args.config]
     if args.impl == "reference":
-        return run_reference(args, wl, emit)
+        return run_reference(args, emit)
 
     import torch
     import torch.distributed as dist
     import paper_2109_05451_b200 as pkg
-    from h2gen import make_xy, SEED
     pkg.load_library()
     ws, rk, lr = dist_env()
     P = ws
@@ -216,181 +477,48 @@ def main():
     dev = torch.device("cuda", lr)
     if P > 1:
         dist.init_process_group("nccl", device_id=dev)
-    t_gen = time.perf_counter()
+    prim, extra = SUITES[args.config]
+    if args.no_extra or args.profile_only:
+        extra = []
+    legs_p = [lg for nm in prim for lg in legs_of(nm)]
+    legs_x = [lg for nm in extra for lg in legs_of(nm)]
     want_cpu = (P == 1 and rk == 0 and not args.no_cpu_baseline and not args.profile_only)
-    tree, st, hglob, kw, (r0, r1) = build_problem(wl, P, rk, with_global=want_cpu)
-    t_gen = time.perf_counter() - t_gen
-    nccl_id = None
-    if P > 1:
-        from paper_2109_05451_b200.operator import broadcast_nccl_id
-        nccl_id = broadcast_nccl_id(dev)
-    nv_max = max(wl["nvs"])
-    op = pkg.H2Operator(dtype=wl["dtype"], nv_max=nv_max, nccl_id=nccl_id, **kw)
-    n_local = int(kw["n_local"])
-    perm_local = tree.perm[r0:r1]
-    tdt = torch.float64 if wl["dtype"] == "f64" else torch.float32
-    X = {nv: torch.from_numpy(make_xy(perm_local, nv, SEED)).to(dev, tdt) for nv in wl["nvs"]}
-    Y = {nv: torch.zeros(nv, n_local, dtype=tdt, device=dev) for nv in wl["nvs"]}
-    stream = torch.cuda.current_stream(dev)
-
-    def barrier():
-        if P > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-
-    def step():
-        for nv in wl["nvs"]:
-            op.matvec(X[nv], Y[nv], 1.0, 0.0, stream)
-
-    for _ in range(args.warmup):
-        step()
-    barrier()
-    # ---- timed region (device time, CUDA events on the launching stream)
-    op.set_profiling(True)
-    op.phase_times()                       # reset
-    clocks = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else lr)
-    per_nv_ms = {nv: 0.0 for nv in wl["nvs"]}
-    per_nv_ph = {nv: {} for nv in wl["nvs"]}
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in wl["nvs"]] for _ in range(args.steps)]
-    with (clocks if not args.profile_only else _Null()):
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for s in range(args.steps):
-            for i, nv in enumerate(wl["nvs"]):
-                ev[s][i][0].record(stream)
-                op.matvec(X[nv], Y[nv], 1.0, 0.0, stream)
-                ev[s][i][1].record(stream)
-        e1.record(stream)
-        barrier()
-    total_ms = e0.elapsed_time(e1)
-    for s in range(args.steps):
-        for i, nv in enumerate(wl["nvs"]):
-            per_nv_ms[nv] += ev[s][i][0].elapsed_time(ev[s][i][1])
-    phases, ncalls = op.phase_times()
-    op.set_profiling(False)
-    # per-nv phase times: one extra profiled pass per nv (same kernels; side streams serialized
-    # so each phase's CUDA events bracket only its own launches)
-    for nv in wl["nvs"]:
-        op.set_profiling(True)
-        for _ in range(3):
-            op.matvec(X[nv], Y[nv], 1.0, 0.0, stream)
-        per_nv_ph[nv], _ = op.phase_times()
-        op.set_profiling(False)
-    # max over ranks
-    t = torch.tensor([total_ms] + [per_nv_ms[nv] for nv in wl["nvs"]], dtype=torch.float64, device=dev)
-    if P > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t[0])
-    for i, nv in enumerate(wl["nvs"]):
-        per_nv_ms[nv] = float(t[i + 1]) / args.steps
-    ms_step = total_ms / args.steps
-    flops_rank = {nv: op.stats(nv)["flops"] for nv in wl["nvs"]}
-    ft = torch.tensor([sum(flops_rank.values())] + [flops_rank[nv] for nv in wl["nvs"]], dtype=torch.float64, device=dev)
-    if P > 1:
-        dist.all_reduce(ft)
-    flops_step = float(ft[0])
-    value = flops_step / (ms_step * 1e-3) / 1e9
-    launches = op.stats(1)["launches"]
-    # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
-    e2e = None
-    if not args.no_e2e and not args.profile_only:
-        Xh = {nv: torch.from_numpy(make_xy(perm_local, nv, SEED)).to(tdt).pin_memory() for nv in wl["nvs"]}
-        Yh = {nv: torch.zeros(nv, n_local, dtype=tdt).pin_memory() for nv in wl["nvs"]}
-        for nv in wl["nvs"]:
-            op.matvec_host(Xh[nv], Yh[nv], 1.0, 0.0, stream)
-        barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(args.steps):
-            for nv in wl["nvs"]:
-                op.matvec_host(Xh[nv], Yh[nv], 1.0, 0.0, stream)
-        b.record(stream)
-        barrier()
-        te = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-        if P > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e_ms = float(te[0]) / args.steps
-        esz = 8 if wl["dtype"] == "f64" else 4
-        e2e = {"value": flops_step / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": sum(n_local * nv * esz for nv in wl["nvs"]),
-               "d2h_bytes_per_step": sum(n_local * nv * esz for nv in wl["nvs"])}
-    # ---- roofline of the dominant kernel (largest phase time over the step)
-    hbm, hbm_src = peaks()
-    step_ph = {k: sum(per_nv_ph[nv].get(k, 0.0) for nv in wl["nvs"]) for k in pkg.PHASES}
-    # phases launched by the same kernel (the coupling rows of the tree levels and of the leaf
-    # level are two k_rows<WRITE> launches) are one kernel for the roofline
-    kof = pkg._binding.KERNEL_OF_PHASE
-    groups = {}
-    for k in pkg.PHASES:
-        groups.setdefault(kof.get(k, k), []).append(k)
-    dom_k = max(groups, key=lambda g: sum(step_ph[k] for k in groups[g]))
-    dom_phases = groups[dom_k]
-    dom = "+".join(dom_phases)
-    bytes_dom = sum(op.phase_stats(nv)[0][k] for nv in wl["nvs"] for k in dom_phases)
-    ms_dom = sum(step_ph[k] for k in dom_phases)
-    achieved = bytes_dom / (ms_dom * 1e-3) / 1e9
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f)
-        if tr.get("config") == args.config and dom in tr.get("phases", {}):
-            traffic = tr["phases"][dom]
-    except Exception:
-        pass
-    roofline = {"bound": "hbm", "kernel": dom_k,
-                "phase": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "peak_source": hbm_src,
-                "algorithmic_bytes_per_step": bytes_dom, "ms_per_step": ms_dom}
-    # FP64 phases whose flops outlast their bytes at the measured peaks (nv = 64) are bounded by the
-    # FP64 tensor pipe: report them against the measured cuBLAS DGEMM rate instead
-    flops_dom = sum(op.phase_stats(nv)[1][k] for nv in wl["nvs"] for k in dom_phases)
-    f64_tf, f64_src = fp64_peak()
-    if wl["dtype"] == "f64" and flops_dom / (f64_tf * 1e12) > bytes_dom / (hbm * 1e9):
-        ach_tf = flops_dom / (ms_dom * 1e-3) / 1e12
-        roofline.update({"bound": "tensor", "achieved": ach_tf, "peak": f64_tf, "unit": "TFLOP/s",
-                         "frac": ach_tf / f64_tf, "peak_source": f64_src,
-                         "algorithmic_flops_per_step": flops_dom, "hbm_frac": achieved / hbm})
-    # ---- CPU oracle beside it (rank 0, N=1 only): one full step, single thread
-    cpu = None
-    if want_cpu:
-        import oracle
-        prep = oracle.prepare(hglob)
-        Xc = {nv: X[nv].double().cpu().numpy() for nv in wl["nvs"]}
-        t0 = time.perf_counter()
-        for nv in wl["nvs"]:
-            oracle.matvec(hglob, Xc[nv], 1.0, 0.0, None, prepared=prep)
-        sec = time.perf_counter() - t0
-        cpu = {"value": flops_step / sec / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
-               "sample": f"one full step ({'+'.join('nv=%d' % v for v in wl['nvs'])} matvecs) of "
-                         f"{args.config} at full size, single-threaded C oracle, {sec:.1f} s"}
+    samplers = []
+    res_p = [run_leg(lg, args, P, rk, dev, pkg, torch, dist, want_cpu, samplers, latency=(lg[0] == "cfg1"))
+             for lg in legs_p]
+    res_x = [run_leg(lg, args, P, rk, dev, pkg, torch, dist, want_cpu, samplers, latency=(lg[0] == "cfg1"))
+             for lg in legs_x]
     if rk == 0:
-        cfg = {"workload": f"{args.config}: {wl['desc']}", "N_global": int(tree.N), "N_per_gpu": n_local,
-               "nvs": list(wl["nvs"]), "parallelism": f"block-rows x{P}" if P > 1 else "single GPU",
-               "l2": "inputs larger than L2 (operator %.2f GB streamed per matvec; L2 126 MB)"
-                     % (op.stats(1)["bytes"] / 1e9),
-               "timing": "CUDA events on the launching stream, barrier+sync both sides, max over ranks",
-               "gen_seconds": round(t_gen, 1)}
+        ms_step = sum(r["ms_per_step"] for r in res_p)
+        flops_step = sum(r["flops_step"] for r in res_p)
+        value = flops_step / (ms_step * 1e-3) / 1e9
+        dom = max(res_p, key=lambda r: r["roofline"]["ms_per_step"])
+        per_nv = {}
+        for r in res_p:
+            for nv, d in r["per_nv"].items():
+                per_nv[nv if len(res_p) == 1 else f"{r['leg']}"] = d
+        e2e = None
+        if all(r["e2e"] for r in res_p):
+            e_ms = sum(r["e2e"]["ms_per_step"] for r in res_p)
+            e2e = {"value": flops_step / (e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e_ms,
+                   "h2d_bytes_per_step": sum(r["e2e"]["h2d_bytes_per_step"] for r in res_p),
+                   "d2h_bytes_per_step": sum(r["e2e"]["d2h_bytes_per_step"] for r in res_p)}
+        cpu = None
+        if all("cpu_baseline" in r for r in res_p):
+            cpu_s = sum(r["flops_step"] / (r["cpu_baseline"]["value"] * 1e9) for r in res_p)
+            cpu = {"value": flops_step / cpu_s / 1e9, "unit": "GFLOP/s", "cores": res_p[0]["cpu_baseline"]["cores"],
+                   "kind": "oracle", "sample": "; ".join(r["cpu_baseline"]["sample"] for r in res_p)}
+        from h2gen.configs import CONFIGS
         out = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": P, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": wl["dtype"], "data": "synthetic",
-               "config": cfg,
-               "per_nv": {str(nv): {"ms_per_matvec": per_nv_ms[nv],
-                                    "gflops": float(ft[i + 1]) / (per_nv_ms[nv] * 1e-3) / 1e9,
-                                    "gflops_per_gpu": float(ft[i + 1]) / (per_nv_ms[nv] * 1e-3) / 1e9 / P,
-                                    "phases_ms": {k: round(v, 5) for k, v in per_nv_ph[nv].items()}}
-                          for i, nv in enumerate(wl["nvs"])},
-               "roofline": roofline,
-               "path_bandwidth": {str(nv): {"algorithmic_bytes": op.stats(nv)["bytes"],
-                                            "GB_s": op.stats(nv)["bytes"] / (per_nv_ms[nv] * 1e-3) / 1e9,
-                                            "frac_of_hbm": op.stats(nv)["bytes"] / (per_nv_ms[nv] * 1e-3) / 1e9 / hbm}
-                                  for nv in wl["nvs"]},
-               "cpu_baseline": cpu, "e2e": e2e,
-               "gpu_launches": launches * len(wl["nvs"]) * args.steps,
-               "clocks": clocks.summary() if not args.profile_only else None}
+               "scaling": CONFIGS[legs_p[0][0]]["scaling"], "vs_baseline": None, "dtype": legs_p[0][1],
+               "data": "synthetic",
+               "config": config_dict(args, P, legs_p, legs_x, res_p[0]["N_global"], res_p[0]["N_per_gpu"]),
+               "per_nv": per_nv, "roofline": dom["roofline"], "e2e": e2e, "cpu_baseline": cpu,
+               "gpu_launches": sum(r["gpu_launches"] for r in res_p),
+               "clocks": clock_summary(samplers) if not args.profile_only else None,
+               "per_config": {r["leg"]: r for r in res_p + res_x}}
         emit(out)
-    op.close()
     if P > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -86,3 +86,12 @@ def grid_points(dims):
 
 def uniform_points(n, dim, seed):
     return np.random.default_rng(seed).random((n, dim))
+
+
+def fd_grid_points(n):
+    """n x n interior vertex grid of Omega = [-1, 1]^2: x_i = -1 + (i+1) h, h = 2 / (n+1)
+    ("N points with spacing h in Omega"; reading R10), meshgrid(ij) order."""
+    h = 2.0 / (n + 1)
+    ax = -1.0 + h * np.arange(1, n + 1, dtype=np.float64)
+    g = np.meshgrid(ax, ax, indexing="ij")
+    return np.stack([a.reshape(-1) for a in g], axis=1)

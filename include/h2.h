@@ -149,6 +149,22 @@ int h2_plan_counts(h2_handle h, int64_t counts[8]);
 int h2_plan_census(const h2_desc *d, int level, int64_t *pid, int64_t *nodes_ptr, int64_t *nodes,
                    int64_t *npid, int64_t *nnodes);
 
+/* ---- Loopback groups (TEST / DIAGNOSTIC entry points) --------------------------------------
+ * Emulate P ranks inside ONE process on the current GPU, so the multi-rank code path (x^ and
+ * x-halo packs, off-diagonal coupling from the receive chunks, halo-fed dense blocks, replicated
+ * top tree, alg:optimized_dist_mult) can be checked with a single device.
+ * The per-call NCCL groups are replaced by device-to-device copies of the same bytes between the
+ * members' send and receive buffers, on one stream, between the members' upsweep halves and their
+ * coupling / downsweep halves.  Production runs use h2_create with NCCL.
+ * h2_group_create: descs[o] is rank o's view (descs[o]->rank == o, ->nranks == P); out[0..P)
+ *   receives the member handles (all NULL on failure).  Same validation and errors as h2_create.
+ * h2_group_matvec: Y[o] := alpha A X[o] + beta Y[o] for every member o (device pointers,
+ *   ld = n_local of o), asynchronous on member 0's stream.  hs must be all members in rank order.
+ *   h2_matvec on a member returns H2_ERR_STATE.  Members are released with h2_destroy. */
+int h2_group_create(const h2_desc *const *descs, int P, int nv_max, h2_handle *out);
+int h2_group_matvec(const h2_handle *hs, int P, double alpha, const void *const *X, double beta,
+                    void *const *Y, int nv);
+
 /* Release device memory, the NCCL communicator and streams.  NULL is a no-op. */
 int h2_destroy(h2_handle h);
 

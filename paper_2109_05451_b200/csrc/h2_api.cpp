@@ -234,6 +234,15 @@ struct Phase {
 }  // namespace
 
 // ------------------------------------------------------------------ the handle
+// P handles of one process on one GPU that exchange in-process (h2_group_create; tests only):
+// the per-call NCCL groups become device-to-device copies between the members' buffers.
+struct h2_group {
+    std::vector<h2_ctx *> members;
+    std::vector<const h2_desc *> descs;
+    std::vector<Layout> layouts;
+    std::vector<RemoteNeeds> needs;
+};
+
 struct h2_ctx {
     Layout L;
     int dtype = H2_F64;
@@ -241,6 +250,7 @@ struct h2_ctx {
     int nv_max = 1;
     int64_t n_local = 0, nleaf = 0;
     bool sticky = false;
+    h2_group *group = nullptr;       // loopback group (tests) or nullptr (NCCL / single rank)
     bool has_top = false;            // P > 1 and the top tree (levels < C) holds couplings
     cudaStream_t stream = nullptr;   // caller's stream (default legacy)
     cudaStream_t s_comm = nullptr;
@@ -342,6 +352,16 @@ ncclDataType_t nccl_type(int dtype) { return dtype == H2_F64 ? ncclDouble : nccl
 int release(h2_ctx *h)
 {
     if (!h) return H2_OK;
+    if (h->group) {                  // detach from a loopback group; the last member frees it
+        h2_group *g = h->group;
+        bool any = false;
+        for (auto &m : g->members) {
+            if (m == h) m = nullptr;
+            any = any || m != nullptr;
+        }
+        if (!any) delete g;
+        h->group = nullptr;
+    }
     // captured graphs hold references to the NCCL communicator's resources: destroy them first
     for (auto &g : h->graph)
         if (g) { cudaGraphExecDestroy(g); g = nullptr; }
@@ -400,17 +420,188 @@ int put_transposed(h2_ctx *h, int mem, const void *src, int64_t batch, int r, in
 template <typename T>
 int run_matvec(h2_ctx *h, T alpha, const T *X, int64_t ldx, T beta, T *Y, int64_t ldy, int nv);
 
+// ======================================================================== setup collectives
+// The setup-time exchanges of h2_create (the compressed node lists are
+// "communicated among GPUs during the setup phase"): all ranks' leaf sizes, the request lists
+// (what each peer needs from me) and, with top-tree couplings, every rank's branch-root transfer.
+// NCCL over the handle's communicator in production; an in-process loopback for h2_group_create
+// (P ranks emulated on one GPU, tests only).
+struct SetupComm {
+    virtual ~SetupComm() {}
+    // all ranks' leaf sizes, rank-major: all[o * nleaf + i]
+    virtual int leaf_sizes(h2_ctx *h, const std::vector<int64_t> &mine, std::vector<int64_t> &all) = 0;
+    // give_x[o] / give_h[o]: the x^ node keys / leaves peer o needs from this rank
+    virtual int requests(h2_ctx *h, const RemoteNeeds &rn, std::map<int, std::vector<int64_t>> &give_x,
+                         std::map<int, std::vector<int64_t>> &give_h) = 0;
+    // dst[o * per ..]: F_C^T of rank o's branch root (k^{C-1} x k^C, column-major)
+    virtual int gather_FtC(h2_ctx *h, void *dst, int64_t per) = 0;
+};
+
+// Peer o asked for `keys` (nx x^ node keys, then leaves): check that this rank owns them.
+int check_requests(h2_ctx *h, int o, const std::vector<int64_t> &keys, int64_t nx,
+                   std::map<int, std::vector<int64_t>> &give_x, std::map<int, std::vector<int64_t>> &give_h)
+{
+    const Layout &L = h->L;
+    for (int64_t i = 0; i < (int64_t)keys.size(); ++i) {
+        if (i < nx) {
+            int l = key_level(keys[i]);
+            if (l > L.q || L.owner(l, key_node(keys[i])) != L.p)
+                return fail(H2_ERR_STRUCT, "peer requested a node this rank does not own");
+            give_x[o].push_back(keys[i]);
+        } else {
+            if (L.owner(L.q, keys[i]) != L.p) return fail(H2_ERR_STRUCT, "peer requested a leaf this rank does not own");
+            give_h[o].push_back(keys[i]);
+        }
+    }
+    return H2_OK;
+}
+
+struct NcclSetup : SetupComm {
+    int leaf_sizes(h2_ctx *h, const std::vector<int64_t> &mine, std::vector<int64_t> &all) override
+    {
+        const int P = h->L.P;
+        const int64_t n = (int64_t)mine.size();
+        cudaError_t err;
+        int64_t *dm = (int64_t *)dalloc(h, n * 8, err);
+        int64_t *dall = (int64_t *)dalloc(h, n * P * 8, err);
+        if (!dm || !dall) return cuda_fail(h, err, "cudaMalloc(setup)");
+        H2_CUDA(h, cudaMemcpy(dm, mine.data(), n * 8, cudaMemcpyHostToDevice));
+        H2_NCCL(h, g_nccl.AllGather(dm, dall, n, ncclInt64, h->comm, h->s_comm));
+        H2_CUDA(h, cudaStreamSynchronize(h->s_comm));
+        all.resize(n * P);
+        H2_CUDA(h, cudaMemcpy(all.data(), dall, n * P * 8, cudaMemcpyDeviceToHost));
+        return H2_OK;
+    }
+    int requests(h2_ctx *h, const RemoteNeeds &rn, std::map<int, std::vector<int64_t>> &give_x,
+                 std::map<int, std::vector<int64_t>> &give_h) override
+    {
+        const int P = h->L.P, p = h->L.p;
+        cudaError_t err;
+        // request counts: cnt[2*o + 0/1] = #x^ nodes / #leaves I need from o
+        std::vector<int64_t> cnt(2 * P, 0), allcnt(2 * P * P, 0);
+        for (auto &kv : rn.need_x) cnt[2 * kv.first] = (int64_t)kv.second.size();
+        for (auto &kv : rn.need_h) cnt[2 * kv.first + 1] = (int64_t)kv.second.size();
+        int64_t *dc = (int64_t *)dalloc(h, 2 * P * 8, err);
+        int64_t *dac = (int64_t *)dalloc(h, 2 * P * P * 8, err);
+        if (!dc || !dac) return cuda_fail(h, err, "cudaMalloc(setup)");
+        H2_CUDA(h, cudaMemcpy(dc, cnt.data(), 2 * P * 8, cudaMemcpyHostToDevice));
+        H2_NCCL(h, g_nccl.AllGather(dc, dac, 2 * P, ncclInt64, h->comm, h->s_comm));
+        H2_CUDA(h, cudaStreamSynchronize(h->s_comm));
+        H2_CUDA(h, cudaMemcpy(allcnt.data(), dac, 2 * P * P * 8, cudaMemcpyDeviceToHost));
+        std::map<int, int64_t *> dreq_out, dreq_in;
+        std::map<int, std::vector<int64_t>> req_out;
+        for (int o = 0; o < P; ++o) {
+            if (o == p) continue;
+            std::vector<int64_t> v;
+            if (rn.need_x.count(o)) v.insert(v.end(), rn.need_x.at(o).begin(), rn.need_x.at(o).end());
+            if (rn.need_h.count(o)) v.insert(v.end(), rn.need_h.at(o).begin(), rn.need_h.at(o).end());
+            int64_t nin = allcnt[2 * P * o + 2 * p] + allcnt[2 * P * o + 2 * p + 1];
+            if (!v.empty()) {
+                dreq_out[o] = (int64_t *)dalloc(h, v.size() * 8, err);
+                if (!dreq_out[o]) return cuda_fail(h, err, "cudaMalloc(setup)");
+                H2_CUDA(h, cudaMemcpy(dreq_out[o], v.data(), v.size() * 8, cudaMemcpyHostToDevice));
+                req_out[o] = v;
+            }
+            if (nin) {
+                dreq_in[o] = (int64_t *)dalloc(h, nin * 8, err);
+                if (!dreq_in[o]) return cuda_fail(h, err, "cudaMalloc(setup)");
+            }
+        }
+        H2_NCCL(h, g_nccl.GroupStart());
+        for (auto &kv : req_out)
+            H2_NCCL(h, g_nccl.Send(dreq_out[kv.first], kv.second.size(), ncclInt64, kv.first, h->comm, h->s_comm));
+        for (auto &kv : dreq_in) {
+            int o = kv.first;
+            int64_t nin = allcnt[2 * P * o + 2 * p] + allcnt[2 * P * o + 2 * p + 1];
+            H2_NCCL(h, g_nccl.Recv(kv.second, nin, ncclInt64, o, h->comm, h->s_comm));
+        }
+        H2_NCCL(h, g_nccl.GroupEnd());
+        H2_CUDA(h, cudaStreamSynchronize(h->s_comm));
+        for (auto &kv : dreq_in) {
+            int o = kv.first;
+            int64_t nx = allcnt[2 * P * o + 2 * p], nh = allcnt[2 * P * o + 2 * p + 1];
+            std::vector<int64_t> v(nx + nh);
+            H2_CUDA(h, cudaMemcpy(v.data(), kv.second, (nx + nh) * 8, cudaMemcpyDeviceToHost));
+            int rc = check_requests(h, o, v, nx, give_x, give_h);
+            if (rc != H2_OK) return rc;
+        }
+        return H2_OK;
+    }
+    int gather_FtC(h2_ctx *h, void *dst, int64_t per) override
+    {
+        H2_NCCL(h, g_nccl.AllGather(h->Ft[h->L.C], dst, per, nccl_type(h->dtype), h->comm, h->s_comm));
+        H2_CUDA(h, cudaStreamSynchronize(h->s_comm));
+        return H2_OK;
+    }
+};
+
+// In-process setup of a loopback group: every member's description is at hand.
+struct LoopSetup : SetupComm {
+    h2_group *g = nullptr;
+    int leaf_sizes(h2_ctx *h, const std::vector<int64_t> &mine, std::vector<int64_t> &all) override
+    {
+        (void)mine;
+        all.clear();
+        for (size_t o = 0; o < g->descs.size(); ++o) {
+            const int64_t n = g->layouts[o].held(g->layouts[o].q);
+            for (int64_t i = 0; i < n; ++i) all.push_back(g->descs[o]->leaf_ptr[i + 1] - g->descs[o]->leaf_ptr[i]);
+        }
+        (void)h;
+        return H2_OK;
+    }
+    int requests(h2_ctx *h, const RemoteNeeds &, std::map<int, std::vector<int64_t>> &give_x,
+                 std::map<int, std::vector<int64_t>> &give_h) override
+    {
+        const int p = h->L.p;
+        for (int o = 0; o < (int)g->descs.size(); ++o) {
+            if (o == p) continue;
+            const RemoteNeeds &ro = g->needs[o];
+            std::vector<int64_t> v;
+            int64_t nx = 0;
+            if (ro.need_x.count(p)) { v = ro.need_x.at(p); nx = (int64_t)v.size(); }
+            if (ro.need_h.count(p)) v.insert(v.end(), ro.need_h.at(p).begin(), ro.need_h.at(p).end());
+            int rc = check_requests(h, o, v, nx, give_x, give_h);
+            if (rc != H2_OK) return rc;
+        }
+        return H2_OK;
+    }
+    int gather_FtC(h2_ctx *h, void *dst, int64_t per) override
+    {
+        const int C = h->L.C;
+        const int kc = h->L.k[C], kp = h->L.k[C - 1];
+        for (int o = 0; o < (int)g->descs.size(); ++o) {
+            const h2_desc *d = g->descs[o];
+            const void *src = d->F[C];
+            void *tmp = nullptr;
+            if (d->mem == H2_MEM_HOST) {
+                H2_CUDA(h, cudaMalloc(&tmp, (size_t)per * h->esz));
+                H2_CUDA(h, cudaMemcpy(tmp, src, (size_t)per * h->esz, cudaMemcpyHostToDevice));
+                src = tmp;
+            }
+            char *slot = static_cast<char *>(dst) + (size_t)o * per * h->esz;
+            cudaError_t e = h->dtype == H2_F64
+                                ? launch_transpose<double>((const double *)src, (double *)slot, 1, kc, kp, 0)
+                                : launch_transpose<float>((const float *)src, (float *)slot, 1, kc, kp, 0);
+            if (e == cudaSuccess) e = cudaDeviceSynchronize();
+            if (tmp) cudaFree(tmp);
+            if (e != cudaSuccess) return cuda_fail(h, e, "transpose(F_C)");
+        }
+        return H2_OK;
+    }
+};
+
 }  // namespace
 
 // ======================================================================== create
-static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id, h2_handle *out)
+static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id, h2_handle *out,
+                       SetupComm *loop = nullptr, h2_group *grp = nullptr)
 {
     if (!out) return fail(H2_ERR_ARG, "out is NULL");
     *out = nullptr;
     Layout L;
     int rc = validate(d, nv_max, L);
     if (rc != H2_OK) return rc;
-    if (L.P > 1 && !nccl_unique_id) return fail(H2_ERR_ARG, "nccl_unique_id required when nranks > 1");
+    if (L.P > 1 && !nccl_unique_id && !loop) return fail(H2_ERR_ARG, "nccl_unique_id required when nranks > 1");
 
     h2_ctx *h = new (std::nothrow) h2_ctx();
     if (!h) return fail(H2_ERR_OOM, "host allocation failed");
@@ -420,6 +611,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     h->nv_max = nv_max;
     h->n_local = d->n_local;
     h->nleaf = L.held(L.q);
+    h->group = grp;
     const int q = L.q, m = L.m, p = L.p, P = L.P, C = L.C;
     const std::vector<int> &k = L.k;
     const int64_t nleaf = h->nleaf;
@@ -445,8 +637,8 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     for (int l = 0; l < C; ++l) n_top += d->S_rowptr[l][L.held(l)];
     h->has_top = (P > 1 && n_top > 0);
 
-    // ---- NCCL communicator
-    if (P > 1) {
+    // ---- NCCL communicator (loopback groups exchange in-process instead)
+    if (P > 1 && !loop) {
         if (!load_nccl()) { release(h); return fail(H2_ERR_NCCL, "cannot load libnccl.so.2 (set H2_NCCL_LIB)"); }
         ncclUniqueId id;
         memcpy(&id, nccl_unique_id, sizeof(id));
@@ -458,10 +650,14 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             release(h);
             return fail(H2_ERR_NCCL, msg);
         }
+    }
+    if (P > 1) {
         H2_TRYC(cudaStreamCreateWithFlags(&h->s_comm, cudaStreamNonBlocking));
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_packed, cudaEventDisableTiming));
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_recv, cudaEventDisableTiming));
     }
+    NcclSetup nccl_setup;
+    SetupComm *sc = loop ? loop : &nccl_setup;
 
     // ---- per-call argument slot and the capture stream
     {
@@ -575,78 +771,10 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     std::map<int, std::vector<int64_t>> give_x, give_h;   // what each peer needs from me
     if (P > 1) {
         cudaError_t err;
-        // leaf sizes (allgather)
         std::vector<int64_t> mine(nleaf);
         for (int64_t i = 0; i < nleaf; ++i) mine[i] = d->leaf_ptr[i + 1] - d->leaf_ptr[i];
-        int64_t *dm = (int64_t *)dalloc(h, nleaf * 8, err);
-        int64_t *dall = (int64_t *)dalloc(h, nleaf * P * 8, err);
-        if (!dm || !dall) H2_TRY(cuda_fail(h, err, "cudaMalloc(setup)"));
-        H2_TRYC(cudaMemcpy(dm, mine.data(), nleaf * 8, cudaMemcpyHostToDevice));
-        H2_TRY([&]() -> int { H2_NCCL(h, g_nccl.AllGather(dm, dall, nleaf, ncclInt64, h->comm, h->s_comm)); return H2_OK; }());
-        H2_TRYC(cudaStreamSynchronize(h->s_comm));
-        gleaf_size.resize(nleaf * P);
-        H2_TRYC(cudaMemcpy(gleaf_size.data(), dall, nleaf * P * 8, cudaMemcpyDeviceToHost));
-        // request counts: cnt[2*o + 0/1] = #x^ nodes / #leaves I need from o
-        std::vector<int64_t> cnt(2 * P, 0), allcnt(2 * P * P, 0);
-        for (auto &kv : need_x) cnt[2 * kv.first] = (int64_t)kv.second.size();
-        for (auto &kv : need_h) cnt[2 * kv.first + 1] = (int64_t)kv.second.size();
-        int64_t *dc = (int64_t *)dalloc(h, 2 * P * 8, err);
-        int64_t *dac = (int64_t *)dalloc(h, 2 * P * P * 8, err);
-        if (!dc || !dac) H2_TRY(cuda_fail(h, err, "cudaMalloc(setup)"));
-        H2_TRYC(cudaMemcpy(dc, cnt.data(), 2 * P * 8, cudaMemcpyHostToDevice));
-        H2_TRY([&]() -> int { H2_NCCL(h, g_nccl.AllGather(dc, dac, 2 * P, ncclInt64, h->comm, h->s_comm)); return H2_OK; }());
-        H2_TRYC(cudaStreamSynchronize(h->s_comm));
-        H2_TRYC(cudaMemcpy(allcnt.data(), dac, 2 * P * P * 8, cudaMemcpyDeviceToHost));
-        // exchange the request lists (setup-time, "communicated among GPUs during
-        // the setup phase")
-        std::map<int, int64_t *> dreq_out, dreq_in;
-        std::map<int, std::vector<int64_t>> req_out;
-        for (int o = 0; o < P; ++o) {
-            if (o == p) continue;
-            std::vector<int64_t> v;
-            if (need_x.count(o)) v.insert(v.end(), need_x[o].begin(), need_x[o].end());
-            if (need_h.count(o)) v.insert(v.end(), need_h[o].begin(), need_h[o].end());
-            int64_t nin = allcnt[2 * P * o + 2 * p] + allcnt[2 * P * o + 2 * p + 1];
-            if (!v.empty()) {
-                dreq_out[o] = (int64_t *)dalloc(h, v.size() * 8, err);
-                if (!dreq_out[o]) H2_TRY(cuda_fail(h, err, "cudaMalloc(setup)"));
-                H2_TRYC(cudaMemcpy(dreq_out[o], v.data(), v.size() * 8, cudaMemcpyHostToDevice));
-                req_out[o] = v;
-            }
-            if (nin) {
-                dreq_in[o] = (int64_t *)dalloc(h, nin * 8, err);
-                if (!dreq_in[o]) H2_TRY(cuda_fail(h, err, "cudaMalloc(setup)"));
-            }
-        }
-        H2_TRY([&]() -> int {
-            H2_NCCL(h, g_nccl.GroupStart());
-            for (auto &kv : req_out)
-                H2_NCCL(h, g_nccl.Send(dreq_out[kv.first], kv.second.size(), ncclInt64, kv.first, h->comm, h->s_comm));
-            for (auto &kv : dreq_in) {
-                int o = kv.first;
-                int64_t nin = allcnt[2 * P * o + 2 * p] + allcnt[2 * P * o + 2 * p + 1];
-                H2_NCCL(h, g_nccl.Recv(kv.second, nin, ncclInt64, o, h->comm, h->s_comm));
-            }
-            H2_NCCL(h, g_nccl.GroupEnd());
-            return H2_OK;
-        }());
-        H2_TRYC(cudaStreamSynchronize(h->s_comm));
-        for (auto &kv : dreq_in) {
-            int o = kv.first;
-            int64_t nx = allcnt[2 * P * o + 2 * p], nh = allcnt[2 * P * o + 2 * p + 1];
-            std::vector<int64_t> v(nx + nh);
-            H2_TRYC(cudaMemcpy(v.data(), kv.second, (nx + nh) * 8, cudaMemcpyDeviceToHost));
-            for (int64_t i = 0; i < nx; ++i) {
-                int l = key_level(v[i]);
-                int64_t g = key_node(v[i]);
-                if (l > q || L.owner(l, g) != p) H2_TRY(fail(H2_ERR_STRUCT, "peer requested a node this rank does not own"));
-                give_x[o].push_back(v[i]);
-            }
-            for (int64_t i = nx; i < nx + nh; ++i) {
-                if (L.owner(q, v[i]) != p) H2_TRY(fail(H2_ERR_STRUCT, "peer requested a leaf this rank does not own"));
-                give_h[o].push_back(v[i]);
-            }
-        }
+        H2_TRY(sc->leaf_sizes(h, mine, gleaf_size));
+        H2_TRY(sc->requests(h, rn, give_x, give_h));
         H2_DBG("rank %d: request lists exchanged (give_x peers %zu, give_h peers %zu)", p, give_x.size(), give_h.size());
         // F_C^T of every rank for the replicated top upsweep (branch-root transfers
         // duplicated at the leaf level of the root branch)
@@ -654,8 +782,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             int64_t per = (int64_t)k[C] * k[C - 1];
             void *all = dalloc(h, (size_t)per * P * h->esz, err);
             if (!all) H2_TRY(cuda_fail(h, err, "cudaMalloc(F_C)"));
-            H2_TRY([&]() -> int { H2_NCCL(h, g_nccl.AllGather(h->Ft[C], all, per, nccl_type(h->dtype), h->comm, h->s_comm)); return H2_OK; }());
-            H2_TRYC(cudaStreamSynchronize(h->s_comm));
+            H2_TRY(sc->gather_FtC(h, all, per));
             h->FtC_all = all;
         }
     }
@@ -1034,9 +1161,10 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     for (auto &kv : need_h) hr += (int64_t)kv.second.size();
     int64_t c8[8] = {n_diag, n_off, n_root, nd_diag, nd_off, peers_n, xr, hr};
     memcpy(h->counts, c8, sizeof(c8));
-    int launches = 2 + (int)(h->use_sweep ? h->up_sweeps.size() : h->up_stages.size()) +
+    // kernels per call: k_set_args, k_up_leaf, the sweeps, k_rows per coupling class, k_leaf_dense
+    int launches = 3 + (int)(h->use_sweep ? h->up_sweeps.size() : h->up_stages.size()) +
                    (int)h->coup_diag.size() + (int)h->coup_leaf.size() +
-                   (int)(h->use_sweep ? h->dn_sweeps.size() : h->down_stages.size()) + 2;
+                   (int)(h->use_sweep ? h->dn_sweeps.size() : h->down_stages.size());
     if (P > 1) {
         launches += 2;   // pack x^, pack halo
         for (int ci = 0; ci < 3; ++ci) launches += h->coup_off[ci].n ? 1 : 0;
@@ -1082,8 +1210,12 @@ const int kPhaseSpan[H2_NPHASE + 1][2] = {{0, 1}, {2, 3}, {3, 4}, {4, 5}, {5, 6}
 
 // Enqueue one matvec for nv vectors on `st`; X, Y, alpha, beta come from the device CallArgs
 // (written by k_set_args before), so the same sequence can be captured once as a CUDA graph.
+// part: PART_ALL (NCCL or single rank), or for loopback groups PART_UP (everything before the
+// exchange: x halo pack, leaf projection, leaf-level coupling, upsweep, x^ pack) and PART_DOWN
+// (everything after it: top tree, couplings, downsweep, leaves), the group copying between them.
+enum { PART_ALL = 0, PART_UP = 1, PART_DOWN = 2 };
 template <typename T>
-int enqueue(h2_ctx *h, int nv, cudaStream_t st)
+int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
 {
     const Layout &L = h->L;
     const int q = L.q, C = L.C;
@@ -1093,13 +1225,15 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     int rc;
 #define H2_MARK(i) if ((rc = mark(h, i, st)) != H2_OK) return rc
     ncclDataType_t ty = nccl_type(h->dtype);
-    // profiling serializes the side stream onto the main one so every phase's events bracket
-    // only its own kernels (clean per-kernel durations for the roofline)
-    cudaStream_t s_leafc = h->prof ? st : h->s_leafc;
+    const bool nccl = L.P > 1 && part == PART_ALL;
+    // profiling (and loopback groups) serialize the side stream onto the main one so every
+    // phase's events bracket only its own kernels (clean per-kernel durations for the roofline)
+    cudaStream_t s_leafc = (h->prof || h->group) ? st : h->s_leafc;
+    if (part != PART_DOWN) {
     H2_MARK(0);
     // 0. x-leaf halo for the off-process dense blocks (P > 1): X is an input, so the exchange
     //    starts at t = 0 on the comm stream
-    if (L.P > 1) {
+    if (nccl) {
         H2_CUDA(h, cudaEventRecord(h->ev_fork, st));
         H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_fork, 0));
         H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_h0, h->nseg_h, (const T *)nullptr, 0, args, (T *)h->hsend, nv, h->s_comm));
@@ -1110,6 +1244,8 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
         }
         H2_NCCL(h, g_nccl.GroupEnd());
         H2_CUDA(h, cudaEventRecord(h->ev_halo, h->s_comm));
+    } else if (L.P > 1) {
+        H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_h0, h->nseg_h, (const T *)nullptr, 0, args, (T *)h->hsend, nv, st));
     }
     // 1. leaf projection (alg:upsweep2 line 3)
     H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
@@ -1138,8 +1274,9 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     H2_MARK(3);
     // 2. exchange (P > 1): pack my x^ nodes that peers need, one NCCL group on the comm stream,
     //    overlapped with the diagonal multiply (alg:optimized_dist_mult)
-    if (L.P > 1) {
+    if (L.P > 1)
         H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_x0, h->nseg_x, xh, h->xh_plane, args, (T *)h->xsend, nv, st));
+    if (nccl) {
         H2_CUDA(h, cudaEventRecord(h->ev_packed, st));
         H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_packed, 0));
         H2_NCCL(h, g_nccl.GroupStart());
@@ -1149,9 +1286,13 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
         }
         H2_NCCL(h, g_nccl.GroupEnd());
         H2_CUDA(h, cudaEventRecord(h->ev_recv, h->s_comm));
-        // replicated top tree: gather the branch roots, upsweep the top
-        if (h->has_top) {
-            const int kC = L.k[C];
+    }
+    if (part == PART_UP) return H2_OK;
+    }
+    // replicated top tree: gather the branch roots, upsweep the top
+    if (h->has_top) {
+        const int kC = L.k[C];
+        if (nccl) {
             // own root -> gather slot p, then allgather in place over the P slots of every plane
             for (int n = 0; n < nv; ++n) {
                 T *g = xh + h->xgather + (int64_t)n * h->xh_plane;
@@ -1159,10 +1300,10 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
                                            kC * sizeof(T), cudaMemcpyDeviceToDevice, st));
                 H2_NCCL(h, g_nccl.AllGather(g + (int64_t)L.p * kC, g, kC, ty, h->comm, st));
             }
-            for (const auto &sg : h->top_stages)
-                H2_CUDA(h, launch_tree<T>(MODE_WRITE, sg.st, sg.nctas, h->d_tasks, h->d_blks, xh, h->xh_plane,
-                                          nv, sg.r, st));
         }
+        for (const auto &sg : h->top_stages)
+            H2_CUDA(h, launch_tree<T>(MODE_WRITE, sg.st, sg.nctas, h->d_tasks, h->d_blks, xh, h->xh_plane,
+                                      nv, sg.r, st));
     }
     H2_MARK(4);
     // 3. coupling multiply, diagonal part of the levels above the leaves (alg:mult)
@@ -1174,7 +1315,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     //    it accumulates into leaf-level rows too, so the leaf coupling stream joins first
     if (L.P > 1) {
         H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_leafc, 0));
-        H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_recv, 0));
+        if (nccl) H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_recv, 0));
         for (int ci = 0; ci < 3; ++ci) {
             const Phase &ph = h->coup_off[ci];
             H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(ph), ph.n, h->d_blks, (const T *)h->xrecv, 0, yh,
@@ -1196,7 +1337,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     H2_MARK(7);
     // 6. leaves: last transfer + U expansion + dense near field + epilogue in one kernel (Y
     //    written once, reading R11/R18), after the side streams joined
-    if (L.P > 1) H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_halo, 0));   // the kernel reads the x halo
+    if (nccl) H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_halo, 0));   // the kernel reads the x halo
     H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_leafc, 0));
     H2_MARK(8);
     const int kq = L.k[q], kp = q >= 1 ? L.k[q - 1] : 1;
@@ -1205,6 +1346,41 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st)
     H2_MARK(9);
     if (h->prof) h->ev_used += NEV;
 #undef H2_MARK
+    return H2_OK;
+}
+
+// Loopback group exchange (tests): every member's x^ / x-halo send chunk for peer o is copied
+// into o's receive chunk from it, and the branch roots of level C into every member's gather
+// region -- the same bytes the NCCL groups move.  All on one stream, between PART_UP and
+// PART_DOWN of every member.
+int group_exchange(h2_group *g, int nv, cudaStream_t st)
+{
+    for (h2_ctx *h : g->members) {
+        const size_t esz = h->esz;
+        for (const auto &pr : h->peers) {
+            h2_ctx *o = g->members[pr.rank];
+            const h2_ctx::Peer *back = nullptr;
+            for (const auto &q : o->peers)
+                if (q.rank == h->L.p) back = &q;
+            if (!back) return fail(H2_ERR_STATE, "loopback group: asymmetric peer lists");
+            if (pr.xs_cnt != back->xr_cnt || pr.hs_cnt != back->hr_cnt)
+                return fail(H2_ERR_STATE, "loopback group: send / receive counts disagree");
+            if (pr.xs_cnt)
+                H2_CUDA(h, cudaMemcpyAsync((char *)o->xrecv + back->xr_off * esz, (char *)h->xsend + pr.xs_off * esz,
+                                           (size_t)pr.xs_cnt * nv * esz, cudaMemcpyDeviceToDevice, st));
+            if (pr.hs_cnt)
+                H2_CUDA(h, cudaMemcpyAsync((char *)o->hrecv + back->hr_off * esz, (char *)h->hsend + pr.hs_off * esz,
+                                           (size_t)pr.hs_cnt * nv * esz, cudaMemcpyDeviceToDevice, st));
+        }
+        if (h->has_top) {
+            const int C = h->L.C, kC = h->L.k[C];
+            for (h2_ctx *o : g->members)
+                H2_CUDA(h, cudaMemcpy2DAsync((char *)h->xh + (h->xgather + (int64_t)o->L.p * kC) * esz,
+                                             (size_t)h->xh_plane * esz, (char *)o->xh + o->xh_base[C] * esz,
+                                             (size_t)o->xh_plane * esz, (size_t)kC * esz, nv,
+                                             cudaMemcpyDeviceToDevice, st));
+        }
+    }
     return H2_OK;
 }
 
@@ -1259,6 +1435,7 @@ extern "C" int h2_matvec_ld(h2_handle h, double alpha, const void *X, int64_t ld
 {
     int rc = check_call(h, nv);
     if (rc != H2_OK) return rc;
+    if (h->group) return fail(H2_ERR_STATE, "handle belongs to a loopback group: use h2_group_matvec");
     if (!X || !Y) return fail(H2_ERR_ARG, "X or Y is NULL");
     if (ldx < h->n_local || ldy < h->n_local) return fail(H2_ERR_SHAPE, "ld < n_local");
     if (h->dtype == H2_F64)
@@ -1291,6 +1468,93 @@ extern "C" int h2_matvec_host(h2_handle h, double alpha, const void *X, double b
     H2_CUDA(h, cudaMemcpyAsync(Y, h->dY, bytes, cudaMemcpyDeviceToHost, h->stream));
     H2_CUDA(h, cudaStreamSynchronize(h->stream));
     return H2_OK;
+}
+
+// ======================================================================== loopback groups
+extern "C" int h2_group_create(const h2_desc *const *descs, int P, int nv_max, h2_handle *out)
+{
+    if (!descs || !out || P < 1) return fail(H2_ERR_ARG, "bad argument");
+    for (int o = 0; o < P; ++o) out[o] = nullptr;
+    try {
+        h2_group *g = new h2_group();
+        g->descs.assign(descs, descs + P);
+        g->layouts.resize(P);
+        g->needs.resize(P);
+        for (int o = 0; o < P; ++o) {
+            int rc = validate(descs[o], nv_max, g->layouts[o]);
+            if (rc == H2_OK && (descs[o]->nranks != P || descs[o]->rank != o))
+                rc = fail(H2_ERR_ARG, "group member o must describe rank o of nranks = P");
+            if (rc != H2_OK) { delete g; return rc; }
+            remote_needs(descs[o], g->layouts[o], g->needs[o]);
+        }
+        g->members.assign(P, nullptr);
+        LoopSetup ls;
+        ls.g = g;
+        for (int o = 0; o < P; ++o) {
+            h2_handle h = nullptr;
+            int rc = create_impl(descs[o], nv_max, nullptr, &h, &ls, g);
+            if (rc != H2_OK) {
+                std::string msg = g_err;
+                int live = 0;
+                for (int u = 0; u < o; ++u) live += g->members[u] != nullptr;
+                for (int u = 0; u < o; ++u) { h2_ctx *m = g->members[u]; if (m) release(m); }
+                if (!live) delete g;
+                for (int u = 0; u < P; ++u) out[u] = nullptr;
+                g_err = msg;
+                return rc;
+            }
+            g->members[o] = h;
+            out[o] = h;
+        }
+        return H2_OK;
+    } catch (const std::exception &e) {
+        return fail(H2_ERR_OOM, std::string("h2_group_create: ") + e.what());
+    }
+}
+
+namespace {
+template <typename T>
+int group_matvec(h2_ctx *const *hs, int P, T alpha, const void *const *X, T beta, void *const *Y, int nv)
+{
+    h2_group *g = hs[0]->group;
+    cudaStream_t st = hs[0]->stream;
+    for (int o = 0; o < P; ++o) {
+        h2_ctx *h = hs[o];
+        if (alpha == T(0)) {
+            H2_CUDA(h, launch_scale<T>((T *)Y[o], h->n_local, h->n_local, nv, beta, st));
+            continue;
+        }
+        H2_CUDA(h, launch_set_args<T>((CallArgs<T> *)h->dargs, (const T *)X[o], h->n_local, (T *)Y[o], h->n_local,
+                                      alpha, beta, st));
+        int rc = enqueue<T>(h, nv, st, PART_UP);
+        if (rc != H2_OK) return rc;
+    }
+    if (alpha == T(0)) return H2_OK;
+    int rc = group_exchange(g, nv, st);
+    if (rc != H2_OK) return rc;
+    for (int o = 0; o < P; ++o) {
+        rc = enqueue<T>(hs[o], nv, st, PART_DOWN);
+        if (rc != H2_OK) return rc;
+    }
+    return H2_OK;
+}
+}  // namespace
+
+extern "C" int h2_group_matvec(const h2_handle *hs, int P, double alpha, const void *const *X, double beta,
+                               void *const *Y, int nv)
+{
+    if (!hs || !X || !Y || P < 1) return fail(H2_ERR_ARG, "bad argument");
+    h2_group *g = hs[0] ? hs[0]->group : nullptr;
+    if (!g || (int)g->members.size() != P) return fail(H2_ERR_ARG, "handles are not one complete loopback group");
+    for (int o = 0; o < P; ++o) {
+        if (hs[o] != g->members[o]) return fail(H2_ERR_ARG, "handles must be the group's members in rank order");
+        int rc = check_call(hs[o], nv);
+        if (rc != H2_OK) return rc;
+        if (!X[o] || !Y[o]) return fail(H2_ERR_ARG, "X or Y is NULL");
+        hs[o]->prof = false;
+    }
+    if (hs[0]->dtype == H2_F64) return group_matvec<double>(hs, P, alpha, X, beta, Y, nv);
+    return group_matvec<float>(hs, P, (float)alpha, X, (float)beta, Y, nv);
 }
 
 extern "C" int h2_set_stream(h2_handle h, void *stream)
