@@ -71,7 +71,9 @@ def make_points(spec, seed=SEED, P=1, weak=False):
     if spec[0] == "uniform":
         return uniform_points(spec[1] * (P if weak else 1), spec[2], seed)
     if spec[0] == "fdgrid":
-        n = FD_WEAK_N.get(P, int(round(spec[1] * np.sqrt(P)))) if weak else spec[1]
+        n = spec[1]
+        if weak and P > 1:
+            n = FD_WEAK_N[P] if n == FD_WEAK_N[1] and P in FD_WEAK_N else int(round(n * np.sqrt(P)))
         return fd_grid_points(n)
     return grid_points(grid_for(spec[1], P) if weak else spec[1])
 

@@ -134,6 +134,9 @@ int h2_set_profiling(h2_handle h, int on);
 int h2_phase_times(h2_handle h, double ms[H2_NPHASE + 1], int64_t *ncalls);
 int h2_phase_stats(h2_handle h, int nv, double bytes[H2_NPHASE + 1], double flops[H2_NPHASE + 1]);
 
+/* Rows of X / Y on this rank (the n_local of the description). */
+int h2_n_local(h2_handle h, int64_t *n_local);
+
 /* Plan facts for tests: counts[0..7] = {diag coupling blocks, offdiag coupling blocks,
  * root (top-tree) coupling blocks, diag dense blocks, offdiag dense blocks, peers,
  * remote x^ nodes received, remote leaves received}. */
@@ -164,6 +167,28 @@ int h2_plan_census(const h2_desc *d, int level, int64_t *pid, int64_t *nodes_ptr
 int h2_group_create(const h2_desc *const *descs, int P, int nv_max, h2_handle *out);
 int h2_group_matvec(const h2_handle *hs, int P, double alpha, const void *const *X, double beta,
                     void *const *Y, int nv);
+
+/* ---- The .h2m flat file ("header {N, m, depth, level ranks}, then level-ordered
+ * arrays"; written by the input generator h2gen/h2m.py) -------------------------------------
+ * Little-endian.  A 512-byte header: magic "H2MFLAT1"; u32 version (1), dtype (0 f64, 1 f32), dim,
+ * m, q, flags (bit 0: V aliases U, bit 1: F aliases E), kernel id, reserved; u64 N, n_D, seed;
+ * f64 eta, kernel parameters[4]; i32 k^l[32]; i64 n_S^l[32].  Then sections, each starting at a
+ * multiple of 64 bytes: points f64[N][dim] (tree order), perm i64[N], leaf_ptr i64[2^q+1],
+ * U_leaf T[2^q][m x k^q], V_leaf (unless aliased), E^l T[2^l][k^l x k^(l-1)] for l = 1..q, F^l
+ * (unless aliased), then per level l = 0..q: S_rowptr i64[2^l+1], S_col i32[n_S^l],
+ * S T[n_S^l][k^l x k^l]; then D_rowptr i64[2^q+1], D_col i32[n_D], D T[n_D][m x m].  All small
+ * matrices column-major; global node / leaf indices.
+ * h2_file_info: info[0..7] = {N, dim, m, q, dtype, total coupling blocks, n_D, k^q}; checks the
+ *   magic, version and that the file is as long as its header says (H2_ERR_STRUCT otherwise;
+ *   H2_ERR_ARG if it cannot be opened).  No device work.
+ * h2_create_from_file: rank `rank` of `nranks` reads only its own view (its branch at levels
+ *   >= C = log2 P, the top levels replicated) and calls h2_create with those
+ *   host arrays (same arguments, errors and collective semantics as h2_create). */
+int h2_file_info(const char *path, int64_t info[8]);
+int h2_create_from_file(const char *path, int rank, int nranks, int nv_max, const void *nccl_unique_id,
+                        h2_handle *out);
+/* Loopback-group form (tests): all P ranks' views read from the file, then h2_group_create. */
+int h2_group_create_from_file(const char *path, int P, int nv_max, h2_handle *out);
 
 /* Release device memory, the NCCL communicator and streams.  NULL is a no-op. */
 int h2_destroy(h2_handle h);

@@ -5,10 +5,10 @@
 Hot path: hand-written sm_100a CUDA kernels behind the C ABI in include/h2.h (libh2b200.so);
 this package is the thin ctypes binding (argument marshalling only).  See DESIGN.md.
 """
-from ._binding import (H2Operator, H2Error, load_library, nccl_unique_id, plan_census, LIB_PATH, EXPORTS, PHASES,
+from ._binding import (H2Operator, H2Group, H2Error, load_library, nccl_unique_id, plan_census, LIB_PATH, EXPORTS, PHASES,
                        H2_OK, H2_ERR_ARG, H2_ERR_SHAPE, H2_ERR_STRUCT, H2_ERR_CUDA, H2_ERR_NCCL,
                        H2_ERR_OOM, H2_ERR_STATE)
-from .operator import operator_from_h2data
+from .operator import operator_from_h2data, group_from_h2data
 
-__all__ = ["H2Operator", "H2Error", "load_library", "nccl_unique_id", "plan_census", "operator_from_h2data",
+__all__ = ["H2Operator", "H2Group", "group_from_h2data", "H2Error", "load_library", "nccl_unique_id", "plan_census", "operator_from_h2data",
            "LIB_PATH", "EXPORTS"]

@@ -15,6 +15,7 @@ H2_F64, H2_F32 = 0, 1
 H2_MEM_HOST, H2_MEM_DEVICE = 0, 1
 
 EXPORTS = ["h2_create", "h2_matvec", "h2_matvec_ld", "h2_matvec_host", "h2_set_stream", "h2_stats",
+           "h2_group_create", "h2_group_matvec", "h2_file_info", "h2_create_from_file", "h2_group_create_from_file", "h2_n_local",
            "h2_set_profiling", "h2_phase_times", "h2_phase_stats",
            "h2_plan_counts", "h2_plan_census", "h2_destroy", "h2_nccl_unique_id", "h2_last_error", "h2_version"]
 PHASES = ["up_leaf", "up_transfer", "exchange_top", "coupling_diag", "coupling_offdiag",
@@ -71,6 +72,12 @@ def load_library(path=None):
         "h2_phase_times": ([vp, C.POINTER(d), C.POINTER(C.c_int64)], i32),
         "h2_phase_stats": ([vp, i32, C.POINTER(d), C.POINTER(d)], i32),
         "h2_destroy": ([vp], i32),
+        "h2_group_create_from_file": ([C.c_char_p, i32, i32, C.POINTER(vp)], i32),
+        "h2_n_local": ([vp, C.POINTER(C.c_int64)], i32),
+        "h2_file_info": ([C.c_char_p, C.POINTER(C.c_int64)], i32),
+        "h2_create_from_file": ([C.c_char_p, i32, i32, i32, vp, C.POINTER(vp)], i32),
+        "h2_group_create": ([C.POINTER(C.POINTER(h2_desc)), i32, i32, C.POINTER(vp)], i32),
+        "h2_group_matvec": ([C.POINTER(vp), i32, d, C.POINTER(vp), d, C.POINTER(vp), i32], i32),
         "h2_nccl_unique_id": ([vp], i32),
         "h2_last_error": ([], C.c_char_p),
         "h2_version": ([], C.c_char_p),
@@ -153,6 +160,14 @@ class _Desc:
         self.desc = d
 
 
+def file_info(path):
+    """Header facts of an .h2m file (no GPU): N, dim, m, q, dtype, n_S (all levels), n_D, k^q."""
+    lib = load_library()
+    info = (C.c_int64 * 8)()
+    _check(lib.h2_file_info(os.fsencode(path), info))
+    return dict(zip(["N", "dim", "m", "q", "dtype", "n_S", "n_D", "k"], list(info)))
+
+
 def plan_census(level, **kw):
     """Host-only compressed off-diagonal node lists (pid, nodes_ptr, nodes) of one rank's view
     (PAPER.md:454-468); level -1 = dense halo leaves.  No GPU needed."""
@@ -202,6 +217,38 @@ class H2Operator:
                 self.device_index = torch.cuda.current_device()
         except Exception:
             pass
+
+    @classmethod
+    def from_file(cls, path, *, nv_max=16, rank=0, nranks=1, nccl_id=None):
+        """h2_create_from_file: this rank's view of an .h2m file (host reads, copied to the GPU)."""
+        lib = load_library()
+        self = cls.__new__(cls)
+        self._lib = lib
+        info = file_info(path)
+        self.dtype = H2_F64 if info["dtype"] == 0 else H2_F32
+        self.np_dtype = np.float64 if self.dtype == H2_F64 else np.float32
+        self.rank, self.nranks, self.nv_max = int(rank), int(nranks), int(nv_max)
+        idbuf = None
+        if self.nranks > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("nccl_id (128 bytes) required when nranks > 1")
+            idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        h = C.c_void_p()
+        _check(lib.h2_create_from_file(os.fsencode(path), self.rank, self.nranks, self.nv_max,
+                                       C.cast(idbuf, C.c_void_p) if idbuf else None, C.byref(h)))
+        self.handle = h
+        self._keep = []
+        nl = C.c_int64()
+        _check(lib.h2_n_local(h, C.byref(nl)))
+        self.n_local = int(nl.value)
+        self.device_index = None
+        try:
+            import torch
+            if torch.cuda.is_available():
+                self.device_index = torch.cuda.current_device()
+        except Exception:
+            pass
+        return self
 
     # -- calls
     def set_stream(self, stream_ptr):
@@ -300,6 +347,73 @@ class H2Operator:
             _check(self._lib.h2_destroy(self.handle))
             self.handle = None
             self._keep = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class H2Group:
+    """P ranks emulated in ONE process on the current GPU (h2_group_create; test entry point):
+    the multi-rank path with the per-call exchange done by device copies instead of NCCL.
+    views: list of P per-rank keyword dicts (operator.shard_arrays output, rank o at index o)."""
+
+    def __init__(self, views, *, dtype="f64", nv_max=16, path=None, P=None):
+        lib = load_library()
+        self._lib = lib
+        if path is not None:                  # h2_group_create_from_file: every view read from an .h2m file
+            self.P = int(P)
+            hs = (C.c_void_p * self.P)()
+            _check(lib.h2_group_create_from_file(os.fsencode(path), self.P, int(nv_max), hs))
+            self.handles, self.nv_max = hs, int(nv_max)
+            self.dtype = H2_F64 if file_info(path)["dtype"] == 0 else H2_F32
+            self.n_local = []
+            for o in range(self.P):
+                nl = C.c_int64()
+                _check(lib.h2_n_local(hs[o], C.byref(nl)))
+                self.n_local.append(int(nl.value))
+            return
+        self.P = len(views)
+        self._descs = [_Desc(dtype=dtype, **v) for v in views]
+        self.n_local = [int(v["n_local"]) for v in views]
+        self.dtype = self._descs[0].dtype
+        arr = (C.POINTER(h2_desc) * self.P)(*[C.pointer(ds.desc) for ds in self._descs])
+        hs = (C.c_void_p * self.P)()
+        _check(lib.h2_group_create(arr, self.P, int(nv_max), hs))
+        self.handles = hs
+        self.nv_max = int(nv_max)
+
+    def matvec(self, Xs, Ys, alpha=1.0, beta=0.0, stream=None):
+        """Ys[o] := alpha A Xs[o] + beta Ys[o]: CUDA tensors (nv, n_local[o]) of the handle dtype."""
+        import torch
+        want = torch.float64 if self.dtype == H2_F64 else torch.float32
+        nv = Xs[0].shape[0]
+        for o in range(self.P):
+            for a in (Xs[o], Ys[o]):
+                if not (a.is_cuda and a.dtype == want and a.is_contiguous() and tuple(a.shape) == (nv, self.n_local[o])):
+                    raise ValueError(f"rank {o}: X, Y must be contiguous CUDA {want} of shape (nv, {self.n_local[o]})")
+        st = stream if stream is not None else torch.cuda.current_stream(Xs[0].device)
+        _check(self._lib.h2_set_stream(self.handles[0], C.c_void_p(st.cuda_stream)))
+        xp = (C.c_void_p * self.P)(*[x.data_ptr() for x in Xs])
+        yp = (C.c_void_p * self.P)(*[y.data_ptr() for y in Ys])
+        _check(self._lib.h2_group_matvec(self.handles, self.P, float(alpha), xp, float(beta), yp, nv))
+        return Ys
+
+    def plan_counts(self, o):
+        c = (C.c_int64 * 8)()
+        _check(self._lib.h2_plan_counts(self.handles[o], c))
+        keys = ["diag_S", "offdiag_S", "root_S", "diag_D", "offdiag_D", "peers", "recv_nodes", "recv_leaves"]
+        return dict(zip(keys, list(c)))
+
+    def close(self):
+        if getattr(self, "handles", None) is not None:
+            for o in range(self.P):
+                if self.handles[o]:
+                    _check(self._lib.h2_destroy(self.handles[o]))
+                    self.handles[o] = None
+            self.handles = None
 
     def __del__(self):
         try:

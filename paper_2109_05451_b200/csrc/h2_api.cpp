@@ -1673,6 +1673,13 @@ extern "C" int h2_plan_census(const h2_desc *d, int level, int64_t *pid, int64_t
     }
 }
 
+extern "C" int h2_n_local(h2_handle h, int64_t *n_local)
+{
+    if (!h || !n_local) return fail(H2_ERR_ARG, "NULL argument");
+    *n_local = h->n_local;
+    return H2_OK;
+}
+
 extern "C" int h2_plan_counts(h2_handle h, int64_t counts[8])
 {
     if (!h || !counts) return fail(H2_ERR_ARG, "NULL argument");
@@ -1700,5 +1707,7 @@ extern "C" int h2_nccl_unique_id(void *out128)
 }
 
 extern "C" const char *h2_last_error(void) { return g_err.c_str(); }
+
+void h2::set_last_error(const std::string &msg) { g_err = msg; }
 
 extern "C" const char *h2_version(void) { return "h2-b200 0.1 (sm_100a)"; }

@@ -3,8 +3,12 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <string>
 
 namespace h2 {
+
+// message returned by h2_last_error() on this thread (h2_api.cpp)
+void set_last_error(const std::string &msg);
 
 constexpr int KMAX = 64;   // max rank k^l and leaf size m supported by the kernels
 constexpr int XLD = 64;    // leading dimension of a staged x operand in shared memory

@@ -5,7 +5,7 @@ l < C replicated, reading R16), and construction of the rank's H2Operator.
 Host-side marshalling only (slicing index ranges of the global arrays); no matvec arithmetic."""
 import numpy as np
 
-from ._binding import H2Operator
+from ._binding import H2Operator, H2Group
 
 
 def c_level(P):
@@ -92,3 +92,20 @@ def operator_from_h2data(h, rank=0, nranks=1, nccl_id=None, dtype="f64", nv_max=
     op = H2Operator(dtype=dtype, nv_max=nv_max, nccl_id=nccl_id, **kw)
     op.row_range = rows
     return op
+
+
+def group_from_h2data(h, P, dtype="f64", nv_max=16):
+    """Loopback group of P emulated ranks on the current GPU (tests): returns (H2Group, row
+    ranges).  Host arrays, copied by h2_group_create."""
+    npdt = np.float64 if dtype == "f64" else np.float32
+    cast = lambda a: None if a is None else np.ascontiguousarray(a, dtype=npdt)
+    views, rows = [], []
+    for o in range(P):
+        kw, rr = shard_arrays(h, o, P)
+        for key in ("U_leaf", "V_leaf", "D"):
+            kw[key] = cast(kw[key])
+        for key in ("E", "F", "S"):
+            kw[key] = [cast(a) for a in kw[key]]
+        views.append(kw)
+        rows.append(rr)
+    return H2Group(views, dtype=dtype, nv_max=nv_max), rows

@@ -20,6 +20,8 @@ def main():
     from h2gen import build_config, make_xy, build_cluster_tree, dual_traversal, random_h2_data
     from h2gen.tree import uniform_points
     from paper_2109_05451_b200.operator import operator_from_h2data
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from tests.gpu_util import with_root_coupling
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     lr = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(lr)
@@ -38,7 +40,8 @@ def main():
              ("rand-k36-nv3", rand(4000, 32, 36, 0.9, 6), 3, "f64"),
              ("rand-k25-nv20-chunks", rand(5000, 64, 25, 0.9, 8), 20, "f64"),
              ("rand-k16-fp32-nv5", rand(4000, 32, 16, 0.9, 9), 5, "f32"),
-             ("top-tree-eta3", rand(5000, 32, 16, 3.0, 7), 2, "f64")]
+             ("top-tree-eta3", rand(5000, 32, 16, 3.0, 7), 2, "f64"),
+             ("top-tree-root-block", with_root_coupling(rand(3000, 32, 12, 0.9, 12)), 4, "f64")]
     fails = 0
     for name, h, nv, dt in cases:
         if dt == "f32":
@@ -72,8 +75,12 @@ def main():
             fails += 0 if ok else 1
             print(f"[dist P={world}] {name}: rel err {err:.2e} offdiag_S={off} root_S(all ranks)={root} "
                   f"{'OK' if ok else 'FAIL'}", flush=True)
-            if name == "top-tree-eta3" and world > 1 and root == 0:
-                print("[dist] warning: top-tree case has no root-branch couplings", flush=True)
+            # eta = 3 has root-branch couplings only at P >= 4 (at P = 2 the top tree is the root
+            # alone); the root-block case has them at every P >= 2
+            if ((name == "top-tree-root-block" and world > 1) or (name == "top-tree-eta3" and world >= 4)) \
+                    and root == 0:
+                print(f"[dist] FAIL: {name} has no root-branch couplings at P={world}", flush=True)
+                fails += 1
         op.close()
     dist.barrier()
     dist.destroy_process_group()

@@ -28,3 +28,16 @@ def gpu_matvec(op, X, alpha, beta, Y0, dtype="f64"):
     op.matvec(Xd, Yd, alpha, beta)
     torch.cuda.synchronize()
     return Yd.double().cpu().numpy()
+
+
+def with_root_coupling(h, seed=77):
+    """The same H² data plus one coupling block at the root (level 0): a valid operator
+    A + U_0 S_00 V_0^T (the matvec does not need the partition property) whose top tree holds a
+    coupling at every P >= 2 -- at P = 2 the only level above the C-level is the root."""
+    import dataclasses
+    rng = np.random.default_rng(seed)
+    k0 = h.ranks[0]
+    Srp = [np.array([0, 1], dtype=np.int64)] + list(h.S_rowptr[1:])
+    Scol = [np.array([0], dtype=np.int32)] + list(h.S_col[1:])
+    S = [rng.uniform(-1.0, 1.0, size=(1, k0, k0)) / k0] + list(h.S[1:])
+    return dataclasses.replace(h, S_rowptr=Srp, S_col=Scol, S=S)
