@@ -311,6 +311,11 @@ struct h2_ctx {
     double ops_local = 0;            // stored operator scalars held by this rank
     int64_t counts[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int launches_per_call = 0;
+    // CTA-tile FP64 engine (h2_cta.cuh) for nv >= cta_min_nv (H2_ENGINE=warp: never, =cta: every nv)
+    int cta_min_nv = 16;
+    int nsm = 148;
+    bool use_cta(int nv) const { return dtype == H2_F64 && nv >= cta_min_nv; }
+    int launches_cta = 0;
 };
 
 namespace {
@@ -675,6 +680,12 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_leafc, cudaEventDisableTiming));
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
         H2_TRYC(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, dev);
+        const char *en = getenv("H2_ENGINE");
+        if (en && !strcmp(en, "warp")) h->cta_min_nv = 1 << 30;
+        else if (en && !strcmp(en, "cta")) h->cta_min_nv = 1;
     }
     // ---- operator arrays on the device; V and F re-laid out as V^T, F^T (operand order)
     const int kq = k[q];
@@ -1171,6 +1182,14 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         if (h->has_top) launches += (int)h->top_stages.size();
     }
     h->launches_per_call = launches;
+    // CTA engine: k_set_args, up_leaf, one launch per coupling class / transfer level, the leaves
+    h->launches_cta = 3 + (int)h->coup_leaf.size() + (int)h->up_lv.size() + (int)h->coup_diag.size() +
+                      (int)h->down_lv.size();
+    if (P > 1) {
+        h->launches_cta += 2;
+        for (int ci = 0; ci < 3; ++ci) h->launches_cta += h->coup_off[ci].n ? 1 : 0;
+        if (h->has_top) h->launches_cta += (int)h->top_stages.size();
+    }
     *out = h;
     return H2_OK;
 #undef H2_TRY
@@ -1229,6 +1248,28 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     // profiling (and loopback groups) serialize the side stream onto the main one so every
     // phase's events bracket only its own kernels (clean per-kernel durations for the roofline)
     cudaStream_t s_leafc = (h->prof || h->group) ? st : h->s_leafc;
+    // CTA-tile engine (FP64, nv >= cta_min_nv): the same tasks, one CTA per output node
+    const bool cta = h->use_cta(nv);
+    auto cjob = [&](const Phase &ph, int kind, int mode, const void *src, int64_t src_ld, void *dst,
+                    int64_t dst_ld) {
+        CtaJob j{};
+        j.tasks = T0(ph);
+        j.dtasks = nullptr;
+        j.blks = h->d_blks;
+        j.ntask = ph.n;
+        j.kind = kind;
+        j.mode = mode;
+        j.src = (const double *)src;
+        j.src_ld = src_ld;
+        j.dst = (double *)dst;
+        j.dst_ld = dst_ld;
+        j.yh = (const double *)yh;
+        j.yh_ld = h->yh_plane;
+        j.halo = (const double *)h->hrecv;
+        j.args = (const CallArgs<double> *)h->dargs;
+        j.nv = nv;
+        return j;
+    };
     if (part != PART_DOWN) {
     H2_MARK(0);
     // 0. x-leaf halo for the off-process dense blocks (P > 1): X is an input, so the exchange
@@ -1248,20 +1289,32 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
         H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_h0, h->nseg_h, (const T *)nullptr, 0, args, (T *)h->hsend, nv, st));
     }
     // 1. leaf projection (alg:upsweep2 line 3)
-    H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
-                                 h->up_leaf.r, st));
+    if (cta)
+        H2_CUDA(h, launch_cta(cjob(h->up_leaf, CK_UPLEAF, MODE_WRITE, nullptr, 0, xh, h->xh_plane), h->up_leaf.r,
+                              h->nsm, st));
+    else
+        H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
+                                     h->up_leaf.r, st));
     H2_MARK(1);
     // 1b. leaf-level coupling (diagonal part) as soon as x^ of the leaves exists (alg:mult's
     //     levels are independent), on its own stream
     H2_CUDA(h, cudaEventRecord(h->ev_upleaf, st));
     H2_CUDA(h, cudaStreamWaitEvent(s_leafc, h->ev_upleaf, 0));
-    for (const Phase &ph : h->coup_leaf)
-        H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
-                                  nv, ph.r, s_leafc));
+    for (const Phase &ph : h->coup_leaf) {
+        if (cta)
+            H2_CUDA(h, launch_cta(cjob(ph, CK_ROWS, MODE_WRITE, xh, h->xh_plane, yh, h->yh_plane), ph.r, h->nsm,
+                                  s_leafc));
+        else
+            H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
+                                      nv, ph.r, s_leafc));
+    }
     H2_CUDA(h, cudaEventRecord(h->ev_leafc, s_leafc));
     H2_MARK(2);
     // 1c. upsweep transfers of the local branch
-    if (h->use_sweep) {
+    if (cta) {
+        for (const Phase &ph : h->up_lv)
+            H2_CUDA(h, launch_cta(cjob(ph, CK_ROWS, MODE_WRITE, xh, h->xh_plane, xh, h->xh_plane), ph.r, h->nsm, st));
+    } else if (h->use_sweep) {
         for (size_t u = 0; u < h->up_sweeps.size(); ++u)
             H2_CUDA(h, launch_sweep<T>(MODE_WRITE, h->up_sweeps[u], h->up_sweep_ctas[u],
                                        h->up_sweep_ctas[u] == 1 && h->up_sweeps[u].nlev > 1 ? 512 : WPB * 32,
@@ -1307,9 +1360,13 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     }
     H2_MARK(4);
     // 3. coupling multiply, diagonal part of the levels above the leaves (alg:mult)
-    for (const Phase &ph : h->coup_diag)
-        H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
-                                  nv, ph.r, st));
+    for (const Phase &ph : h->coup_diag) {
+        if (cta)
+            H2_CUDA(h, launch_cta(cjob(ph, CK_ROWS, MODE_WRITE, xh, h->xh_plane, yh, h->yh_plane), ph.r, h->nsm, st));
+        else
+            H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
+                                      nv, ph.r, st));
+    }
     H2_MARK(5);
     // 4. off-diagonal part after the exchange (waitAll, alg:optimized_dist_mult line 11-12);
     //    it accumulates into leaf-level rows too, so the leaf coupling stream joins first
@@ -1318,13 +1375,19 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
         if (nccl) H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_recv, 0));
         for (int ci = 0; ci < 3; ++ci) {
             const Phase &ph = h->coup_off[ci];
-            H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(ph), ph.n, h->d_blks, (const T *)h->xrecv, 0, yh,
-                                      h->yh_plane, nv, ph.r, st));
+            if (cta)
+                H2_CUDA(h, launch_cta(cjob(ph, CK_ROWS, MODE_ACCUM, h->xrecv, 0, yh, h->yh_plane), ph.r, h->nsm, st));
+            else
+                H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(ph), ph.n, h->d_blks, (const T *)h->xrecv, 0, yh,
+                                          h->yh_plane, nv, ph.r, st));
         }
     }
     H2_MARK(6);
     // 5. downsweep transfers (alg:downsweep)
-    if (h->use_sweep) {
+    if (cta) {
+        for (const Phase &ph : h->down_lv)
+            H2_CUDA(h, launch_cta(cjob(ph, CK_ROWS, MODE_ACCUM, yh, h->yh_plane, yh, h->yh_plane), ph.r, h->nsm, st));
+    } else if (h->use_sweep) {
         for (size_t u = 0; u < h->dn_sweeps.size(); ++u)
             H2_CUDA(h, launch_sweep<T>(MODE_ACCUM, h->dn_sweeps[u], h->dn_sweep_ctas[u],
                                        h->dn_sweep_ctas[u] == 1 && h->dn_sweeps[u].nlev > 1 ? 512 : WPB * 32,
@@ -1341,8 +1404,14 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_leafc, 0));
     H2_MARK(8);
     const int kq = L.k[q], kp = q >= 1 ? L.k[q - 1] : 1;
-    H2_CUDA(h, launch_leaf_dense<T>(T0(h->leaf), T0(h->dense), h->leaf.n, h->d_blks, yh, h->yh_plane, args,
-                                    (const T *)h->hrecv, nv, kq, kp, h->leaf.r, st));
+    if (cta) {
+        CtaJob j = cjob(h->leaf, CK_LEAF, MODE_WRITE, nullptr, 0, nullptr, 0);
+        j.dtasks = T0(h->dense);
+        H2_CUDA(h, launch_cta(j, std::max(h->leaf.r, kq), h->nsm, st));
+    } else {
+        H2_CUDA(h, launch_leaf_dense<T>(T0(h->leaf), T0(h->dense), h->leaf.n, h->d_blks, yh, h->yh_plane, args,
+                                        (const T *)h->hrecv, nv, kq, kp, h->leaf.r, st));
+    }
     H2_MARK(9);
     if (h->prof) h->ev_used += NEV;
 #undef H2_MARK
@@ -1580,7 +1649,7 @@ extern "C" int h2_stats(h2_handle h, int nv, double *flops, double *bytes, doubl
         for (const auto &pr : h->peers) x += (double)(pr.xr_cnt + pr.hr_cnt) * nv * h->esz;
         *xchg_bytes = x;
     }
-    if (launches) *launches = h->launches_per_call;
+    if (launches) *launches = h->use_cta(nv) ? h->launches_cta : h->launches_per_call;
     return H2_OK;
 }
 

@@ -122,4 +122,26 @@ struct SweepParams {
 template <typename T>
 cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads, T *buf, int64_t ld, int nv,
                          int r, cudaStream_t s);
+
+// CTA-tile FP64 engine (h2_cta.cuh): one output node per CTA at a time, every block staged once
+// in shared memory for all the CTA's warps.
+enum { CK_ROWS = 0, CK_UPLEAF = 1, CK_LEAF = 2 };
+struct CtaJob {
+    const Task *tasks;       // primary tasks (rows / leaf projections / leaves [E][U])
+    const Task *dtasks;      // CK_LEAF: dense row of the same leaf
+    const Blk *blks;
+    int ntask;
+    int kind, mode;          // CK_*, MODE_WRITE / MODE_ACCUM (CK_ROWS)
+    const double *src;       // CK_ROWS: x^ / y^ source plane (element offsets in Blk::x)
+    int64_t src_ld;
+    double *dst;             // CK_ROWS / CK_UPLEAF: output plane
+    int64_t dst_ld;
+    const double *yh;        // CK_LEAF: y^ plane (E's parent operand, z's own part)
+    int64_t yh_ld;
+    const double *halo;      // x rows received from peers (Blk::x < 0)
+    const CallArgs<double> *args;
+    int nv;
+};
+// rmax: the widest output tile of the job's tasks; nsm: SMs (grid = min(ntask, nsm))
+cudaError_t launch_cta(const CtaJob &j, int rmax, int nsm, cudaStream_t s);
 }  // namespace h2

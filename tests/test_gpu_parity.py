@@ -180,3 +180,21 @@ def test_cfg3s_full_size_sampled():
     ref = oracle.matvec(h, X, 1.0, 0.0, None, leaf_mask=mask)
     rows = np.concatenate([np.arange(h.leaf_ptr[i], h.leaf_ptr[i + 1]) for i in np.flatnonzero(mask)])
     assert colmax_rel(out[:, rows], ref[:, rows]) <= TOL64
+
+
+@pytest.mark.parametrize("engine", ["warp", "cta"])
+@pytest.mark.parametrize("N,m,k,nv,eta,seed", [
+    (3000, 32, 16, 1, 0.9, 51), (3000, 32, 25, 3, 0.9, 52), (5000, 64, 25, 8, 0.9, 53),
+    (5000, 64, 25, 16, 0.9, 54), (4000, 64, 36, 17, 0.9, 55), (4000, 64, 64, 33, 1.1, 56),
+    (4000, 64, 64, 64, 1.1, 57), (2500, 48, 40, 20, 0.9, 58)])
+def test_engines(engine, N, m, k, nv, eta, seed, monkeypatch):
+    """Both FP64 engines on every shape class: the warp-task engine (H2_ENGINE=warp) and the
+    CTA-tile engine (H2_ENGINE=cta: every block staged once in shared memory for all warps of
+    the CTA), odd / even k, ragged leaves, nv inside and across the 16-vector chunks."""
+    monkeypatch.setenv("H2_ENGINE", engine)
+    h = random_case(N, m, lambda l: k, seed, eta=eta)
+    X = make_xy(h.perm, nv, seed, -1.0, 1.0)
+    Y0 = make_xy(h.perm, nv, seed + 1, -1.0, 1.0, stream=1)
+    out = gpu_matvec(_op(h, nv_max=max(nv, 16)), X, -0.6, 1.3, Y0)
+    ref = oracle.matvec(h, X, -0.6, 1.3, Y0)
+    assert colmax_rel(out, ref) <= TOL64
