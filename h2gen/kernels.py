@@ -54,11 +54,15 @@ def _r2(x, y):
     return r2
 
 
-def fd_kappa(x):
-    """Diffusivity field: kappa = 1 + f with a smooth bump f peaking at e^-1 (PAPER.md:762-765,
-    reading R10); kappa in [1, 1 + e^-1]."""
-    r2 = np.sum(x * x, axis=-1)
-    inside = r2 < 0.25
+def fd_bump(x, c, ell):
+    """f(x; c, l) = exp(-1 / (1 - r^2)) for |r| < 1, r = (x - c) / (l / 2); 0 otherwise."""
+    r = (np.asarray(x, dtype=np.float64) - c) / (0.5 * ell)
+    inside = np.abs(r) < 1.0
     with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
-        f = np.where(inside, np.exp(-1.0 / np.maximum(1e-300, 1.0 - 4.0 * r2)), 0.0)
-    return 1.0 + f
+        return np.where(inside, np.exp(-1.0 / np.maximum(1e-300, 1.0 - r * r)), 0.0)
+
+
+def fd_kappa(x):
+    """Diffusivity kappa(x) = 1 + f(x_1; 0, 1.5) f(x_2; 0, 2.0) (PAPER.md:728-737, reading R10);
+    kappa in [1, 1 + e^-2]."""
+    return 1.0 + fd_bump(x[..., 0], 0.0, 1.5) * fd_bump(x[..., 1], 0.0, 2.0)

@@ -99,3 +99,19 @@ def test_flop_convention_matches_paper(golden):
     per_pt = 2 * ops / N
     ref = golden["flop_per_point_per_vector_paper"]["value"]
     assert abs(per_pt - ref) / ref < 0.015
+
+
+def test_fd_kernel_and_diffusivity():
+    """FD operator (reading R10): K_ij = -2 a(x_i, x_j) / |x_j - x_i|^(2+2beta),
+    K_ii = 0, a = sqrt(kappa_i kappa_j), kappa = 1 + f(x1; 0, 1.5) f(x2; 0, 2.0)."""
+    import numpy as np
+    from h2gen.kernels import Kernel, fd_kappa
+    k = Kernel("fd", beta=0.75)
+    x = np.array([[0.9, 0.9], [0.9, -0.1], [0.0, 0.0]])
+    assert np.isclose(fd_kappa(x[:1])[0], 1.0) and np.isclose(fd_kappa(x[2:])[0], 1.0 + np.exp(-2.0))
+    K = k(x[:, None, :], x[None, :, :])
+    assert K[0, 1] == -2.0                          # kappa = 1 at both, distance 1
+    assert np.all(np.diag(K) == 0.0)
+    r = np.linalg.norm(x[0] - x[2])
+    assert np.isclose(K[0, 2], -2.0 * np.sqrt(1.0 + np.exp(-2.0)) / r ** 3.5)
+    assert np.allclose(K, K.T)
