@@ -16,6 +16,7 @@ class Kernel:
     ell: float = 0.1
     p: int = 4                 # poly: order (degree p-1)
     beta: float = 0.75         # fd
+    sign: float = -1.0         # fd: -1 for K, +1 for K^ (the D assembly)
     params: dict = field(default_factory=dict)
 
     def __call__(self, x, y):
@@ -38,7 +39,7 @@ class Kernel:
             kx = fd_kappa(x)
             ky = fd_kappa(y)
             with np.errstate(divide="ignore", invalid="ignore"):
-                v = -2.0 * np.sqrt(kx * ky) / r2 ** (1.0 + self.beta)
+                v = 2.0 * self.sign * np.sqrt(kx * ky) / r2 ** (1.0 + self.beta)
             return np.where(r2 > 0, v, 0.0)
         if self.name == "zero":
             return np.zeros(np.broadcast_shapes(x.shape, y.shape)[:-1])

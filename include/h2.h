@@ -190,6 +190,24 @@ int h2_create_from_file(const char *path, int rank, int nranks, int nv_max, cons
 /* Loopback-group form (tests): all P ranks' views read from the file, then h2_group_create. */
 int h2_group_create_from_file(const char *path, int P, int nv_max, h2_handle *out);
 
+/* ---- Fractional-diffusion solve ------------------
+ * The system h^2 (D + K + C) u = b of the paper's application, with K the H² operator of handle K
+ * (n = its n_local rows, tree order, FP64, one rank), D diagonal, C sparse.  All device memory,
+ * FP64, synchronous (legacy stream).
+ * h2_fd_diag: diag[i] = (K^ 1)[idx[i]] + cdiag[i] (cdiag may be NULL) for i < n: D from one H²
+ *   matvec of the extended-grid operator K^ (handle khat, "recast as the product
+ *   K^ 1") with the ones vector, gathered at the interior points' rows idx (tree order of K^).
+ * h2_pcg: preconditioned conjugate gradients on A u = scale (diag u + K u + C' u)
+ *   = b, C' = C without its diagonal (CSR C_rowptr [n+1], C_col [nnz] (tree-order columns),
+ *   C_val; diagonal entries are skipped -- fold them into diag), Jacobi preconditioner
+ *   scale * diag.  u: initial guess in, solution out.  Stops when ||b - A u|| <= rtol ||b|| or
+ *   after maxit iterations; *iters = iterations done; res_hist[0..*iters] (host, may be NULL) =
+ *   the relative residual norms.  H2_ERR_ARG for NULL / bad sizes. */
+int h2_fd_diag(h2_handle khat, const int64_t *idx, const double *cdiag, int64_t n, double *diag);
+int h2_pcg(h2_handle K, double scale, const double *diag, const int64_t *C_rowptr, const int32_t *C_col,
+           const double *C_val, const double *b, double *u, double rtol, int maxit, int *iters,
+           double *res_hist);
+
 /* Release device memory, the NCCL communicator and streams.  NULL is a no-op. */
 int h2_destroy(h2_handle h);
 

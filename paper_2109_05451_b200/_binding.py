@@ -15,7 +15,7 @@ H2_F64, H2_F32 = 0, 1
 H2_MEM_HOST, H2_MEM_DEVICE = 0, 1
 
 EXPORTS = ["h2_create", "h2_matvec", "h2_matvec_ld", "h2_matvec_host", "h2_set_stream", "h2_stats",
-           "h2_group_create", "h2_group_matvec", "h2_file_info", "h2_create_from_file", "h2_group_create_from_file", "h2_n_local",
+           "h2_group_create", "h2_group_matvec", "h2_file_info", "h2_create_from_file", "h2_group_create_from_file", "h2_n_local", "h2_fd_diag", "h2_pcg",
            "h2_set_profiling", "h2_phase_times", "h2_phase_stats",
            "h2_plan_counts", "h2_plan_census", "h2_destroy", "h2_nccl_unique_id", "h2_last_error", "h2_version"]
 PHASES = ["up_leaf", "up_transfer", "exchange_top", "coupling_diag", "coupling_offdiag",

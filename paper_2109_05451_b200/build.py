@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libh2b200.so")
 SOURCES = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.startswith("h2_k_") and f.endswith(".cu")) + \
-    [os.path.join(CSRC, "h2_api.cpp"), os.path.join(CSRC, "h2_file.cpp")]
+    [os.path.join(CSRC, "h2_api.cpp"), os.path.join(CSRC, "h2_file.cpp"), os.path.join(CSRC, "h2_solver.cu")]
 DEPS = SOURCES + sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))) + \
     [os.path.join(ROOT, "include", "h2.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

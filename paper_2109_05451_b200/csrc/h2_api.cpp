@@ -311,8 +311,9 @@ struct h2_ctx {
     double ops_local = 0;            // stored operator scalars held by this rank
     int64_t counts[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int launches_per_call = 0;
-    // CTA-tile FP64 engine (h2_cta.cuh) for nv >= cta_min_nv (H2_ENGINE=warp: never, =cta: every nv)
-    int cta_min_nv = 16;
+    // CTA-tile FP64 engine (h2_cta.cuh) for nv >= cta_min_nv (H2_ENGINE=warp: never, =cta: every nv);
+    // measured: faster than the warp engine at nv = 64 (cfg3), slower at nv <= 16 (cfg2, cfg5)
+    int cta_min_nv = 17;
     int nsm = 148;
     bool use_cta(int nv) const { return dtype == H2_F64 && nv >= cta_min_nv; }
     int launches_cta = 0;

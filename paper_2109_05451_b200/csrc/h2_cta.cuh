@@ -178,12 +178,12 @@ __device__ __forceinline__ void issue(const Step &st, double *As, double *Xs, in
 
 }  // namespace cta
 
-// NS-stage ring, WR x WC consumer warps (MT m-tiles x 2 n-tiles each) + 1 producer warp.
-template <int MT, int WR, int WC, int NS>
+// NS-stage ring, WR x WC consumer warps (MT m-tiles x NT n-tiles each) + 1 producer warp.
+template <int MT, int NT, int WR, int WC, int NS>
 __global__ void __launch_bounds__((WR * WC + 1) * 32, 1) k_cta(const __grid_constant__ CtaJob j)
 {
     using namespace cta;
-    constexpr int NW = WR * WC, NVT = 16 * WC, NT = 2;
+    constexpr int NW = WR * WC, NVT = 8 * NT * WC;
     constexpr int AEL = CMAX * LDM, XEL = NVT * LDM, STAGE = AEL + XEL;
     extern __shared__ __align__(128) double sm[];
     Meta *meta = reinterpret_cast<Meta *>(sm + NS * STAGE);
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__((WR * WC + 1) * 32, 1) k_cta(const __grid_cons
     // ==================================================================== consumer warps
     const int wr = wid % WR, wc = wid / WR;
     const int g = lane >> 2, t4 = lane & 3;
-    const int row0 = wr * 8 * MT, col0 = wc * 16;
+    const int row0 = wr * 8 * MT, col0 = wc * 8 * NT;
     const bool active = col0 < nv;
     double acc[MT][NT][2];
     auto each = [&](auto f) {
@@ -388,11 +388,12 @@ cudaError_t launch_cta(const CtaJob &j, int rmax, int nsm, cudaStream_t s)
     };
     const bool big = rmax > 32;
     if (j.nv <= 16) {
-        if (big) go(k_cta<2, 4, 1, 4>, 4, 16, 4); else go(k_cta<1, 4, 1, 4>, 4, 16, 4);
+        if (big) go(k_cta<2, 2, 4, 1, 4>, 4, 16, 4); else go(k_cta<1, 2, 4, 1, 4>, 4, 16, 4);
     } else if (j.nv <= 32) {
-        if (big) go(k_cta<2, 4, 2, 3>, 8, 32, 3); else go(k_cta<1, 4, 2, 3>, 8, 32, 3);
+        if (big) go(k_cta<2, 2, 4, 2, 3>, 8, 32, 3); else go(k_cta<1, 2, 4, 2, 3>, 8, 32, 3);
     } else {
-        if (big) go(k_cta<4, 2, 4, 3>, 8, 64, 3); else go(k_cta<2, 2, 4, 3>, 8, 64, 3);
+        // (MT, NT) = (4, 4) on 2 x 2 warps and (2, 4) on 4 x 2 warps measured 12 % / 0 % slower on cfg3
+        if (big) go(k_cta<4, 2, 2, 4, 3>, 8, 64, 3); else go(k_cta<2, 2, 2, 4, 3>, 8, 64, 3);
     }
     return err;
 }
