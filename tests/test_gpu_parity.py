@@ -198,3 +198,27 @@ def test_engines(engine, N, m, k, nv, eta, seed, monkeypatch):
     out = gpu_matvec(_op(h, nv_max=max(nv, 16)), X, -0.6, 1.3, Y0)
     ref = oracle.matvec(h, X, -0.6, 1.3, Y0)
     assert colmax_rel(out, ref) <= TOL64
+
+
+def test_matvec_ld_larger_leading_dimensions():
+    """h2_matvec_ld with ldx, ldy > n_local (include/h2.h): columns strided inside larger buffers;
+    the padding between columns is neither read into the result nor written."""
+    import torch
+    h = random_case(3000, 32, lambda l: 12, 71)
+    op = _op(h, nv_max=5)
+    nv, N = 5, h.N
+    ldx, ldy = N + 37, N + 64
+    X = make_xy(h.perm, nv, 7, -1.0, 1.0)
+    Y0 = make_xy(h.perm, nv, 8, -1.0, 1.0, stream=1)
+    Xb = torch.full((nv * ldx,), float("nan"), dtype=torch.float64, device="cuda")
+    Yb = torch.full((nv * ldy,), 123.0, dtype=torch.float64, device="cuda")
+    for c in range(nv):
+        Xb[c * ldx:c * ldx + N] = torch.from_numpy(X[c])
+        Yb[c * ldy:c * ldy + N] = torch.from_numpy(Y0[c])
+    op.matvec_ld(Xb, ldx, Yb, ldy, nv, -0.5, 0.25)
+    torch.cuda.synchronize()
+    Yh = Yb.cpu().numpy()
+    out = np.stack([Yh[c * ldy:c * ldy + N] for c in range(nv)])
+    assert colmax_rel(out, oracle.matvec(h, X, -0.5, 0.25, Y0)) <= TOL64
+    pad = np.concatenate([Yh[c * ldy + N:(c + 1) * ldy] for c in range(nv)])
+    assert np.all(pad == 123.0)
