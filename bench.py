@@ -34,8 +34,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "H2 matvec GFLOP/s per GPU and ms/matvec (nv=1,16,64) at 1/2/4/8 B200"
+# a workload name with ":sym" = the same workload on the symmetric-storage path (H2_SYMMETRIC,
+# nv = 1 legs only: SURVEY.md §8(f) NEXT-2)
 SUITES = {
-    "suite": (["cfg2"], ["cfg3", "cfg1"]),
+    "suite": (["cfg2"], ["cfg3", "cfg2:sym", "cfg1"]),
+    "cfg2sym": (["cfg2:sym"], []), "cfg4sym": (["cfg4:sym"], []),
     "cfg1": (["cfg1"], []), "cfg2": (["cfg2"], []), "cfg3": (["cfg3"], []), "cfg3s": (["cfg3s"], []),
     "cfg4": (["cfg4"], []), "cfg5": (["cfg5"], []),
 }
@@ -125,9 +128,13 @@ def dist_env():
 
 
 def legs_of(name):
-    """[(config, dtype, nvs)] of one workload (cfg5: one leg per precision)."""
+    """[(config, dtype, nvs)] of one workload (cfg5: one leg per precision; "name:sym": the
+    symmetric-storage path, nv = 1 only)."""
     from h2gen.configs import CONFIGS
-    c = CONFIGS[name]
+    base, _, opt = name.partition(":")
+    c = CONFIGS[base]
+    if opt == "sym":
+        return [(name, dt, (1,)) for dt in c["dtypes"]]
     return [(name, dt, tuple(c["nvs"])) for dt in c["dtypes"]]
 
 
@@ -136,11 +143,15 @@ def leg_key(leg):
     return f"{name}/{dt}/nv={'+'.join(map(str, nvs))}"
 
 
+def base_name(name):
+    return name.partition(":")[0]
+
+
 def config_dict(args, P, legs_primary, legs_extra, N_global, n_local):
     from h2gen.configs import CONFIGS
-    prim = legs_primary[0][0]
+    prim = base_name(legs_primary[0][0])
     scal = CONFIGS[prim]["scaling"]
-    return {"workload": "; ".join(f"{leg_key(lg)}: {CONFIGS[lg[0]]['desc']}" for lg in legs_primary),
+    return {"workload": "; ".join(f"{leg_key(lg)}: {CONFIGS[base_name(lg[0])]['desc']}" for lg in legs_primary),
             "extra_legs": [leg_key(lg) for lg in legs_extra],
             "N_global": N_global, "N_per_gpu": n_local,
             "parallelism": f"block rows x{P} ({scal} scaling)" if P > 1 else "single GPU",
@@ -156,7 +167,7 @@ def build_leg_problem(name, P, rank, with_global):
     from h2gen.configs import build_structure
     from h2gen.h2data import build_h2
     from h2gen.shard import build_h2_shard
-    tree, st, kern, c = build_structure(name, P)
+    tree, st, kern, c = build_structure(base_name(name), P)
     if with_global or P == 1:
         from paper_2109_05451_b200.operator import shard_arrays
         h = build_h2(tree, st, kern, c["p"])
@@ -259,7 +270,7 @@ def run_reference(args, emit):
     val = flops_step / sec / 1e9
     from h2gen.configs import CONFIGS
     P = ws
-    n_first = int(parts[0][0].N) if CONFIGS[legs[0][0]]["scaling"] == "weak" else int(parts[0][0].N)
+    n_first = int(parts[0][0].N)
     # per-GPU rows of rank 0 = its branch at the C-level (the same rows the GPU arm reports)
     C = P.bit_length() - 1
     lp = np.asarray(parts[0][0].leaf_ptr)
@@ -267,7 +278,7 @@ def run_reference(args, emit):
     ours_cfg = config_dict(args, ws, legs, [lg for nm in extra for lg in legs_of(nm)], n_first, n_rank0)
     out = {"metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-           "scaling": CONFIGS[legs[0][0]]["scaling"], "vs_baseline": None, "dtype": legs[0][1], "data": "synthetic",
+           "scaling": CONFIGS[base_name(legs[0][0])]["scaling"], "vs_baseline": None, "dtype": legs[0][1], "data": "synthetic",
            "config": ours_cfg, "impl": "reference",
            "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
                             "sample": "; ".join(sample) + "; time scaled by the work fraction"},
@@ -286,7 +297,11 @@ def run_leg(leg, args, P, rank, dev, pkg, torch, dist, want_cpu, samplers, laten
     if P > 1:
         from paper_2109_05451_b200.operator import broadcast_nccl_id
         nccl_id = broadcast_nccl_id(dev)
-    op = pkg.H2Operator(dtype=dtype, nv_max=max(nvs), nccl_id=nccl_id, **cast_kw(kw, dtype))
+    sym = name.endswith(":sym")
+    kw = cast_kw(kw, dtype)
+    if sym:                                   # H2_SYMMETRIC: U = V and E = F as one array each
+        kw = dict(kw, V_leaf=kw["U_leaf"], F=kw["E"])
+    op = pkg.H2Operator(dtype=dtype, nv_max=max(nvs), nccl_id=nccl_id, symmetric=sym, **kw)
     del kw
     n_local = int(op.n_local)
     perm_local = tree.perm[r0:r1]
@@ -511,7 +526,7 @@ def main():
         from h2gen.configs import CONFIGS
         out = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": P, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-               "scaling": CONFIGS[legs_p[0][0]]["scaling"], "vs_baseline": None, "dtype": legs_p[0][1],
+               "scaling": CONFIGS[base_name(legs_p[0][0])]["scaling"], "vs_baseline": None, "dtype": legs_p[0][1],
                "data": "synthetic",
                "config": config_dict(args, P, legs_p, legs_x, res_p[0]["N_global"], res_p[0]["N_per_gpu"]),
                "per_nv": per_nv, "roofline": dom["roofline"], "e2e": e2e, "cpu_baseline": cpu,

@@ -78,7 +78,19 @@ typedef struct {
     const int64_t *D_rowptr;     /* [2^(q-C) + 1] dense block rows of my leaves */
     const int32_t *D_col;        /* GLOBAL leaf index (may be remote)                          */
     const void *D;               /* per block m x m col-major, zero-padded                     */
+    int32_t flags;               /* H2_SYMMETRIC or 0 (see below)                              */
 } h2_desc;
+
+/* h2_desc.flags.  H2_SYMMETRIC: the caller asserts the operator is symmetric with a symmetric block
+ * structure -- U = V (V_leaf must be the same array as U_leaf), E = F, S^l_st = (S^l_ts)^T and
+ * D_st = (D_ts)^T -- and the library stores only the blocks (t, s) with t <= s, applying each
+ * stored off-diagonal block also transposed (y_s += A_ts^T x_t) from the same read: about half the
+ * coupling and dense bytes per matvec (a representation change outside
+ * the paper).  Supported for nv_max == 1 and nranks == 1 (H2_ERR_ARG otherwise);
+ * results are order-dependent in the last bits (atomic accumulation).  The flop model
+ * (h2_stats) keeps the paper's convention over the full operator; the byte model counts what is
+ * stored. */
+enum { H2_SYMMETRIC = 1 };
 
 typedef struct h2_ctx *h2_handle;
 

@@ -13,6 +13,7 @@ H2_OK, H2_ERR_ARG, H2_ERR_SHAPE, H2_ERR_STRUCT, H2_ERR_CUDA, H2_ERR_NCCL, H2_ERR
     0, -1, -2, -3, -4, -5, -6, -7
 H2_F64, H2_F32 = 0, 1
 H2_MEM_HOST, H2_MEM_DEVICE = 0, 1
+H2_SYMMETRIC = 1
 
 EXPORTS = ["h2_create", "h2_matvec", "h2_matvec_ld", "h2_matvec_host", "h2_set_stream", "h2_stats",
            "h2_group_create", "h2_group_matvec", "h2_file_info", "h2_create_from_file", "h2_group_create_from_file", "h2_n_local", "h2_fd_diag", "h2_pcg",
@@ -42,6 +43,7 @@ class h2_desc(C.Structure):
         ("E", C.c_void_p), ("F", C.c_void_p),
         ("S_rowptr", C.c_void_p), ("S_col", C.c_void_p), ("S", C.c_void_p),
         ("D_rowptr", C.c_void_p), ("D_col", C.c_void_p), ("D", C.c_void_p),
+        ("flags", C.c_int32),
     ]
 
 
@@ -109,7 +111,7 @@ class _Desc:
     """Marshals one rank's arrays into an h2_desc (keeps the buffers alive)."""
 
     def __init__(self, *, depth, leaf_size, level_rank, leaf_ptr, U_leaf, V_leaf, E, F, S_rowptr,
-                 S_col, S, D_rowptr, D_col, D, n_local, rank=0, nranks=1, dtype="f64"):
+                 S_col, S, D_rowptr, D_col, D, n_local, rank=0, nranks=1, dtype="f64", symmetric=False):
         self.dtype = {"f64": H2_F64, "f32": H2_F32}[dtype]
         self.np_dtype = np.float64 if self.dtype == H2_F64 else np.float32
         fl = [U_leaf, V_leaf, D] + [a for a in list(E) + list(F) + list(S) if a is not None]
@@ -157,6 +159,7 @@ class _Desc:
                                     C.cast(self.S, C.c_void_p))
         d.D_rowptr, d.D_col = iptr(D_rowptr, np.int64), iptr(D_col, np.int32)
         d.D = fptr(D)
+        d.flags = H2_SYMMETRIC if symmetric else 0
         self.desc = d
 
 

@@ -251,6 +251,8 @@ struct h2_ctx {
     int64_t n_local = 0, nleaf = 0;
     bool sticky = false;
     h2_group *group = nullptr;       // loopback group (tests) or nullptr (NCCL / single rank)
+    bool sym = false;                // symmetric storage (h2_desc.flags & H2_SYMMETRIC; NEXT-2)
+    double ops_stored = 0;           // operator scalars actually stored (bytes model)
     bool has_top = false;            // P > 1 and the top tree (levels < C) holds couplings
     cudaStream_t stream = nullptr;   // caller's stream (default legacy)
     cudaStream_t s_comm = nullptr;
@@ -394,6 +396,28 @@ int put_array(h2_ctx *h, int mem, const void *src, int64_t n, const void **out)
     if (!p) return cuda_fail(h, err, "cudaMalloc(operator)");
     H2_CUDA(h, cudaMemcpy(p, src, (size_t)n * h->esz, cudaMemcpyHostToDevice));
     *out = p;
+    return H2_OK;
+}
+
+// Device copy of the blocks kept[0..] (original block indices, ascending) of an array of blocks of
+// `per` elements, compacted in that order (symmetric storage); runs of consecutive blocks are copied
+// at once.
+int put_gathered(h2_ctx *h, int mem, const void *src, const std::vector<int64_t> &kept, int64_t per, const void **out)
+{
+    if (kept.empty()) { *out = nullptr; return H2_OK; }
+    cudaError_t err;
+    void *dst = dalloc(h, (size_t)kept.size() * per * h->esz, err);
+    if (!dst) return cuda_fail(h, err, "cudaMalloc(symmetric blocks)");
+    const cudaMemcpyKind kind = mem == H2_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    const size_t bb = (size_t)per * h->esz;
+    size_t i = 0;
+    while (i < kept.size()) {
+        size_t j = i + 1;
+        while (j < kept.size() && kept[j] == kept[j - 1] + 1) ++j;
+        H2_CUDA(h, cudaMemcpy((char *)dst + i * bb, (const char *)src + (size_t)kept[i] * bb, (j - i) * bb, kind));
+        i = j;
+    }
+    *out = dst;
     return H2_OK;
 }
 
@@ -618,6 +642,11 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     h->n_local = d->n_local;
     h->nleaf = L.held(L.q);
     h->group = grp;
+    h->sym = (d->flags & H2_SYMMETRIC) != 0;
+    if (h->sym && (nv_max != 1 || L.P != 1 || d->U_leaf != d->V_leaf)) {
+        delete h;
+        return fail(H2_ERR_ARG, "H2_SYMMETRIC needs nv_max == 1, one rank and V_leaf == U_leaf (same array)");
+    }
     const int q = L.q, m = L.m, p = L.p, P = L.P, C = L.C;
     const std::vector<int> &k = L.k;
     const int64_t nleaf = h->nleaf;
@@ -701,15 +730,44 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         H2_TRY(put_transposed(h, d->mem, d->F[l], L.held(l), k[l], k[l - 1], &h->Ft[l]));
         ops += 2.0 * L.held(l) * k[l] * k[l - 1];
     }
+    // symmetric storage: only the blocks (t, s) with s >= t are kept (compacted, CSR order);
+    // cidx maps an original block to its compact index (-1: dropped, applied as a transpose)
+    std::vector<std::vector<int64_t>> cidxS(q + 1);
+    std::vector<int64_t> cidxD;
+    double ops_stored = ops;
+    auto keep_list = [&](const int64_t *rp, const int32_t *col, int64_t rows, std::vector<int64_t> &cidx,
+                         std::vector<int64_t> &kept) {
+        cidx.assign(rp[rows], -1);
+        for (int64_t t = 0; t < rows; ++t)
+            for (int64_t b = rp[t]; b < rp[t + 1]; ++b)
+                if (col[b] >= t) { cidx[b] = (int64_t)kept.size(); kept.push_back(b); }
+    };
     for (int l = 0; l <= q; ++l) {
         int64_t nb = d->S_rowptr[l][L.held(l)];
-        H2_TRY(put_array(h, d->mem, d->S[l], nb * k[l] * k[l], &h->S[l]));
         ops += (double)nb * k[l] * k[l];
+        if (h->sym) {
+            std::vector<int64_t> kept;
+            keep_list(d->S_rowptr[l], d->S_col[l], L.held(l), cidxS[l], kept);
+            H2_TRY(put_gathered(h, d->mem, d->S[l], kept, (int64_t)k[l] * k[l], &h->S[l]));
+            ops_stored += (double)kept.size() * k[l] * k[l];
+        } else {
+            H2_TRY(put_array(h, d->mem, d->S[l], nb * k[l] * k[l], &h->S[l]));
+            ops_stored += (double)nb * k[l] * k[l];
+        }
     }
     const int64_t nD = d->D_rowptr[nleaf];
-    H2_TRY(put_array(h, d->mem, d->D, nD * m * m, &h->D));
     ops += (double)nD * m * m;
-    h->ops_local = ops;
+    if (h->sym) {
+        std::vector<int64_t> kept;
+        keep_list(d->D_rowptr, d->D_col, nleaf, cidxD, kept);
+        H2_TRY(put_gathered(h, d->mem, d->D, kept, (int64_t)m * m, &h->D));
+        ops_stored += (double)kept.size() * m * m;
+    } else {
+        H2_TRY(put_array(h, d->mem, d->D, nD * m * m, &h->D));
+        ops_stored += (double)nD * m * m;
+    }
+    h->ops_local = ops;          // flop model: the operator as described (paper convention)
+    h->ops_stored = ops_stored;  // bytes model: what is stored and streamed
     {
         // per-phase operator scalars and vector elements (per vector), DESIGN.md "Measurement"
         double Fops = 0, Eops_mid = 0, tree_up = 0, tree_mid = 0;
@@ -726,6 +784,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         for (int l = 0; l <= q; ++l)
             for (int64_t i = 0; i < L.held(l); ++i)
                 for (int64_t b = d->S_rowptr[l][i]; b < d->S_rowptr[l][i + 1]; ++b) {
+                    if (h->sym && d->S_col[l][b] < L.g0(l) + i) continue;   // not stored
                     int o = L.owner(l, d->S_col[l][b]);
                     double e = (double)k[l] * k[l];
                     if (o >= 0 && o != p) So += e;
@@ -745,7 +804,8 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         h->ph_vec[5] = tree_mid;
         h->ph_ops[6] = (q >= 1 ? (double)nleaf * kq * k[q - 1] : 0.0) + (double)nleaf * m * kq;
         h->ph_vec[6] = (double)nleaf * kq + (q >= 1 ? (double)L.held(q - 1) * k[q - 1] : 0.0) + 2.0 * d->n_local;
-        h->ph_ops[7] = (double)nD * m * m;
+        h->ph_ops[7] = h->sym ? (double)cidxD.size() - (double)std::count(cidxD.begin(), cidxD.end(), -1) : (double)nD;
+        h->ph_ops[7] *= (double)m * m;
         h->ph_vec[7] = 2.0 * d->n_local;   // X read (once), Y write
     }
 
@@ -936,9 +996,11 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
                 for (int64_t b = rp[i]; b < rp[i + 1]; ++b) {
                     int64_t s = d->S_col[l][b];
                     int o = L.owner(l, s);
-                    const void *A = at(h->S[l], b * k[l] * k[l]);
+                    if (h->sym && cidxS[l][b] < 0) continue;      // applied as the transpose of (s, t)
+                    const void *A = at(h->S[l], (h->sym ? cidxS[l][b] : b) * k[l] * k[l]);
                     if (o < 0 || o == p)
-                        bl.push_back({A, h->xh_base[l] + (s - L.g0(l)) * k[l], k[l], 0});
+                        bl.push_back({A, h->xh_base[l] + (s - L.g0(l)) * k[l], k[l],
+                                      (int32_t)(h->sym && s > L.g0(l) + i ? -1 : 0)});
                     else {
                         auto pos = xrecv_pos.at(node_key(l, s));
                         offb.push_back({A, pos.first, k[l], (int32_t)pos.second});
@@ -1035,10 +1097,12 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             for (int64_t b = d->D_rowptr[t]; b < d->D_rowptr[t + 1]; ++b) {
                 int64_t s = d->D_col[b];
                 int o = L.owner(q, s);
-                const void *A = at(h->D, b * m * m);
+                if (h->sym && cidxD[b] < 0) continue;
+                const void *A = at(h->D, (h->sym ? cidxD[b] : b) * m * m);
                 if (o == p) {
                     int64_t slot = s - L.g0(q);
-                    blks.push_back({A, d->leaf_ptr[slot], (int32_t)(d->leaf_ptr[slot + 1] - d->leaf_ptr[slot]), 0});
+                    blks.push_back({A, d->leaf_ptr[slot], (int32_t)(d->leaf_ptr[slot + 1] - d->leaf_ptr[slot]),
+                                    (int32_t)(h->sym && s > L.g0(q) + t ? -1 : 0)});
                 } else {
                     auto pos = hrecv_pos.at(s);
                     blks.push_back({A, -1 - pos.first, (int32_t)gleaf_size[s], (int32_t)pos.second});
@@ -1182,7 +1246,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         for (int ci = 0; ci < 3; ++ci) launches += h->coup_off[ci].n ? 1 : 0;
         if (h->has_top) launches += (int)h->top_stages.size();
     }
-    h->launches_per_call = launches;
+    h->launches_per_call = launches + (h->sym ? 1 : 0);    // + the beta pass of the symmetric leaves
     // CTA engine: k_set_args, up_leaf, one launch per coupling class / transfer level, the leaves
     h->launches_cta = 3 + (int)h->coup_leaf.size() + (int)h->up_lv.size() + (int)h->coup_diag.size() +
                       (int)h->down_lv.size();
@@ -1233,10 +1297,59 @@ const int kPhaseSpan[H2_NPHASE + 1][2] = {{0, 1}, {2, 3}, {3, 4}, {4, 5}, {5, 6}
 // part: PART_ALL (NCCL or single rank), or for loopback groups PART_UP (everything before the
 // exchange: x halo pack, leaf projection, leaf-level coupling, upsweep, x^ pack) and PART_DOWN
 // (everything after it: top tree, couplings, downsweep, leaves), the group copying between them.
+// Symmetric storage (one rank, nv = 1): the same phases with the coupling rows and the leaves
+// applying every stored off-diagonal block also transposed (h2_sym.cuh), accumulating with atomics
+// into a zeroed y^ and a beta-scaled Y.
+template <typename T>
+int enqueue_sym(h2_ctx *h, int nv, cudaStream_t st)
+{
+    T *xh = (T *)h->xh, *yh = (T *)h->yh;
+    const CallArgs<T> *args = (const CallArgs<T> *)h->dargs;
+    auto T0 = [&](const Phase &ph) { return h->d_tasks + ph.t0; };
+    int rc;
+#define H2_MARK(i) if ((rc = mark(h, i, st)) != H2_OK) return rc
+    cudaStream_t s_leafc = h->prof ? st : h->s_leafc;
+    H2_MARK(0);
+    H2_CUDA(h, cudaMemsetAsync(yh, 0, (size_t)h->yh_plane * nv * sizeof(T), st));
+    H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
+                                 h->up_leaf.r, st));
+    H2_MARK(1);
+    H2_CUDA(h, cudaEventRecord(h->ev_upleaf, st));
+    H2_CUDA(h, cudaStreamWaitEvent(s_leafc, h->ev_upleaf, 0));
+    for (const Phase &ph : h->coup_leaf)
+        H2_CUDA(h, launch_sym_rows<T>(T0(ph), ph.n, h->d_blks, xh, yh, ph.r, s_leafc));
+    H2_CUDA(h, cudaEventRecord(h->ev_leafc, s_leafc));
+    H2_MARK(2);
+    for (size_t u = 0; u < h->up_sweeps.size(); ++u)
+        H2_CUDA(h, launch_sweep<T>(MODE_WRITE, h->up_sweeps[u], h->up_sweep_ctas[u],
+                                   h->up_sweep_ctas[u] == 1 && h->up_sweeps[u].nlev > 1 ? 512 : WPB * 32, xh,
+                                   h->xh_plane, nv, h->sweep_r_up, st));
+    H2_MARK(3);
+    H2_MARK(4);
+    for (const Phase &ph : h->coup_diag)
+        H2_CUDA(h, launch_sym_rows<T>(T0(ph), ph.n, h->d_blks, xh, yh, ph.r, st));
+    H2_MARK(5);
+    H2_MARK(6);
+    for (size_t u = 0; u < h->dn_sweeps.size(); ++u)
+        H2_CUDA(h, launch_sweep<T>(MODE_ACCUM, h->dn_sweeps[u], h->dn_sweep_ctas[u],
+                                   h->dn_sweep_ctas[u] == 1 && h->dn_sweeps[u].nlev > 1 ? 512 : WPB * 32, yh,
+                                   h->yh_plane, nv, h->sweep_r_dn, st));
+    H2_MARK(7);
+    H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_leafc, 0));
+    H2_CUDA(h, launch_beta<T>(args, h->n_local, nv, st));
+    H2_MARK(8);
+    H2_CUDA(h, launch_sym_leaf<T>(T0(h->leaf), T0(h->dense), h->leaf.n, h->d_blks, yh, args, h->leaf.r, st));
+    H2_MARK(9);
+    if (h->prof) h->ev_used += NEV;
+#undef H2_MARK
+    return H2_OK;
+}
+
 enum { PART_ALL = 0, PART_UP = 1, PART_DOWN = 2 };
 template <typename T>
 int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
 {
+    if (h->sym) return enqueue_sym<T>(h, nv, st);
     const Layout &L = h->L;
     const int q = L.q, C = L.C;
     T *xh = (T *)h->xh, *yh = (T *)h->yh;
@@ -1644,7 +1757,7 @@ extern "C" int h2_stats(h2_handle h, int nv, double *flops, double *bytes, doubl
     for (int l = 0; l <= L.q; ++l) tree += (double)L.held(l) * L.k[l];
     if (flops) *flops = 2.0 * nv * h->ops_local;
     // operator once + X read + Y write + x^, y^ trees written and read once each
-    if (bytes) *bytes = (double)h->esz * (h->ops_local + nv * (2.0 * h->n_local + 4.0 * tree));
+    if (bytes) *bytes = (double)h->esz * (h->ops_stored + nv * (2.0 * h->n_local + 4.0 * tree));
     if (xchg_bytes) {
         double x = 0;
         for (const auto &pr : h->peers) x += (double)(pr.xr_cnt + pr.hr_cnt) * nv * h->esz;

@@ -142,6 +142,14 @@ struct CtaJob {
     const CallArgs<double> *args;
     int nv;
 };
+// symmetric storage (h2_sym.cuh): blocks with Blk::xld == -1 are also applied transposed
+template <typename T>
+cudaError_t launch_sym_rows(const Task *t, int ntask, const Blk *b, const T *xh, T *yh, int r, cudaStream_t s);
+template <typename T>
+cudaError_t launch_sym_leaf(const Task *lt, const Task *dt, int ntask, const Blk *b, const T *yh,
+                            const CallArgs<T> *args, int m, cudaStream_t s);
+template <typename T>
+cudaError_t launch_beta(const CallArgs<T> *args, int64_t n, int nv, cudaStream_t s);
 // rmax: the widest output tile of the job's tasks; nsm: SMs (grid = min(ntask, nsm))
 cudaError_t launch_cta(const CtaJob &j, int rmax, int nsm, cudaStream_t s);
 }  // namespace h2

@@ -71,7 +71,7 @@ def broadcast_nccl_id(device):
 
 
 def operator_from_h2data(h, rank=0, nranks=1, nccl_id=None, dtype="f64", nv_max=16, device=False,
-                         torch_device=None):
+                         torch_device=None, symmetric=False):
     """H2Operator for `rank` of `nranks`.  device=True uploads the floating arrays as CUDA torch
     tensors that the handle adopts (H2_MEM_DEVICE); otherwise h2_create copies host arrays."""
     kw, rows = shard_arrays(h, rank, nranks)
@@ -89,7 +89,10 @@ def operator_from_h2data(h, rank=0, nranks=1, nccl_id=None, dtype="f64", nv_max=
             kw[key] = up(kw[key])
         for key in ("E", "F", "S"):
             kw[key] = [up(a) for a in kw[key]]
-    op = H2Operator(dtype=dtype, nv_max=nv_max, nccl_id=nccl_id, **kw)
+    if symmetric:
+        kw["V_leaf"] = kw["U_leaf"]        # the same array (H2_SYMMETRIC asserts U = V)
+        kw["F"] = kw["E"]
+    op = H2Operator(dtype=dtype, nv_max=nv_max, nccl_id=nccl_id, symmetric=symmetric, **kw)
     op.row_range = rows
     return op
 
