@@ -46,6 +46,7 @@ struct NcclApi {
     ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
@@ -75,6 +76,7 @@ bool load_nccl()
     H2_SYM(Send, "ncclSend")
     H2_SYM(Recv, "ncclRecv")
     H2_SYM(AllGather, "ncclAllGather")
+    H2_SYM(AllReduce, "ncclAllReduce")
     H2_SYM(GroupStart, "ncclGroupStart")
     H2_SYM(GroupEnd, "ncclGroupEnd")
     H2_SYM(GetErrorString, "ncclGetErrorString")
@@ -292,6 +294,29 @@ struct h2_ctx {
         int64_t hs_off = 0, hs_cnt = 0, hr_off = 0, hr_cnt = 0;   // rows per vector
     };
     std::vector<Peer> peers;
+    // device-initiated peer exchange (NEXT-1; H2_EXCHANGE=nccl keeps the NCCL groups): peers read
+    // my x^ plane and my packed x rows directly through CUDA-IPC mappings, synchronised by epoch
+    // flags in the handles' signal blocks (h2_internal.h SIG_*)
+    bool p2p = false;
+    bool p2p_direct = false;           // H2_EXCHANGE=p2p-direct: the off-diagonal kernels read the peers'
+                                       // x^ over NVLink themselves (measured slower: latency-bound)
+    int32_t *sig = nullptr;
+    struct Pull { int owner, group; int64_t seg0, nseg; };
+    std::vector<Pull> pulls;           // per (level group, owner): segments copying the owner's x^ nodes I
+                                       // need from its mapped plane into my receive chunk
+    struct PeerMap {
+        const void *xh = nullptr, *hsend = nullptr;
+        int32_t *sig = nullptr;
+        int64_t hs_off = -1;           // offset of my chunk in the peer's hsend
+    };
+    std::vector<PeerMap> pmap;         // by rank
+    std::vector<void *> ipc_open;
+    struct P2PPhase { int owner, group; Phase ph; };
+    std::vector<P2PPhase> p2p_phases;  // off-diagonal tasks reading one peer's x^ directly
+    int32_t *d_begin_waits = nullptr, *d_wait_xl = nullptr, *d_wait_xu = nullptr, *d_wait_h = nullptr;
+    int32_t **d_tgt_xl = nullptr, **d_tgt_xu = nullptr, **d_tgt_h = nullptr, **d_tgt_cx = nullptr, **d_tgt_ch = nullptr;
+    int n_begin_waits = 0, n_wait_xl = 0, n_wait_xu = 0, n_wait_h = 0, n_tgt_xl = 0, n_tgt_xu = 0, n_tgt_h = 0,
+        n_tgt_cx = 0, n_tgt_ch = 0;
     int64_t xsend_tot = 0, xrecv_tot = 0, hsend_tot = 0, hrecv_tot = 0;
     ncclComm_t comm = nullptr;
     // e2e staging
@@ -374,6 +399,15 @@ int release(h2_ctx *h)
     for (auto &g : h->graph)
         if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     cudaDeviceSynchronize();
+    if (!h->ipc_open.empty() || h->sig) {
+        // peers may still read my buffers: a barrier over the communicator before anything is freed
+        if (h->comm && g_nccl.loaded && h->s_comm && h->sig) {
+            g_nccl.AllReduce(h->sig, h->sig, 1, ncclInt32, ncclMax, h->comm, h->s_comm);
+            cudaStreamSynchronize(h->s_comm);
+        }
+        for (void *p : h->ipc_open) cudaIpcCloseMemHandle(p);
+        h->ipc_open.clear();
+    }
     if (h->comm && g_nccl.loaded) g_nccl.CommDestroy(h->comm);
     for (void *p : h->owned) cudaFree(p);
     for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
@@ -912,6 +946,87 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         h->hsend = dalloc(h, (size_t)h->hsend_tot * h->esz, err);
         h->hrecv = dalloc(h, (size_t)h->hrecv_tot * h->esz, err);
         if (!h->xsend || !h->xrecv || !h->hsend || !h->hrecv) H2_TRY(cuda_fail(h, err, "cudaMalloc(exchange buffers)"));
+        const char *ex = getenv("H2_EXCHANGE");
+        h->p2p = !loop && !(ex && !strcmp(ex, "nccl"));
+        h->p2p_direct = h->p2p && ex && !strcmp(ex, "p2p-direct");
+        if (h->p2p) {
+            // ---- device-initiated exchange: signal block, IPC handles of x^ / hsend / signals and
+            //      every rank's chunk offsets, exchanged once over the communicator
+            h->sig = (int32_t *)dalloc(h, SIG_INTS * sizeof(int32_t), err);
+            if (!h->sig) H2_TRY(cuda_fail(h, err, "cudaMalloc(signals)"));
+            H2_TRYC(cudaMemset(h->sig, 0, SIG_INTS * sizeof(int32_t)));
+            const size_t rec = 3 * sizeof(cudaIpcMemHandle_t) + (size_t)P * sizeof(int64_t);
+            std::vector<unsigned char> mine(rec, 0), all(rec * P, 0);
+            cudaIpcMemHandle_t hd[3];
+            H2_TRYC(cudaIpcGetMemHandle(&hd[0], h->xh));
+            H2_TRYC(cudaIpcGetMemHandle(&hd[1], h->hsend));
+            H2_TRYC(cudaIpcGetMemHandle(&hd[2], h->sig));
+            memcpy(mine.data(), hd, sizeof(hd));
+            std::vector<int64_t> hso(P, -1);
+            for (const auto &pr : h->peers) hso[pr.rank] = pr.hs_off;
+            memcpy(mine.data() + sizeof(hd), hso.data(), P * sizeof(int64_t));
+            void *dmine = dalloc(h, rec, err), *dall = dalloc(h, rec * P, err);
+            if (!dmine || !dall) H2_TRY(cuda_fail(h, err, "cudaMalloc(setup)"));
+            H2_TRYC(cudaMemcpy(dmine, mine.data(), rec, cudaMemcpyHostToDevice));
+            H2_TRY([&]() -> int { H2_NCCL(h, g_nccl.AllGather(dmine, dall, rec, ncclUint8, h->comm, h->s_comm)); return H2_OK; }());
+            H2_TRYC(cudaStreamSynchronize(h->s_comm));
+            H2_TRYC(cudaMemcpy(all.data(), dall, rec * P, cudaMemcpyDeviceToHost));
+            h->pmap.assign(P, h2_ctx::PeerMap{});
+            for (int o = 0; o < P; ++o) {
+                if (o == p) continue;
+                const unsigned char *r = all.data() + rec * o;
+                cudaIpcMemHandle_t ho[3];
+                memcpy(ho, r, sizeof(ho));
+                void *ptr[3];
+                for (int i = 0; i < 3; ++i) {
+                    H2_TRYC(cudaIpcOpenMemHandle(&ptr[i], ho[i], cudaIpcMemLazyEnablePeerAccess));
+                    h->ipc_open.push_back(ptr[i]);
+                }
+                h->pmap[o].xh = ptr[0];
+                h->pmap[o].hsend = ptr[1];
+                h->pmap[o].sig = (int32_t *)ptr[2];
+                memcpy(&h->pmap[o].hs_off, r + sizeof(ho) + (size_t)p * sizeof(int64_t), sizeof(int64_t));
+            }
+            // who reads what: x^ readers / sources (all ranks when the top tree gathers roots)
+            std::vector<int32_t> begin, wxl, wxu, wh;
+            std::vector<int32_t *> txl, txu, th, tcx, tch;
+            for (int o = 0; o < P; ++o) {
+                if (o == p) continue;
+                const bool x_reader = give_x.count(o) || h->has_top, x_source = need_x.count(o) || h->has_top;
+                const bool h_reader = give_h.count(o) > 0, h_source = need_h.count(o) > 0;
+                int32_t *os = h->pmap[o].sig;
+                if (x_reader) { begin.push_back(SIG_CONS_X + o); txl.push_back(os + SIG_XLEAF + p); txu.push_back(os + SIG_XUP + p); }
+                if (h_reader) { begin.push_back(SIG_CONS_H + o); th.push_back(os + SIG_HALO + p); }
+                if (x_source) { wxl.push_back(SIG_XLEAF + o); wxu.push_back(SIG_XUP + o); tcx.push_back(os + SIG_CONS_X + p); }
+                if (h_source) { wh.push_back(SIG_HALO + o); tch.push_back(os + SIG_CONS_H + p); }
+            }
+            auto upload_i = [&](const std::vector<int32_t> &v, int32_t **out, int &n) -> int {
+                cudaError_t e2;
+                n = (int)v.size();
+                *out = (int32_t *)dalloc(h, (v.size() + 1) * sizeof(int32_t), e2);
+                if (!*out) return cuda_fail(h, e2, "cudaMalloc(signal lists)");
+                if (!v.empty()) H2_CUDA(h, cudaMemcpy(*out, v.data(), v.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+                return H2_OK;
+            };
+            auto upload_p = [&](const std::vector<int32_t *> &v, int32_t ***out, int &n) -> int {
+                cudaError_t e2;
+                n = (int)v.size();
+                *out = (int32_t **)dalloc(h, (v.size() + 1) * sizeof(int32_t *), e2);
+                if (!*out) return cuda_fail(h, e2, "cudaMalloc(signal lists)");
+                if (!v.empty()) H2_CUDA(h, cudaMemcpy(*out, v.data(), v.size() * sizeof(int32_t *), cudaMemcpyHostToDevice));
+                return H2_OK;
+            };
+            H2_TRY(upload_i(begin, &h->d_begin_waits, h->n_begin_waits));
+            H2_TRY(upload_i(wxl, &h->d_wait_xl, h->n_wait_xl));
+            H2_TRY(upload_i(wxu, &h->d_wait_xu, h->n_wait_xu));
+            H2_TRY(upload_i(wh, &h->d_wait_h, h->n_wait_h));
+            H2_TRY(upload_p(txl, &h->d_tgt_xl, h->n_tgt_xl));
+            H2_TRY(upload_p(txu, &h->d_tgt_xu, h->n_tgt_xu));
+            H2_TRY(upload_p(th, &h->d_tgt_h, h->n_tgt_h));
+            H2_TRY(upload_p(tcx, &h->d_tgt_cx, h->n_tgt_cx));
+            H2_TRY(upload_p(tch, &h->d_tgt_ch, h->n_tgt_ch));
+            H2_DBG("rank %d: p2p exchange mapped (%d x-sources, %d halo sources)", p, h->n_wait_xu, h->n_wait_h);
+        }
     }
 
     // ---- the task / block tables
@@ -977,6 +1092,9 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     //     (PAPER.md:328-331, 496); every held row gets a task (empty rows write 0)
     std::vector<Task> offd_tasks[3];
     std::vector<Blk> offd_blks[3];
+    std::vector<Task> p2p_tasks[2][3];     // [leaf level, upper levels][class]
+    std::vector<Blk> p2p_blks[2][3];
+    std::vector<int> p2p_owner[2][3];
     {
         // classes: engine class ci (0..2) for the levels above the leaves, 3 + ci for the leaf
         // level (its coupling only needs x^ of the leaves: it runs on its own stream right after
@@ -1001,7 +1119,11 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
                     if (o < 0 || o == p)
                         bl.push_back({A, h->xh_base[l] + (s - L.g0(l)) * k[l], k[l],
                                       (int32_t)(h->sym && s > L.g0(l) + i ? -1 : 0)});
-                    else {
+                    else if (h->p2p_direct) {
+                        // the owner's x^ plane has my layout: its slot of node s at its level-l base
+                        const int64_t og0 = (int64_t)o << (l - C);
+                        offb.push_back({A, h->xh_base[l] + (s - og0) * k[l], k[l], (int32_t)o});
+                    } else {
                         auto pos = xrecv_pos.at(node_key(l, s));
                         offb.push_back({A, pos.first, k[l], (int32_t)pos.second});
                     }
@@ -1011,7 +1133,21 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
                 cls[cj].push_back(t);
                 cls_lvl[cj].push_back(l);
                 cls_blk[cj].push_back(bl);
-                if (!offb.empty()) {
+                if (!offb.empty() && h->p2p_direct) {
+                    // one task per (row, owner): each launch reads one peer's mapped x^ plane;
+                    // Blk::xld carried the owner rank only until here (0 = the plane's own ld)
+                    const int g = (l == q) ? 0 : 1;
+                    std::map<int, std::vector<Blk>> by;
+                    for (Blk bb : offb) { const int o = bb.xld; bb.xld = 0; by[o].push_back(bb); }
+                    for (auto &kv : by) {
+                        Task to = t;
+                        to.nblk = (int32_t)kv.second.size();
+                        to.blk0 = (int64_t)p2p_blks[g][ci].size();
+                        p2p_tasks[g][ci].push_back(to);
+                        p2p_owner[g][ci].push_back(kv.first);
+                        p2p_blks[g][ci].insert(p2p_blks[g][ci].end(), kv.second.begin(), kv.second.end());
+                    }
+                } else if (!offb.empty()) {
                     Task to = t;
                     to.nblk = (int32_t)offb.size();
                     to.blk0 = (int64_t)offd_blks[ci].size();
@@ -1039,6 +1175,26 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             }
             if (ph.n) (cj < 3 ? h->coup_diag : h->coup_leaf).push_back(ph);
         }
+        // device-initiated exchange: one launch per (level group, class, owner)
+        for (int g = 0; g < 2; ++g)
+            for (int ci = 0; ci < 3; ++ci) {
+                std::map<int, std::vector<size_t>> by;
+                for (size_t u = 0; u < p2p_tasks[g][ci].size(); ++u) by[p2p_owner[g][ci][u]].push_back(u);
+                for (auto &kv : by) {
+                    h2_ctx::P2PPhase pp{kv.first, g, Phase{}};
+                    pp.ph.t0 = tasks.size();
+                    pp.ph.r = cls_r[ci];
+                    pp.ph.n = (int)kv.second.size();
+                    for (size_t u : kv.second) {
+                        Task t = p2p_tasks[g][ci][u];
+                        const int64_t b0 = t.blk0;
+                        t.blk0 = (int64_t)blks.size();
+                        blks.insert(blks.end(), p2p_blks[g][ci].begin() + b0, p2p_blks[g][ci].begin() + b0 + t.nblk);
+                        tasks.push_back(t);
+                    }
+                    h->p2p_phases.push_back(pp);
+                }
+            }
         for (int ci = 0; ci < 3; ++ci) {
             h->coup_off[ci].t0 = tasks.size();
             h->coup_off[ci].r = cls_r[ci];
@@ -1222,6 +1378,26 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         h->seg_x0 = 0; h->nseg_x = (int64_t)segs_x.size();
         h->seg_h0 = (int64_t)segs.size(); h->nseg_h = (int64_t)segs_h.size();
         segs.insert(segs.end(), segs_h.begin(), segs_h.end());
+        if (h->p2p && !h->p2p_direct) {
+            // pull segments: node (l, s) of owner o sits in o's plane at xh_base[l] + (s - o's g0) k^l
+            // and lands in my receive chunk exactly where the NCCL receive would put it
+            for (int g = 0; g < 2; ++g)
+                for (const auto &pr : h->peers) {
+                    if (!need_x.count(pr.rank)) continue;
+                    h2_ctx::Pull pl{pr.rank, g, (int64_t)segs.size(), 0};
+                    int64_t pos = 0;
+                    for (int64_t key : need_x[pr.rank]) {
+                        const int l = key_level(key);
+                        const int64_t og0 = (int64_t)pr.rank << (l - C);
+                        if ((l == q) == (g == 0))
+                            segs.push_back({h->xh_base[l] + (key_node(key) - og0) * k[l], pr.xr_off + pos, k[l],
+                                            (int32_t)pr.xr_cnt});
+                        pos += k[l];
+                    }
+                    pl.nseg = (int64_t)segs.size() - pl.seg0;
+                    if (pl.nseg) h->pulls.push_back(pl);
+                }
+        }
         h->d_segs = (PackSeg *)dalloc(h, segs.size() * sizeof(PackSeg), err);
         if (!h->d_tasks || !h->d_blks || !h->d_segs) H2_TRY(cuda_fail(h, err, "cudaMalloc(plan)"));
         H2_TRYC(cudaMemcpy(h->d_tasks, tasks.data(), tasks.size() * sizeof(Task), cudaMemcpyHostToDevice));
@@ -1241,20 +1417,24 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     int launches = 3 + (int)(h->use_sweep ? h->up_sweeps.size() : h->up_stages.size()) +
                    (int)h->coup_diag.size() + (int)h->coup_leaf.size() +
                    (int)(h->use_sweep ? h->dn_sweeps.size() : h->down_stages.size());
-    if (P > 1) {
-        launches += 2;   // pack x^, pack halo
-        for (int ci = 0; ci < 3; ++ci) launches += h->coup_off[ci].n ? 1 : 0;
-        if (h->has_top) launches += (int)h->top_stages.size();
+    // distributed extras: the packs and off-diagonal launches (NCCL), or the pack, the signal /
+    // wait kernels and the per-owner off-diagonal launches (device-initiated exchange)
+    int dist = 0;
+    if (P > 1 && !h->p2p) {
+        dist += 2;   // pack x^, pack halo
+        for (int ci = 0; ci < 3; ++ci) dist += h->coup_off[ci].n ? 1 : 0;
+    } else if (P > 1) {
+        dist += 2 + (int)h->p2p_phases.size() + (int)h->pulls.size();   // p2p_begin, pack halo, off-diagonal / pulls
+        if (!h->p2p_direct)
+            for (int ci = 0; ci < 3; ++ci) dist += h->coup_off[ci].n ? 1 : 0;
+        dist += (h->n_tgt_h > 0) + (h->n_wait_h > 0) + (h->n_tgt_ch > 0) + (h->n_tgt_xl > 0) + (h->n_tgt_xu > 0) +
+                (h->n_wait_xl > 0) + (h->n_wait_xu > 0) + (h->n_tgt_cx > 0) + (h->has_top && h->n_wait_xu > 0);
     }
-    h->launches_per_call = launches + (h->sym ? 1 : 0);    // + the beta pass of the symmetric leaves
+    if (h->has_top) dist += (int)h->top_stages.size();
+    h->launches_per_call = launches + dist + (h->sym ? 1 : 0);   // + the beta pass of the symmetric leaves
     // CTA engine: k_set_args, up_leaf, one launch per coupling class / transfer level, the leaves
     h->launches_cta = 3 + (int)h->coup_leaf.size() + (int)h->up_lv.size() + (int)h->coup_diag.size() +
-                      (int)h->down_lv.size();
-    if (P > 1) {
-        h->launches_cta += 2;
-        for (int ci = 0; ci < 3; ++ci) h->launches_cta += h->coup_off[ci].n ? 1 : 0;
-        if (h->has_top) h->launches_cta += (int)h->top_stages.size();
-    }
+                      (int)h->down_lv.size() + dist;
     *out = h;
     return H2_OK;
 #undef H2_TRY
@@ -1384,11 +1564,28 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
         j.nv = nv;
         return j;
     };
+    const bool p2p = nccl && h->p2p;
     if (part != PART_DOWN) {
     H2_MARK(0);
     // 0. x-leaf halo for the off-process dense blocks (P > 1): X is an input, so the exchange
     //    starts at t = 0 on the comm stream
-    if (nccl) {
+    if (p2p) {
+        // device-initiated exchange (NEXT-1): wait until the peers are done with my previous
+        // call's data, pack my x rows, flag them; the comm stream pulls the peers' rows over
+        // NVLink (IPC mappings) as soon as their flags arrive and acknowledges
+        H2_CUDA(h, launch_p2p_begin(h->sig, h->d_begin_waits, h->n_begin_waits, st));
+        H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_h0, h->nseg_h, (const T *)nullptr, 0, args, (T *)h->hsend, nv, st));
+        H2_CUDA(h, launch_p2p_signal(h->sig, h->d_tgt_h, h->n_tgt_h, st));
+        H2_CUDA(h, cudaEventRecord(h->ev_fork, st));
+        H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_fork, 0));
+        H2_CUDA(h, launch_p2p_wait(h->sig, h->d_wait_h, h->n_wait_h, h->s_comm));
+        for (const auto &pr : h->peers)
+            if (pr.hr_cnt)
+                H2_CUDA(h, cudaMemcpyAsync((T *)h->hrecv + pr.hr_off, (const T *)h->pmap[pr.rank].hsend + h->pmap[pr.rank].hs_off,
+                                           (size_t)pr.hr_cnt * nv * sizeof(T), cudaMemcpyDeviceToDevice, h->s_comm));
+        H2_CUDA(h, launch_p2p_signal(h->sig, h->d_tgt_ch, h->n_tgt_ch, h->s_comm));
+        H2_CUDA(h, cudaEventRecord(h->ev_halo, h->s_comm));
+    } else if (nccl) {
         H2_CUDA(h, cudaEventRecord(h->ev_fork, st));
         H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_fork, 0));
         H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_h0, h->nseg_h, (const T *)nullptr, 0, args, (T *)h->hsend, nv, h->s_comm));
@@ -1409,11 +1606,28 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     else
         H2_CUDA(h, launch_up_leaf<T>(T0(h->up_leaf), h->up_leaf.n, h->d_blks, args, xh, h->xh_plane, nv,
                                      h->up_leaf.r, st));
+    if (p2p) H2_CUDA(h, launch_p2p_signal(h->sig, h->d_tgt_xl, h->n_tgt_xl, st));   // leaf-level x^ ready
     H2_MARK(1);
     // 1b. leaf-level coupling (diagonal part) as soon as x^ of the leaves exists (alg:mult's
     //     levels are independent), on its own stream
     H2_CUDA(h, cudaEventRecord(h->ev_upleaf, st));
     H2_CUDA(h, cudaStreamWaitEvent(s_leafc, h->ev_upleaf, 0));
+    if (p2p && !h->p2p_direct) {
+        // the comm stream pulls the peers' x^ nodes I need into my receive chunks as their flags
+        // arrive (leaf level first), overlapped with my upsweep and diagonal coupling; ev_upleaf
+        // also orders it after my previous call's off-diagonal reads of those chunks
+        H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_upleaf, 0));
+        for (int g = 0; g < 2; ++g) {
+            H2_CUDA(h, launch_p2p_wait(h->sig, g == 0 ? h->d_wait_xl : h->d_wait_xu, g == 0 ? h->n_wait_xl : h->n_wait_xu,
+                                       h->s_comm));
+            for (const auto &pl : h->pulls)
+                if (pl.group == g)
+                    H2_CUDA(h, launch_pack<T>(h->d_segs + pl.seg0, pl.nseg, (const T *)h->pmap[pl.owner].xh, h->xh_plane,
+                                              args, (T *)h->xrecv, nv, h->s_comm));
+        }
+        H2_CUDA(h, launch_p2p_signal(h->sig, h->d_tgt_cx, h->n_tgt_cx, h->s_comm));
+        H2_CUDA(h, cudaEventRecord(h->ev_recv, h->s_comm));
+    }
     for (const Phase &ph : h->coup_leaf) {
         if (cta)
             H2_CUDA(h, launch_cta(cjob(ph, CK_ROWS, MODE_WRITE, xh, h->xh_plane, yh, h->yh_plane), ph.r, h->nsm,
@@ -1439,11 +1653,13 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
                                       sg.r, st));
     }
     H2_MARK(3);
+    if (p2p) H2_CUDA(h, launch_p2p_signal(h->sig, h->d_tgt_xu, h->n_tgt_xu, st));   // upper-level x^ ready
     // 2. exchange (P > 1): pack my x^ nodes that peers need, one NCCL group on the comm stream,
-    //    overlapped with the diagonal multiply (alg:optimized_dist_mult)
-    if (L.P > 1)
+    //    overlapped with the diagonal multiply (alg:optimized_dist_mult); the device-initiated
+    //    exchange needs no pack: peers read my x^ plane directly
+    if (L.P > 1 && !p2p)
         H2_CUDA(h, launch_pack<T>(h->d_segs + h->seg_x0, h->nseg_x, xh, h->xh_plane, args, (T *)h->xsend, nv, st));
-    if (nccl) {
+    if (nccl && !p2p) {
         H2_CUDA(h, cudaEventRecord(h->ev_packed, st));
         H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_packed, 0));
         H2_NCCL(h, g_nccl.GroupStart());
@@ -1459,7 +1675,16 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     // replicated top tree: gather the branch roots, upsweep the top
     if (h->has_top) {
         const int kC = L.k[C];
-        if (nccl) {
+        if (p2p) {
+            // every rank's branch root, read from the peers' x^ planes once they are complete
+            H2_CUDA(h, launch_p2p_wait(h->sig, h->d_wait_xu, h->n_wait_xu, st));
+            for (int o = 0; o < L.P; ++o) {
+                const T *src = (o == L.p ? xh : (const T *)h->pmap[o].xh) + h->xh_base[C];
+                H2_CUDA(h, cudaMemcpy2DAsync(xh + h->xgather + (int64_t)o * kC, (size_t)h->xh_plane * sizeof(T), src,
+                                             (size_t)h->xh_plane * sizeof(T), (size_t)kC * sizeof(T), nv,
+                                             cudaMemcpyDeviceToDevice, st));
+            }
+        } else if (nccl) {
             // own root -> gather slot p, then allgather in place over the P slots of every plane
             for (int n = 0; n < nv; ++n) {
                 T *g = xh + h->xgather + (int64_t)n * h->xh_plane;
@@ -1484,9 +1709,27 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     H2_MARK(5);
     // 4. off-diagonal part after the exchange (waitAll, alg:optimized_dist_mult line 11-12);
     //    it accumulates into leaf-level rows too, so the leaf coupling stream joins first
-    if (L.P > 1) {
+    if (p2p && h->p2p_direct) {
+        // off-diagonal blocks read the owners' x^ planes directly (NVLink): leaf level first
+        // (flagged right after the owners' leaf projection), then the upper levels
         H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_leafc, 0));
-        if (nccl) H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_recv, 0));
+        for (int g = 0; g < 2; ++g) {
+            H2_CUDA(h, launch_p2p_wait(h->sig, g == 0 ? h->d_wait_xl : h->d_wait_xu, g == 0 ? h->n_wait_xl : h->n_wait_xu, st));
+            for (const auto &pp : h->p2p_phases) {
+                if (pp.group != g) continue;
+                const T *src = (const T *)h->pmap[pp.owner].xh;
+                if (cta)
+                    H2_CUDA(h, launch_cta(cjob(pp.ph, CK_ROWS, MODE_ACCUM, src, h->xh_plane, yh, h->yh_plane), pp.ph.r,
+                                          h->nsm, st));
+                else
+                    H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(pp.ph), pp.ph.n, h->d_blks, src, h->xh_plane, yh,
+                                              h->yh_plane, nv, pp.ph.r, st));
+            }
+        }
+        H2_CUDA(h, launch_p2p_signal(h->sig, h->d_tgt_cx, h->n_tgt_cx, st));
+    } else if (L.P > 1) {
+        H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_leafc, 0));
+        if (nccl) H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_recv, 0));     // NCCL receive or p2p pulls
         for (int ci = 0; ci < 3; ++ci) {
             const Phase &ph = h->coup_off[ci];
             if (cta)

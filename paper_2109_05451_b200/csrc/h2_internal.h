@@ -142,6 +142,22 @@ struct CtaJob {
     const CallArgs<double> *args;
     int nv;
 };
+// Device-initiated peer exchange: a per-handle signal block in device
+// memory, written by the peers through CUDA-IPC mappings over NVLink.  Layout (int32 slots):
+constexpr int SIG_EPOCH = 0;        // my call counter
+constexpr int SIG_XLEAF = 32;       // + o: peer o's leaf-level x^ is ready (its epoch)
+constexpr int SIG_XUP = 96;         // + o: peer o's upper-level x^ is ready
+constexpr int SIG_HALO = 160;       // + o: peer o packed the x rows I need
+constexpr int SIG_CONS_X = 224;     // + o: peer o finished reading my x^
+constexpr int SIG_CONS_H = 288;     // + o: peer o finished reading my packed x rows
+constexpr int SIG_INTS = 352;       // (P <= 64)
+// begin a call: epoch += 1, then wait until sig[waits[i]] >= epoch - 1 (WAR: peers done with the
+// previous call's data); signal: *targets[i] = my epoch (release, system scope); wait: until
+// sig[offs[i]] >= my epoch (acquire).  Spins are bounded (trap after ~20 s: no silent hang).
+cudaError_t launch_p2p_begin(int32_t *sig, const int32_t *waits, int nwait, cudaStream_t s);
+cudaError_t launch_p2p_signal(const int32_t *sig, int32_t *const *targets, int n, cudaStream_t s);
+cudaError_t launch_p2p_wait(const int32_t *sig, const int32_t *offs, int n, cudaStream_t s);
+
 // symmetric storage (h2_sym.cuh): blocks with Blk::xld == -1 are also applied transposed
 template <typename T>
 cudaError_t launch_sym_rows(const Task *t, int ntask, const Blk *b, const T *xh, T *yh, int r, cudaStream_t s);

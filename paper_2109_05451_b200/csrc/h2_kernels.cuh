@@ -274,18 +274,40 @@ __device__ __forceinline__ const T *resolve(const Src<T> &s, int64_t x, int32_t 
 // acc += A (r x K, col-major, contiguous) * xs (K x nvc in shared memory, ld xld): columns in
 // groups of U with two groups in flight (the loads of group g+2 are issued behind the FMAs of
 // group g), so each warp keeps 2U column loads outstanding without exposing HBM latency.
+// x row j (NVB vectors, contiguous: the stream stages x vector-fastest) into registers with 16-byte
+// shared loads (broadcast: every lane reads the same row) -- NVB / (16 / sizeof(T)) loads per column
+// instead of NVB scalar loads
+template <typename T, int NVB>
+__device__ __forceinline__ void smem_row(T (&xv)[NVB], const T *p)
+{
+    if constexpr ((NVB * sizeof(T)) % 16 == 0) {
+#pragma unroll
+        for (int n = 0; n < NVB; n += 16 / (int)sizeof(T)) {
+            const float4 q = *reinterpret_cast<const float4 *>(p + n);
+            const T *qt = reinterpret_cast<const T *>(&q);
+#pragma unroll
+            for (int i = 0; i < 16 / (int)sizeof(T); ++i) xv[n + i] = qt[i];
+        }
+    } else {
+#pragma unroll
+        for (int n = 0; n < NVB; ++n) xv[n] = p[n];
+    }
+}
+
+// acc += a (U columns in registers) * xs rows j .. j+U-1 (row e at xs + e * NVB; rows >= K are zero)
 template <typename T, int RPL, int NVB, int U>
 __device__ __forceinline__ void simt_fma_cols(SimtAcc<T, RPL, NVB> &acc, const T (&a)[U][RPL], int j, int K,
                                               const T *xs, int xld)
 {
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+    for (int u = 0; u < U; ++u) {
+        T xv[NVB];
+        smem_row<T, NVB>(xv, xs + (int64_t)(j + u) * NVB);
 #pragma unroll
-        for (int n = 0; n < NVB; ++n) {
-            const T xv = (j + u < K) ? xs[j + u + n * xld] : T(0);
+        for (int n = 0; n < NVB; ++n)
 #pragma unroll
-            for (int ri = 0; ri < RPL; ++ri) acc.v[ri][n] = fma(a[u][ri], xv, acc.v[ri][n]);
-        }
+            for (int ri = 0; ri < RPL; ++ri) acc.v[ri][n] = fma(a[u][ri], xv[n], acc.v[ri][n]);
+    }
 }
 
 template <typename T, int RPL, int NVB>
@@ -309,7 +331,7 @@ __device__ __forceinline__ void simt_stream(SimtAcc<T, RPL, NVB> &acc, const T *
                                             int c, int nblk, const Blk *__restrict__ blks,
                                             const Src<T> &src, int nvc, int lane, T *xs, int xcap)
 {
-    int per = xcap / (c * NVB);
+    int per = (xcap - 16 * NVB) / (c * NVB);          // room for the 2U zero rows of the tail
     per = per < 1 ? 1 : (per > 32 ? 32 : per);
     for (int b0 = 0; b0 < nblk; b0 += per) {
         const int nb = min(per, nblk - b0);
@@ -330,9 +352,12 @@ __device__ __forceinline__ void simt_stream(SimtAcc<T, RPL, NVB> &acc, const T *
                 int64_t ld;
                 const T *p = resolve(src, bxo, bxl, ld);
 #pragma unroll
-                for (int n = 0; n < NVB; ++n) xs[e + n * K] = (j < bxr && n < nvc) ? p[j + n * ld] : T(0);
+                for (int n = 0; n < NVB; ++n) xs[e * NVB + n] = (j < bxr && n < nvc) ? p[j + n * ld] : T(0);
             }
         }
+        // rows K .. K + 2U - 1 are read by the pipelined tail (their A columns are zero): keep them 0
+        constexpr int UP = RPL == 1 ? 8 : 4;
+        for (int e = K * NVB + lane; e < (K + 2 * UP) * NVB; e += 32) xs[e] = T(0);
         __syncwarp();
         simt_cols_pipelined<T, RPL, NVB>(acc, A0 + (int64_t)b0 * r * c, r, K, xs, K, lane);
         __syncwarp();
@@ -489,7 +514,8 @@ struct Simt {
     static constexpr int MINB = NVB <= 2 ? (RPL == 1 ? 4 : 3) : 2;
     static constexpr bool SIMT1 = (RPL == 1 && NVB == 1);
     static constexpr bool MMA = false;
-    static constexpr int SCRATCH = XCAP_BYTES;      // per-warp smem for the stream staging
+    // per-warp smem for the stream staging: >= one 64-column block of x plus the 16 zero tail rows
+    static constexpr int SCRATCH = (int)(80 * NVB * sizeof(T)) > XCAP_BYTES ? (int)(80 * NVB * sizeof(T)) : XCAP_BYTES;
     __device__ static void block(Acc &acc, const T *A, int r, int c, const T *src, int64_t ld, int xrows,
                                  int nvc, int lane, int lda = -1)
     { simt_block<T, RPL, NVB>(acc, A, r, c, src, ld, xrows, nvc, lane); }
@@ -499,18 +525,23 @@ struct Simt {
     { simt_block<T, RPL, NVB, true>(acc, A, r, c, src, ld, xrows, nvc, lane); }
     __device__ static void stream(Acc &acc, const T *A0, int r, int c, int nblk, const Blk *blks,
                                   const Src<T> &src, int nvc, int lane, void *scratch)
-    { simt_stream<T, RPL, NVB>(acc, A0, r, c, nblk, blks, src, nvc, lane, (T *)scratch, XCAP_BYTES / (int)sizeof(T)); }
-    // acc += As (r x c, col-major ld r, shared) * xs (c x nvc, ld xld, shared)
+    { simt_stream<T, RPL, NVB>(acc, A0, r, c, nblk, blks, src, nvc, lane, (T *)scratch, SCRATCH / (int)sizeof(T)); }
+    // acc += As (r x c, col-major ld r, shared) * xs (c x nvc, ld xld, shared): outer products,
+    // column j of As and row j of xs per step (RPL + NVB shared loads for RPL x NVB FMAs)
     __device__ static void smem_block(Acc &acc, const T *As, int r, int c, const T *xs, int xld, int nvc, int lane)
     {
-        acc.each(lane, [&](int row, int n, T &v) {
-            if (row < r && n < nvc) {
-                T s = v;
-#pragma unroll 8
-                for (int j = 0; j < c; ++j) s = fma(As[j * r + row], xs[j + n * xld], s);
-                v = s;
+#pragma unroll 4
+        for (int j = 0; j < c; ++j) {
+            T a[RPL];
+#pragma unroll
+            for (int ri = 0; ri < RPL; ++ri) a[ri] = (lane + 32 * ri < r) ? As[j * r + lane + 32 * ri] : T(0);
+#pragma unroll
+            for (int n = 0; n < NVB; ++n) {
+                const T xv = n < nvc ? xs[j + n * xld] : T(0);
+#pragma unroll
+                for (int ri = 0; ri < RPL; ++ri) acc.v[ri][n] = fma(a[ri], xv, acc.v[ri][n]);
             }
-        });
+        }
     }
 };
 
