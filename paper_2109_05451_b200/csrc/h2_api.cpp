@@ -1612,21 +1612,23 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     //     levels are independent), on its own stream
     H2_CUDA(h, cudaEventRecord(h->ev_upleaf, st));
     H2_CUDA(h, cudaStreamWaitEvent(s_leafc, h->ev_upleaf, 0));
+    // the comm stream pulls the peers' x^ nodes I need into my receive chunks as their flags
+    // arrive, overlapped with my upsweep and diagonal coupling; ev_upleaf also orders it after my
+    // previous call's off-diagonal reads of those chunks.  Every wait is enqueued (host order)
+    // after my own signals that it transitively depends on: streams may share a hardware queue,
+    // so a spinning wait must never sit ahead of a signal its peers are waiting for.
+    auto pull = [&](int g) -> int {
+        H2_CUDA(h, launch_p2p_wait(h->sig, g == 0 ? h->d_wait_xl : h->d_wait_xu, g == 0 ? h->n_wait_xl : h->n_wait_xu,
+                                   h->s_comm));
+        for (const auto &pl : h->pulls)
+            if (pl.group == g)
+                H2_CUDA(h, launch_pack<T>(h->d_segs + pl.seg0, pl.nseg, (const T *)h->pmap[pl.owner].xh, h->xh_plane,
+                                          args, (T *)h->xrecv, nv, h->s_comm));
+        return H2_OK;
+    };
     if (p2p && !h->p2p_direct) {
-        // the comm stream pulls the peers' x^ nodes I need into my receive chunks as their flags
-        // arrive (leaf level first), overlapped with my upsweep and diagonal coupling; ev_upleaf
-        // also orders it after my previous call's off-diagonal reads of those chunks
         H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_upleaf, 0));
-        for (int g = 0; g < 2; ++g) {
-            H2_CUDA(h, launch_p2p_wait(h->sig, g == 0 ? h->d_wait_xl : h->d_wait_xu, g == 0 ? h->n_wait_xl : h->n_wait_xu,
-                                       h->s_comm));
-            for (const auto &pl : h->pulls)
-                if (pl.group == g)
-                    H2_CUDA(h, launch_pack<T>(h->d_segs + pl.seg0, pl.nseg, (const T *)h->pmap[pl.owner].xh, h->xh_plane,
-                                              args, (T *)h->xrecv, nv, h->s_comm));
-        }
-        H2_CUDA(h, launch_p2p_signal(h->sig, h->d_tgt_cx, h->n_tgt_cx, h->s_comm));
-        H2_CUDA(h, cudaEventRecord(h->ev_recv, h->s_comm));
+        if ((rc = pull(0)) != H2_OK) return rc;          // leaf level: after my "leaf x^ ready" signal
     }
     for (const Phase &ph : h->coup_leaf) {
         if (cta)
@@ -1654,6 +1656,11 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     }
     H2_MARK(3);
     if (p2p) H2_CUDA(h, launch_p2p_signal(h->sig, h->d_tgt_xu, h->n_tgt_xu, st));   // upper-level x^ ready
+    if (p2p && !h->p2p_direct) {                          // upper levels: after my "upper x^ ready"
+        if ((rc = pull(1)) != H2_OK) return rc;
+        H2_CUDA(h, launch_p2p_signal(h->sig, h->d_tgt_cx, h->n_tgt_cx, h->s_comm));
+        H2_CUDA(h, cudaEventRecord(h->ev_recv, h->s_comm));
+    }
     // 2. exchange (P > 1): pack my x^ nodes that peers need, one NCCL group on the comm stream,
     //    overlapped with the diagonal multiply (alg:optimized_dist_mult); the device-initiated
     //    exchange needs no pack: peers read my x^ plane directly

@@ -4,6 +4,8 @@
 // mappings (st.release.sys) and polled with ld.acquire.sys.
 #include "h2_internal.h"
 
+#include <cstdio>
+
 namespace h2 {
 namespace {
 
@@ -17,12 +19,15 @@ __device__ __forceinline__ void st_rel(int32_t *p, int v)
 {
     asm volatile("st.release.sys.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void spin_until(const int32_t *p, int target)
+__device__ __forceinline__ void spin_until(const int32_t *p, int target, int slot)
 {
     unsigned long long n = 0;
     while (ld_acq(p) < target) {
         __nanosleep(128);
-        if (++n > 150000000ull) __trap();     // ~20 s: a peer is gone; fail loudly instead of hanging
+        if (++n > 150000000ull) {             // ~20 s: a peer is gone; fail loudly instead of hanging
+            printf("h2 p2p: signal slot %d stuck at %d (waiting for %d)\n", slot, ld_acq(p), target);
+            __trap();
+        }
     }
 }
 
@@ -30,7 +35,7 @@ __global__ void k_p2p_begin(int32_t *sig, const int32_t *waits, int nwait)
 {
     const int e = sig[SIG_EPOCH] + 1;
     sig[SIG_EPOCH] = e;
-    for (int i = 0; i < nwait; ++i) spin_until(sig + waits[i], e - 1);
+    for (int i = 0; i < nwait; ++i) spin_until(sig + waits[i], e - 1, waits[i]);
     __threadfence_system();
 }
 
@@ -44,7 +49,7 @@ __global__ void k_p2p_signal(const int32_t *sig, int32_t *const *targets, int n)
 __global__ void k_p2p_wait(const int32_t *sig, const int32_t *offs, int n)
 {
     const int e = sig[SIG_EPOCH];
-    for (int i = 0; i < n; ++i) spin_until(sig + offs[i], e);
+    for (int i = 0; i < n; ++i) spin_until(sig + offs[i], e, offs[i]);
     __threadfence_system();
 }
 
