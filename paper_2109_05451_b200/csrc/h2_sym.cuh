@@ -5,7 +5,7 @@
 // (h2_desc.flags & H2_SYMMETRIC).  A warp owns block row t and applies every stored block (t, s)
 // of it twice from ONE read of the block: directly, y_t += A x_s (registers), and -- for s > t,
 // the "mirrored" blocks -- transposed, y_s += A^T x_t, by a 32-column reduce-scatter across the
-// lanes (31 shuffles per 32 columns) and one red.global.add per column.  Outputs therefore
+// lanes (16 shuffles per 16 columns) and one red.global.add per column.  Outputs therefore
 // accumulate with atomics: the coupling rows into a zeroed y^, the leaves into Y after a beta pass.
 // nv = 1 (the HBM-bound case the halved bytes pay for).
 #pragma once
@@ -16,12 +16,13 @@ namespace sym {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-// lane c ends with sum over lanes of v[c] (v[0] holds it)
+// lanes c and c + 16 end with the sum over all lanes of v[c] (in v[0]): a 16-value reduce-scatter
+// over the lane bits 0..3 (15 shuffles), then one exchange across bit 4
 template <typename T>
-__device__ __forceinline__ void reduce_scatter32(T (&v)[32], int lane)
+__device__ __forceinline__ void reduce_scatter16(T (&v)[16], int lane)
 {
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
+    for (int o = 8; o >= 1; o >>= 1) {
         const bool hi = lane & o;
 #pragma unroll
         for (int i = 0; i < o; ++i) {
@@ -30,6 +31,7 @@ __device__ __forceinline__ void reduce_scatter32(T (&v)[32], int lane)
             v[i] = keep + __shfl_xor_sync(FULL, send, o);
         }
     }
+    v[0] += __shfl_xor_sync(FULL, v[0], 16);
 }
 
 // acc (r rows: lane, lane + 32) += A (r x c, column-major) x_s, x_s held as xs0 / xs1 (rows lane,
@@ -38,21 +40,22 @@ template <typename T, int RPL, bool MIRROR>
 __device__ __forceinline__ void block(T (&acc)[RPL], const T *__restrict__ A, int r, int c, T xs0, T xs1, T xt0,
                                       T xt1, T *ymir, T alpha, int lane)
 {
-    for (int j0 = 0; j0 < c; j0 += 32) {
-        T v[32];
+    for (int j0 = 0; j0 < c; j0 += 16) {
+        T v[16];
+        const T xsrc = j0 < 32 ? xs0 : xs1;
 #pragma unroll
-        for (int u = 0; u < 32; ++u) {
+        for (int u = 0; u < 16; ++u) {
             const int j = j0 + u;
             const T a0 = (j < c && lane < r) ? __ldcs(A + (int64_t)j * r + lane) : T(0);
             const T a1 = (RPL == 2 && j < c && lane + 32 < r) ? __ldcs(A + (int64_t)j * r + lane + 32) : T(0);
-            const T xj = __shfl_sync(FULL, j0 == 0 ? xs0 : xs1, u);
+            const T xj = __shfl_sync(FULL, xsrc, (j0 & 31) + u);
             acc[0] = fma(a0, xj, acc[0]);
             if (RPL == 2) acc[RPL - 1] = fma(a1, xj, acc[RPL - 1]);
             if (MIRROR) v[u] = RPL == 2 ? fma(a1, xt1, a0 * xt0) : a0 * xt0;
         }
         if (MIRROR) {
-            reduce_scatter32(v, lane);
-            if (j0 + lane < c) atomicAdd(ymir + j0 + lane, alpha * v[0]);
+            reduce_scatter16(v, lane);
+            if (lane < 16 && j0 + lane < c) atomicAdd(ymir + j0 + lane, alpha * v[0]);
         }
     }
 }
@@ -80,7 +83,7 @@ __device__ __forceinline__ void apply(T (&acc)[RPL], const Blk &b, int r, int c,
 // x^ and y^ share the plane layout, so Blk::x addresses both x^_s and y^_s and Task::out both y^_t
 // and x^_t.  y^ was zeroed before the launch.
 template <typename T, int RPL>
-__global__ void __launch_bounds__(256) k_sym_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
+__global__ void __launch_bounds__(256, 2) k_sym_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
                                                   const T *__restrict__ xh, T *yh)
 {
     const int lane = threadIdx.x & 31;
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(256) k_sym_rows(const Task *__restrict__ tasks
 // Leaves: z = y^_t + E_t y^_parent ; Y_t += alpha (U_t z + sum_{s >= t} D_ts x_s) ;
 // Y_s += alpha D_ts^T x_t (s > t).  Y was scaled by beta before the launch.
 template <typename T, int RPL>
-__global__ void __launch_bounds__(256) k_sym_leaf(const Task *__restrict__ ltasks, const Task *__restrict__ dtasks,
+__global__ void __launch_bounds__(256, 2) k_sym_leaf(const Task *__restrict__ ltasks, const Task *__restrict__ dtasks,
                                                   int ntask, const Blk *__restrict__ blks, const T *__restrict__ yh,
                                                   const CallArgs<T> *__restrict__ args)
 {

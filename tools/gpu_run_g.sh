@@ -1,0 +1,10 @@
+#!/bin/bash
+# full single-GPU suite + the default bench line + cfg5 / cfg4 / cfg4sym legs
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/g_build.log 2>&1; echo smoke rc=$?
+timeout 1500 python -m pytest tests -m gpu -q -x -rs > gpurun_out/g_pytest.log 2>&1; echo pytest rc=$?
+tail -4 gpurun_out/g_pytest.log
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/g_suite.json 2> gpurun_out/g_suite.err; echo suite rc=$?
+for c in cfg5 cfg4 cfg4sym; do
+timeout 900 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/g_$c.json 2> gpurun_out/g_$c.err; echo $c rc=$?
+done
