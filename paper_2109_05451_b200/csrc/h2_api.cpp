@@ -344,10 +344,6 @@ struct h2_ctx {
     int nsm = 148;
     bool use_cta(int nv) const { return dtype == H2_F64 && nv >= cta_min_nv; }
     int launches_cta = 0;
-    // single cooperative launch for L2-resident operators at nv = 1 (h2_mono.cuh; H2_MONO=0 disables)
-    bool mono = false;
-    MonoPlan mono_plan{};
-    int mono_kmax = 1;
 };
 
 namespace {
@@ -1436,32 +1432,6 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     }
     if (h->has_top) dist += (int)h->top_stages.size();
     h->launches_per_call = launches + dist + (h->sym ? 1 : 0);   // + the beta pass of the symmetric leaves
-    {
-        // latency path: one rank, general storage, operator within ~half of L2
-        const char *mo = getenv("H2_MONO");
-        const bool small = h->ops_stored * (double)h->esz <= 64.0 * (1 << 20);
-        h->mono = P == 1 && !h->sym && (mo ? mo[0] == '1' : small);
-        MonoPlan &mp = h->mono_plan;
-        auto add = [&](const Phase &ph, int kind, int sync) {
-            if (mp.nph >= MONO_MAXPH) { h->mono = false; return; }
-            if (ph.n == 0) { if (sync && mp.nph) mp.ph[mp.nph - 1].sync = 1; return; }
-            mp.ph[mp.nph++] = MonoPhase{ph.t0, ph.n, (int16_t)kind, (int16_t)sync};
-            h->mono_kmax = std::max(h->mono_kmax, ph.r);
-        };
-        add(h->up_leaf, MONO_UPLEAF, 1);
-        // the leaf-level coupling needs only the leaf x^: it shares a phase with the first transfer level
-        for (const Phase &ph : h->coup_leaf) add(ph, MONO_COUP, 0);
-        for (const Phase &ph : h->up_lv) add(ph, MONO_UP, 1);
-        for (size_t i = 0; i < h->coup_diag.size(); ++i) add(h->coup_diag[i], MONO_COUP, i + 1 == h->coup_diag.size());
-        if (mp.nph) mp.ph[mp.nph - 1].sync = 1;
-        for (const Phase &ph : h->down_lv) add(ph, MONO_DOWN, 1);
-        add(h->leaf, MONO_LEAF, 0);
-        mp.dense_t0 = h->dense.t0;
-        mp.k = k[q];
-        mp.kp = q >= 1 ? k[q - 1] : 1;
-        h->mono_kmax = std::max(h->mono_kmax, k[q]);
-        for (int l = 0; l <= q; ++l) h->mono_kmax = std::max(h->mono_kmax, k[l]);
-    }
     // CTA engine: k_set_args, up_leaf, one launch per coupling class / transfer level, the leaves
     h->launches_cta = 3 + (int)h->coup_leaf.size() + (int)h->up_lv.size() + (int)h->coup_diag.size() +
                       (int)h->down_lv.size() + dist;
@@ -1560,11 +1530,6 @@ template <typename T>
 int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
 {
     if (h->sym) return enqueue_sym<T>(h, nv, st);
-    if (h->mono && nv == 1 && !h->prof) {
-        H2_CUDA(h, launch_mono<T>(h->mono_plan, h->d_tasks, h->d_blks, (T *)h->xh, (T *)h->yh, h->xh_plane,
-                                  (const CallArgs<T> *)h->dargs, h->mono_kmax, h->L.m, h->nsm, st));
-        return H2_OK;
-    }
     const Layout &L = h->L;
     const int q = L.q, C = L.C;
     T *xh = (T *)h->xh, *yh = (T *)h->yh;
@@ -2048,7 +2013,7 @@ extern "C" int h2_stats(h2_handle h, int nv, double *flops, double *bytes, doubl
         for (const auto &pr : h->peers) x += (double)(pr.xr_cnt + pr.hr_cnt) * nv * h->esz;
         *xchg_bytes = x;
     }
-    if (launches) *launches = (h->mono && nv == 1) ? 2 : h->use_cta(nv) ? h->launches_cta : h->launches_per_call;
+    if (launches) *launches = h->use_cta(nv) ? h->launches_cta : h->launches_per_call;
     return H2_OK;
 }
 

@@ -158,25 +158,6 @@ cudaError_t launch_p2p_begin(int32_t *sig, const int32_t *waits, int nwait, cuda
 cudaError_t launch_p2p_signal(const int32_t *sig, int32_t *const *targets, int n, cudaStream_t s);
 cudaError_t launch_p2p_wait(const int32_t *sig, const int32_t *offs, int n, cudaStream_t s);
 
-// Single cooperative launch for L2-resident problems (h2_mono.cuh)
-enum { MONO_UP = 0, MONO_COUP = 1, MONO_DOWN = 2, MONO_UPLEAF = 3, MONO_LEAF = 4 };
-constexpr int MONO_MAXPH = 96;
-struct MonoPhase {
-    int64_t t0;        // first task
-    int32_t n;         // tasks
-    int16_t kind;      // MONO_*
-    int16_t sync;      // grid barrier after this phase
-};
-struct MonoPlan {
-    MonoPhase ph[MONO_MAXPH];
-    int64_t dense_t0;  // the dense row of leaf task i is task dense_t0 + i
-    int32_t nph;
-    int32_t k, kp;     // leaf rank and parent rank (MONO_LEAF)
-};
-template <typename T>
-cudaError_t launch_mono(const MonoPlan &mp, const Task *tasks, const Blk *blks, T *xh, T *yh, int64_t plane,
-                        const CallArgs<T> *args, int kmax, int m, int nsm, cudaStream_t s);
-
 // symmetric storage (h2_sym.cuh): blocks with Blk::xld == -1 are also applied transposed
 template <typename T>
 cudaError_t launch_sym_rows(const Task *t, int ntask, const Blk *b, const T *xh, T *yh, int r, cudaStream_t s);

@@ -222,25 +222,3 @@ def test_matvec_ld_larger_leading_dimensions():
     assert colmax_rel(out, oracle.matvec(h, X, -0.5, 0.25, Y0)) <= TOL64
     pad = np.concatenate([Yh[c * ldy + N:(c + 1) * ldy] for c in range(nv)])
     assert np.all(pad == 123.0)
-
-
-@pytest.mark.parametrize("mono", ["0", "1"])
-@pytest.mark.parametrize("name,dtype", [("cfg1", "f64"), ("cfg1grid", "f64"), ("cfg1", "f32")])
-def test_latency_path(mono, name, dtype, monkeypatch):
-    """nv = 1 on an L2-resident operator: the single cooperative launch (H2_MONO=1, default there)
-    and the staged launches (H2_MONO=0) both match the oracle; the launch count drops to 2."""
-    monkeypatch.setenv("H2_MONO", mono)
-    h = build_config(name)
-    hh = h.astype(np.float32) if dtype == "f32" else h
-    X = make_xy(h.perm, 1, 9, -1.0, 1.0)
-    Y0 = make_xy(h.perm, 1, 10, -1.0, 1.0, stream=1)
-    if dtype == "f32":
-        X, Y0 = X.astype(np.float32).astype(np.float64), Y0.astype(np.float32).astype(np.float64)
-    op = _op(hh, nv_max=4, dtype=dtype)
-    for _ in range(3):                                   # eager, capture, graph replay
-        out = gpu_matvec(op, X, -0.7, 0.3, Y0, dtype)
-    launches = op.stats(1)["launches"]
-    op.close()
-    ref = oracle.matvec(hh.astype(np.float64) if dtype == "f32" else h, X, -0.7, 0.3, Y0)
-    assert colmax_rel(out, ref) <= (TOL64 if dtype == "f64" else TOL32)
-    assert (launches == 2) == (mono == "1")
