@@ -395,7 +395,15 @@ def run_leg(leg, args, P, rank, dev, pkg, torch, dist, want_cpu, samplers, laten
         del Xh, Yh
     # roofline of the leg's dominant kernel (largest summed phase time)
     pk = fp_peaks()
-    kof = pkg._binding.KERNEL_OF_PHASE
+    kof = dict(pkg._binding.KERNEL_OF_PHASE)
+    if dtype == "f64" and max(nvs) > 16 and not name.endswith(":sym"):   # the CTA-tile engine runs these legs
+        kof.update({"up_leaf": "k_cta<leaf projection>", "up_transfer": "k_cta<upsweep levels>",
+                    "coupling_diag": "k_cta<coupling rows>", "coupling_leaf": "k_cta<coupling rows>",
+                    "coupling_offdiag": "k_cta<coupling rows, off-diagonal>", "down_transfer": "k_cta<downsweep levels>",
+                    "leaf_u": "k_cta<leaves: expansion + dense + epilogue>", "dense": "k_cta<leaves: expansion + dense + epilogue>"})
+    if name.endswith(":sym"):
+        kof.update({"coupling_diag": "k_sym_rows", "coupling_leaf": "k_sym_rows", "leaf_u": "k_sym_leaf",
+                    "dense": "k_sym_leaf"})
     step_ph = {k: sum(per_nv_ph[nv].get(k, 0.0) for nv in nvs) for k in pkg.PHASES}
     groups = {}
     for k in pkg.PHASES:
