@@ -504,7 +504,7 @@ def main():
     if args.no_extra or args.profile_only:
         extra = []
     legs_p = [lg for nm in prim for lg in legs_of(nm)]
-    legs_x = [lg for nm in extra for lg in legs_of(nm)]
+    legs_x = [lg for nm in extra for lg in legs_of(nm) if not (P > 1 and lg[0].endswith(":sym"))]   # one rank only
     want_cpu = (P == 1 and rk == 0 and not args.no_cpu_baseline and not args.profile_only)
     samplers = []
     res_p = [run_leg(lg, args, P, rk, dev, pkg, torch, dist, want_cpu, samplers, latency=(lg[0] == "cfg1"))
