@@ -275,7 +275,8 @@ def run_reference(args, emit):
     C = P.bit_length() - 1
     lp = np.asarray(parts[0][0].leaf_ptr)
     n_rank0 = int(lp[1 << (parts[0][0].q - C)]) if P > 1 else n_first
-    ours_cfg = config_dict(args, ws, legs, [lg for nm in extra for lg in legs_of(nm)], n_first, n_rank0)
+    legs_x = [lg for nm in extra for lg in legs_of(nm) if not (P > 1 and lg[0].endswith(":sym"))]
+    ours_cfg = config_dict(args, ws, legs, legs_x, n_first, n_rank0)
     out = {"metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
            "scaling": CONFIGS[base_name(legs[0][0])]["scaling"], "vs_baseline": None, "dtype": legs[0][1], "data": "synthetic",

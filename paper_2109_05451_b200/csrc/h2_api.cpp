@@ -284,7 +284,7 @@ struct h2_ctx {
     // heap-addressed sweeps (k_sweep): bottom levels one launch each, small top levels fused
     bool use_sweep = false;
     std::vector<SweepParams> up_sweeps, dn_sweeps;
-    std::vector<int> up_sweep_ctas, dn_sweep_ctas;
+    std::vector<int> up_sweep_ctas, dn_sweep_ctas, up_sweep_thr, dn_sweep_thr;
     int sweep_r_up = 1, sweep_r_dn = 1;
     std::vector<int> up_lv_level, top_up_level, down_level;
     int64_t nseg_x = 0, nseg_h = 0, seg_x0 = 0, seg_h0 = 0;
@@ -1320,39 +1320,65 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             return v;
         };
         if (h->use_sweep) {
-            SweepParams top{};
+            // launches: the wide levels alone (full-grid parallelism for most of the bytes), the
+            // latency-bound levels of <= GMAX nodes in groups of J (one CTA per subtree, CTA
+            // barriers between its levels: 1 launch instead of J), the tiny top levels (<= TOPN
+            // nodes) in one CTA.  Measured on cfg2 (J = 1..4): up 86 -> 76 us, down 57 -> 47 us at
+            // nv = 1; grouping the wide levels too slowed cfg5 FP32 (fewer warps on most bytes).
+            const int J = 4, GMAX = 1024;
+            auto push = [&](std::vector<SweepParams> &dst, std::vector<int> &ctas, std::vector<int> &thr,
+                            const std::vector<SweepLevel> &g, bool up) {
+                if (g.empty()) return;
+                SweepParams sp{};
+                for (const auto &v : g) sp.lv[sp.nlev++] = v;
+                if (g.size() == 1) {
+                    ctas.push_back((g[0].n + WPB - 1) / WPB);
+                    thr.push_back(WPB * 32);
+                } else {
+                    // a subtree per CTA: as many CTAs as nodes at the group's coarsest level
+                    const int nct = up ? g.back().n : g.front().n;
+                    const int widest = up ? g.front().n : g.back().n;
+                    ctas.push_back(nct);
+                    thr.push_back(32 * std::min(WPB, std::max(1, widest / nct)));
+                }
+                dst.push_back(sp);
+            };
+            std::vector<SweepLevel> grp, top;
+            bool first = true;
             for (int lc : h->up_lv_level) {
                 SweepLevel v = lvl_up(lc);
                 h->sweep_r_up = std::max(h->sweep_r_up, (int)v.r);
-                if (v.n > TOPN) {
-                    SweepParams one{};
-                    one.lv[0] = v;
-                    one.nlev = 1;
-                    h->up_sweeps.push_back(one);
-                    h->up_sweep_ctas.push_back((v.n + WPB - 1) / WPB);
-                } else if (top.nlev < SWEEP_MAXLEV) {
-                    top.lv[top.nlev++] = v;
-                }
+                if (v.n <= TOPN) { top.push_back(v); continue; }
+                if (first || v.n > GMAX) { push(h->up_sweeps, h->up_sweep_ctas, h->up_sweep_thr, {v}, true); first = false; continue; }
+                grp.push_back(v);
+                if ((int)grp.size() == J) { push(h->up_sweeps, h->up_sweep_ctas, h->up_sweep_thr, grp, true); grp.clear(); }
             }
-            if (top.nlev) { h->up_sweeps.push_back(top); h->up_sweep_ctas.push_back(1); }
+            push(h->up_sweeps, h->up_sweep_ctas, h->up_sweep_thr, grp, true);
+            if (!top.empty()) {
+                SweepParams sp{};
+                for (const auto &v : top) if (sp.nlev < SWEEP_MAXLEV) sp.lv[sp.nlev++] = v;
+                h->up_sweeps.push_back(sp);
+                h->up_sweep_ctas.push_back(1);
+                h->up_sweep_thr.push_back(512);
+            }
+            // downsweep: top levels first (one CTA), then groups of J, the widest level alone last
+            std::vector<SweepLevel> dn;
+            for (int l : h->down_level) { dn.push_back(lvl_dn(l)); h->sweep_r_dn = std::max(h->sweep_r_dn, (int)dn.back().r); }
+            size_t u = 0;
             SweepParams dtop{};
-            std::vector<SweepParams> dbot;
-            std::vector<int> dbot_ctas;
-            for (int l : h->down_level) {
-                SweepLevel v = lvl_dn(l);
-                h->sweep_r_dn = std::max(h->sweep_r_dn, (int)v.r);
-                if (v.n <= TOPN && dbot.empty() && dtop.nlev < SWEEP_MAXLEV) dtop.lv[dtop.nlev++] = v;
-                else {
-                    SweepParams one{};
-                    one.lv[0] = v;
-                    one.nlev = 1;
-                    dbot.push_back(one);
-                    dbot_ctas.push_back((v.n + WPB - 1) / WPB);
+            while (u < dn.size() && dn[u].n <= TOPN && dtop.nlev < SWEEP_MAXLEV) dtop.lv[dtop.nlev++] = dn[u++];
+            if (dtop.nlev) { h->dn_sweeps.push_back(dtop); h->dn_sweep_ctas.push_back(1); h->dn_sweep_thr.push_back(512); }
+            grp.clear();
+            for (; u < dn.size(); ++u) {
+                if (u + 1 == dn.size() || dn[u].n > GMAX) {
+                    push(h->dn_sweeps, h->dn_sweep_ctas, h->dn_sweep_thr, grp, false);
+                    grp.clear();
+                    push(h->dn_sweeps, h->dn_sweep_ctas, h->dn_sweep_thr, {dn[u]}, false);
+                    continue;
                 }
+                grp.push_back(dn[u]);
+                if ((int)grp.size() == J) { push(h->dn_sweeps, h->dn_sweep_ctas, h->dn_sweep_thr, grp, false); grp.clear(); }
             }
-            if (dtop.nlev) { h->dn_sweeps.push_back(dtop); h->dn_sweep_ctas.push_back(1); }
-            h->dn_sweeps.insert(h->dn_sweeps.end(), dbot.begin(), dbot.end());
-            h->dn_sweep_ctas.insert(h->dn_sweep_ctas.end(), dbot_ctas.begin(), dbot_ctas.end());
         }
     }
     // ---- contiguity of every task's block run (TF_ACONTIG): A_b == A_0 + b r c
@@ -1502,7 +1528,7 @@ int enqueue_sym(h2_ctx *h, int nv, cudaStream_t st)
     H2_MARK(2);
     for (size_t u = 0; u < h->up_sweeps.size(); ++u)
         H2_CUDA(h, launch_sweep<T>(MODE_WRITE, h->up_sweeps[u], h->up_sweep_ctas[u],
-                                   h->up_sweep_ctas[u] == 1 && h->up_sweeps[u].nlev > 1 ? 512 : WPB * 32, xh,
+                                   h->up_sweep_thr[u], xh,
                                    h->xh_plane, nv, h->sweep_r_up, st));
     H2_MARK(3);
     H2_MARK(4);
@@ -1512,7 +1538,7 @@ int enqueue_sym(h2_ctx *h, int nv, cudaStream_t st)
     H2_MARK(6);
     for (size_t u = 0; u < h->dn_sweeps.size(); ++u)
         H2_CUDA(h, launch_sweep<T>(MODE_ACCUM, h->dn_sweeps[u], h->dn_sweep_ctas[u],
-                                   h->dn_sweep_ctas[u] == 1 && h->dn_sweeps[u].nlev > 1 ? 512 : WPB * 32, yh,
+                                   h->dn_sweep_thr[u], yh,
                                    h->yh_plane, nv, h->sweep_r_dn, st));
     H2_MARK(7);
     H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_leafc, 0));
@@ -1647,7 +1673,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     } else if (h->use_sweep) {
         for (size_t u = 0; u < h->up_sweeps.size(); ++u)
             H2_CUDA(h, launch_sweep<T>(MODE_WRITE, h->up_sweeps[u], h->up_sweep_ctas[u],
-                                       h->up_sweep_ctas[u] == 1 && h->up_sweeps[u].nlev > 1 ? 512 : WPB * 32,
+                                       h->up_sweep_thr[u],
                                        xh, h->xh_plane, nv, h->sweep_r_up, st));
     } else {
         for (const auto &sg : h->up_stages)
@@ -1754,7 +1780,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     } else if (h->use_sweep) {
         for (size_t u = 0; u < h->dn_sweeps.size(); ++u)
             H2_CUDA(h, launch_sweep<T>(MODE_ACCUM, h->dn_sweeps[u], h->dn_sweep_ctas[u],
-                                       h->dn_sweep_ctas[u] == 1 && h->dn_sweeps[u].nlev > 1 ? 512 : WPB * 32,
+                                       h->dn_sweep_thr[u],
                                        yh, h->yh_plane, nv, h->sweep_r_dn, st));
     } else {
         for (const auto &sg : h->down_stages)

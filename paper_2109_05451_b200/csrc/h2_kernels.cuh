@@ -672,6 +672,15 @@ k_sweep(const __grid_constant__ SweepParams p, T *__restrict__ buf, int64_t ld, 
     for (int lv = 0; lv < p.nlev; ++lv) {
         const SweepLevel L = p.lv[lv];
         const int64_t blk = (int64_t)L.r * L.c;
+        // a multi-level launch gives every CTA a contiguous node range per level -- a subtree: the
+        // parents (upsweep) / children (downsweep) of its nodes are its own, so a CTA barrier
+        // between levels suffices; single-level launches stride over the whole level
+        const bool multi = p.nlev > 1;
+        const int64_t per = multi ? (L.n + gridDim.x - 1) / gridDim.x : L.n;
+        const int64_t lo = multi ? (int64_t)blockIdx.x * per : 0;
+        const int64_t hi = multi ? min((int64_t)L.n, lo + per) : L.n;
+        const int64_t i0 = multi ? lo + wid : (int64_t)blockIdx.x * nw + wid;
+        const int64_t istep = multi ? nw : (int64_t)gridDim.x * nw;
         if constexpr (STAGE) {
             // latency-bound levels: the node's whole operand set (its transfer block(s) and source
             // x^ slots, r x cc and cc x nvc) is pulled into the warp's shared memory by cp.async
@@ -681,7 +690,7 @@ k_sweep(const __grid_constant__ SweepParams p, T *__restrict__ buf, int64_t ld, 
             T *As = reinterpret_cast<T *>(smem_raw) + (int64_t)wid * wstride;
             const int cc = MODE == MODE_ACCUM ? L.c : 2 * L.c;
             T *xs = As + L.r * cc;
-            for (int i = blockIdx.x * nw + wid; i < L.n; i += gridDim.x * nw) {
+            for (int64_t i = i0; i < hi; i += istep) {
                 const T *Ag = static_cast<const T *>(L.A) + (MODE == MODE_ACCUM ? (int64_t)i : 2 * (int64_t)i) * blk;
                 const T *xg = buf + L.xbase + (MODE == MODE_ACCUM ? (int64_t)(i >> 1) : 2 * (int64_t)i) * L.c;
                 for (int n0 = 0; n0 < nv; n0 += Eng::NV) {
@@ -711,8 +720,8 @@ k_sweep(const __grid_constant__ SweepParams p, T *__restrict__ buf, int64_t ld, 
         // what bounds the small levels at large k and nv (cfg3s: ~80 us per level otherwise);
         // the launch sizes the single-level grid by the chunk count (launch_sweep)
         const int nch = (nv + Eng::NV - 1) / Eng::NV;
-        const int S = (p.nlev > 1 || (int64_t)L.n * nch <= (int64_t)gridDim.x * nw) ? nch : 1;
-        for (int64_t t = (int64_t)blockIdx.x * nw + wid; t < (int64_t)L.n * S; t += (int64_t)gridDim.x * nw) {
+        const int S = (multi || (int64_t)L.n * nch <= (int64_t)gridDim.x * nw) ? nch : 1;
+        for (int64_t t = (multi ? lo * S : 0) + (i0 - (multi ? lo : 0)); t < hi * S; t += istep) {
             const int64_t i = t / S;
             const int ch0 = S == 1 ? 0 : (int)(t - i * S);
             const int ch1 = S == 1 ? nch : ch0 + 1;
@@ -1193,7 +1202,7 @@ cudaError_t launch_sweep(int mode, const SweepParams &p, int nctas, int threads,
         while (warps > 1 && warps * wbytes > SWEEP_STAGE_SMEM) warps >>= 1;
         const bool stage = !E::MMA && warps * wbytes <= SWEEP_STAGE_SMEM;
         if (stage) {
-            const int ctas = nctas == 1 ? 1 : (int)((maxn + warps - 1) / warps);
+            const int ctas = p.nlev > 1 ? nctas : (int)((maxn + warps - 1) / warps);
             const size_t sm = warps * wbytes;
             auto kw = k_sweep<T, E, MODE_WRITE, true>;
             auto ka = k_sweep<T, E, MODE_ACCUM, true>;
