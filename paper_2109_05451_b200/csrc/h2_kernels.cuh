@@ -567,6 +567,141 @@ struct Mma {
     { mma_block<MT, NT, false>(acc, As, r, c, xs, xld, c, nvc, lane, r); }
 };
 
+// =========================================================================== FP32 tensor engine
+// FP32 on the tensor cores by the 3xTF32 split: a = a_hi + a_lo with a_hi =
+// tf32(a), a_lo = tf32(a - a_hi); a b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi (the dropped a_lo b_lo is
+// ~2^-22 relative), accumulated in FP32 by mma.sync.m16n8k8.tf32 -- FP32-level accuracy (parity
+// <= 1e-5 against the FP64 oracle) at tensor-core throughput, so FP32 at nv >= 5 is bound by HBM
+// instead of by FFMA issue (the SIMT stream reached 0.32-0.37 of HBM on cfg5).
+// Fragments (PTX m16n8k8 .tf32, g = lane / 4, t = lane % 4):
+//   A 16x8: a0 (g, t), a1 (g+8, t), a2 (g, t+4), a3 (g+8, t+4);  B 8x8: b0 (t, g), b1 (t+4, g);
+//   C 16x8: c0 (g, 2t), c1 (g, 2t+1), c2 (g+8, 2t), c3 (g+8, 2t+1).
+template <int MT, int NT>
+struct TfAcc {
+    float v[MT][NT][4];
+    template <typename F>
+    __device__ __forceinline__ void each(int lane, F f) {
+        const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) f(mt * 16 + g + (i >> 1) * 8, nt * 8 + 2 * t + (i & 1), v[mt][nt][i]);
+    }
+};
+
+__device__ __forceinline__ void tf32_split(float x, uint32_t &hi, uint32_t &lo)
+{
+    asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(hi) : "f"(x));
+    const float r = x - __uint_as_float(hi);
+    asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(lo) : "f"(r));
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1)
+{
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};\n"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int MT, int NT>
+struct TfFrag {
+    float a[MT][4], b[NT][2];
+};
+
+// fragments of k-step ks (columns 8ks .. 8ks+7) of A (r x c, col-major, lda) and B (c x nvc at
+// src[j + n ld]; rows >= xrows and vectors >= nvc are zero)
+template <int MT, int NT, bool A_STREAM>
+__device__ __forceinline__ void tf_load(TfFrag<MT, NT> &f, const float *__restrict__ A, int r, int c, int lda,
+                                        const float *src, int64_t ld, int xrows, int nvc, int ks, int g, int t)
+{
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int row = mt * 16 + g + (i & 1) * 8, col = ks * 8 + t + (i >> 1) * 4;
+            const float *p = A + (int64_t)col * lda + row;
+            f.a[mt][i] = (row < r && col < c) ? (A_STREAM ? __ldcs(p) : *p) : 0.f;
+        }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int row = ks * 8 + t + i * 4, n = nt * 8 + g;
+            f.b[nt][i] = (row < xrows && row < c && n < nvc) ? src[row + n * ld] : 0.f;
+        }
+}
+
+template <int MT, int NT>
+__device__ __forceinline__ void tf_mma(TfAcc<MT, NT> &acc, const TfFrag<MT, NT> &f)
+{
+    uint32_t ah[MT][4], al[MT][4], bh[NT][2], bl[NT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tf32_split(f.a[mt][i], ah[mt][i], al[mt][i]);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) tf32_split(f.b[nt][i], bh[nt][i], bl[nt][i]);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            mma_tf32(acc.v[mt][nt], al[mt], bh[nt][0], bh[nt][1]);     // small terms first
+            mma_tf32(acc.v[mt][nt], ah[mt], bl[nt][0], bl[nt][1]);
+            mma_tf32(acc.v[mt][nt], ah[mt], bh[nt][0], bh[nt][1]);
+        }
+}
+
+// acc += A (r x c) B (c x nvc), fragments of k-step ks+1 loaded behind the MMAs of k-step ks
+template <int MT, int NT, bool A_STREAM>
+__device__ __forceinline__ void tf_block(TfAcc<MT, NT> &acc, const float *__restrict__ A, int r, int c, int lda,
+                                         const float *src, int64_t ld, int xrows, int nvc, int lane)
+{
+    const int g = lane >> 2, t = lane & 3;
+    const int ksn = (c + 7) >> 3;
+    TfFrag<MT, NT> f[2];
+    tf_load<MT, NT, A_STREAM>(f[0], A, r, c, lda, src, ld, xrows, nvc, 0, g, t);
+    for (int ks = 0; ks < ksn; ++ks) {
+        if (ks + 1 < ksn) tf_load<MT, NT, A_STREAM>(f[(ks + 1) & 1], A, r, c, lda, src, ld, xrows, nvc, ks + 1, g, t);
+        tf_mma(acc, f[ks & 1]);
+    }
+}
+
+template <int MT, int NT>
+struct Tf3 {
+    using Acc = TfAcc<MT, NT>;
+    static constexpr int NV = 8 * NT;
+    static constexpr int MINB = 2;
+    static constexpr bool SIMT1 = false;
+    static constexpr bool MMA = true;
+    static constexpr int SCRATCH = 32;
+    __device__ static void block(Acc &acc, const float *A, int r, int c, const float *src, int64_t ld, int xrows,
+                                 int nvc, int lane, int lda = -1)
+    { tf_block<MT, NT, true>(acc, A, r, c, lda < 0 ? r : lda, src, ld, xrows, nvc, lane); }
+    __device__ static void block_wide(Acc &acc, const float *A, int r, int c, const float *src, int64_t ld, int xrows,
+                                      int nvc, int lane)
+    { tf_block<MT, NT, true>(acc, A, r, c, r, src, ld, xrows, nvc, lane); }
+    // a contiguous run of blocks: one block at a time, each with its own x source
+    __device__ static void stream(Acc &acc, const float *A0, int r, int c, int nblk, const Blk *blks,
+                                  const Src<float> &src, int nvc, int lane, void *, int lda = -1)
+    {
+        const int la = lda < 0 ? r : lda;
+        for (int b = 0; b < nblk; ++b) {
+            const Blk bk = blks[b];
+            int64_t ld;
+            const float *x = resolve(src, bk.x, bk.xld, ld);
+            tf_block<MT, NT, true>(acc, A0 + (int64_t)b * la * c, r, c, la, x, ld, bk.xrows, nvc, lane);
+        }
+    }
+    __device__ static void smem_block(Acc &acc, const float *As, int r, int c, const float *xs, int xld, int nvc,
+                                      int lane)
+    { tf_block<MT, NT, false>(acc, As, r, c, r, xs, xld, c, nvc, lane); }
+};
+
 // ---------------------------------------------------------------------------------------
 // Upsweep leaves: x^_s (k x nv) = Vt_s (k x m) x_s (m x nv), Vt = V^T re-laid out at create.
 template <typename T, typename Eng>
@@ -1020,7 +1155,8 @@ static inline cudaError_t smem_opt_in(K kern, size_t bytes)
 
 template <typename T>
 struct Dispatch {
-    // f(Eng) with Eng chosen from (rows r -> RPL / MT, nv -> NVB / NT)
+    // f(Eng) with Eng chosen from (rows r -> RPL / MT, nv -> NVB / NT): FP32 runs SIMT up to nv = 4
+    // and the 3xTF32 tensor engine above
     template <typename F>
     static void run(int r, int nv, F f)
     {
@@ -1028,8 +1164,11 @@ struct Dispatch {
         if (nv <= 1) { if (rpl == 1) f(Simt<T, 1, 1>{}); else f(Simt<T, 2, 1>{}); }
         else if (nv <= 2) { if (rpl == 1) f(Simt<T, 1, 2>{}); else f(Simt<T, 2, 2>{}); }
         else if (nv <= 4) { if (rpl == 1) f(Simt<T, 1, 4>{}); else f(Simt<T, 2, 4>{}); }
-        else if (nv <= 8) { if (rpl == 1) f(Simt<T, 1, 8>{}); else f(Simt<T, 2, 8>{}); }
-        else { if (rpl == 1) f(Simt<T, 1, 16>{}); else f(Simt<T, 2, 16>{}); }
+        else if (nv <= 8) {
+            if (r <= 16) f(Tf3<1, 1>{}); else if (r <= 32) f(Tf3<2, 1>{}); else f(Tf3<4, 1>{});
+        } else {
+            if (r <= 16) f(Tf3<1, 2>{}); else if (r <= 32) f(Tf3<2, 2>{}); else f(Tf3<4, 2>{});
+        }
     }
     template <typename F>
     static void run2(int rk, int rm, int nv, F f)

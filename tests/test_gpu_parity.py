@@ -222,3 +222,17 @@ def test_matvec_ld_larger_leading_dimensions():
     assert colmax_rel(out, oracle.matvec(h, X, -0.5, 0.25, Y0)) <= TOL64
     pad = np.concatenate([Yh[c * ldy + N:(c + 1) * ldy] for c in range(nv)])
     assert np.all(pad == 123.0)
+
+
+@pytest.mark.parametrize("N,m,k,nv,eta,seed", [
+    (3000, 32, 16, 5, 0.9, 61), (5000, 64, 25, 8, 0.9, 62), (5000, 64, 25, 16, 0.9, 63),
+    (4000, 64, 36, 17, 0.9, 64), (4000, 64, 64, 16, 1.1, 65), (2500, 48, 40, 33, 0.9, 66)])
+def test_fp32_tensor_engine(N, m, k, nv, eta, seed):
+    """FP32 at nv >= 5 runs the 3xTF32 tensor engine (Tf3): within 1e-5 of the FP64 oracle on the
+    FP32-rounded operator and vectors, ragged leaves, nv inside and across the 8/16-vector chunks."""
+    h = random_case(N, m, lambda l: k, seed, eta=eta).astype(np.float32)
+    X = make_xy(h.perm, nv, seed, -1.0, 1.0).astype(np.float32).astype(np.float64)
+    Y0 = make_xy(h.perm, nv, seed + 1, -1.0, 1.0, stream=1).astype(np.float32).astype(np.float64)
+    out = gpu_matvec(_op(h, nv_max=max(nv, 16), dtype="f32"), X, -0.6, 1.3, Y0, "f32")
+    ref = oracle.matvec(h.astype(np.float64), X, -0.6, 1.3, Y0)
+    assert colmax_rel(out, ref) <= TOL32
