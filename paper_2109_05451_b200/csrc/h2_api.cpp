@@ -277,7 +277,7 @@ struct h2_ctx {
     Task *d_tasks = nullptr;
     Blk *d_blks = nullptr;
     PackSeg *d_segs = nullptr;
-    Phase up_leaf, coup_off[3], leaf, dense;
+    Phase up_leaf, coup_off[3], coup_off_leaf[3], leaf, dense;   // off-diagonal: upper levels / leaf level
     std::vector<Phase> up_lv, top_up_lv, coup_diag, coup_leaf, down_lv;
     struct Stage { TreeStage st; int nctas; int r; };
     std::vector<Stage> up_stages, top_stages, down_stages;
@@ -1090,8 +1090,8 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     }
     // (4) coupling multiply, diagonal part, all levels in one launch per engine class
     //     (PAPER.md:328-331, 496); every held row gets a task (empty rows write 0)
-    std::vector<Task> offd_tasks[3];
-    std::vector<Blk> offd_blks[3];
+    std::vector<Task> offd_tasks[2][3];    // [leaf level, upper levels][class]
+    std::vector<Blk> offd_blks[2][3];
     std::vector<Task> p2p_tasks[2][3];     // [leaf level, upper levels][class]
     std::vector<Blk> p2p_blks[2][3];
     std::vector<int> p2p_owner[2][3];
@@ -1148,11 +1148,12 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
                         p2p_blks[g][ci].insert(p2p_blks[g][ci].end(), kv.second.begin(), kv.second.end());
                     }
                 } else if (!offb.empty()) {
+                    const int g = (l == q) ? 0 : 1;
                     Task to = t;
                     to.nblk = (int32_t)offb.size();
-                    to.blk0 = (int64_t)offd_blks[ci].size();
-                    offd_tasks[ci].push_back(to);
-                    offd_blks[ci].insert(offd_blks[ci].end(), offb.begin(), offb.end());
+                    to.blk0 = (int64_t)offd_blks[g][ci].size();
+                    offd_tasks[g][ci].push_back(to);
+                    offd_blks[g][ci].insert(offd_blks[g][ci].end(), offb.begin(), offb.end());
                 }
             }
         }
@@ -1195,14 +1196,16 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
                     h->p2p_phases.push_back(pp);
                 }
             }
-        for (int ci = 0; ci < 3; ++ci) {
-            h->coup_off[ci].t0 = tasks.size();
-            h->coup_off[ci].r = cls_r[ci];
-            h->coup_off[ci].n = (int)offd_tasks[ci].size();
-            int64_t b0 = (int64_t)blks.size();
-            for (Task t : offd_tasks[ci]) { t.blk0 += b0; tasks.push_back(t); }
-            blks.insert(blks.end(), offd_blks[ci].begin(), offd_blks[ci].end());
-        }
+        for (int g = 0; g < 2; ++g)
+            for (int ci = 0; ci < 3; ++ci) {
+                Phase &ph = g == 0 ? h->coup_off_leaf[ci] : h->coup_off[ci];
+                ph.t0 = tasks.size();
+                ph.r = cls_r[ci];
+                ph.n = (int)offd_tasks[g][ci].size();
+                int64_t b0 = (int64_t)blks.size();
+                for (Task t : offd_tasks[g][ci]) { t.blk0 += b0; tasks.push_back(t); }
+                blks.insert(blks.end(), offd_blks[g][ci].begin(), offd_blks[g][ci].end());
+            }
     }
     // (5) downsweep transfers y^_c += E_c y^_parent, levels 1 .. q-1;
     //     top levels only when the top tree has couplings (else they are all zero)
@@ -1448,11 +1451,11 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     int dist = 0;
     if (P > 1 && !h->p2p) {
         dist += 2;   // pack x^, pack halo
-        for (int ci = 0; ci < 3; ++ci) dist += h->coup_off[ci].n ? 1 : 0;
+        for (int ci = 0; ci < 3; ++ci) dist += (h->coup_off[ci].n ? 1 : 0) + (h->coup_off_leaf[ci].n ? 1 : 0);
     } else if (P > 1) {
         dist += 2 + (int)h->p2p_phases.size() + (int)h->pulls.size();   // p2p_begin, pack halo, off-diagonal / pulls
         if (!h->p2p_direct)
-            for (int ci = 0; ci < 3; ++ci) dist += h->coup_off[ci].n ? 1 : 0;
+            for (int ci = 0; ci < 3; ++ci) dist += (h->coup_off[ci].n ? 1 : 0) + (h->coup_off_leaf[ci].n ? 1 : 0);
         dist += (h->n_tgt_h > 0) + (h->n_wait_h > 0) + (h->n_tgt_ch > 0) + (h->n_tgt_xl > 0) + (h->n_tgt_xu > 0) +
                 (h->n_wait_xl > 0) + (h->n_wait_xu > 0) + (h->n_tgt_cx > 0) + (h->has_top && h->n_wait_xu > 0);
     }
@@ -1591,6 +1594,17 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
         return j;
     };
     const bool p2p = nccl && h->p2p;
+    auto offdiag = [&](const Phase *grp, cudaStream_t s) -> int {     // off-diagonal rows from xrecv
+        for (int ci = 0; ci < 3; ++ci) {
+            const Phase &ph = grp[ci];
+            if (cta)
+                H2_CUDA(h, launch_cta(cjob(ph, CK_ROWS, MODE_ACCUM, h->xrecv, 0, yh, h->yh_plane), ph.r, h->nsm, s));
+            else
+                H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(ph), ph.n, h->d_blks, (const T *)h->xrecv, 0, yh,
+                                          h->yh_plane, nv, ph.r, s));
+        }
+        return H2_OK;
+    };
     if (part != PART_DOWN) {
     H2_MARK(0);
     // 0. x-leaf halo for the off-process dense blocks (P > 1): X is an input, so the exchange
@@ -1665,6 +1679,12 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
                                       nv, ph.r, s_leafc));
     }
     H2_CUDA(h, cudaEventRecord(h->ev_leafc, s_leafc));
+    if (p2p && !h->p2p_direct) {
+        // the leaf-level off-diagonal blocks as soon as their x^ is pulled (most of the
+        // off-diagonal work), after the leaf-level diagonal coupling wrote those rows
+        H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_leafc, 0));
+        if ((rc = offdiag(h->coup_off_leaf, h->s_comm)) != H2_OK) return rc;
+    }
     H2_MARK(2);
     // 1c. upsweep transfers of the local branch
     if (cta) {
@@ -1763,14 +1783,9 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     } else if (L.P > 1) {
         H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_leafc, 0));
         if (nccl) H2_CUDA(h, cudaStreamWaitEvent(st, h->ev_recv, 0));     // NCCL receive or p2p pulls
-        for (int ci = 0; ci < 3; ++ci) {
-            const Phase &ph = h->coup_off[ci];
-            if (cta)
-                H2_CUDA(h, launch_cta(cjob(ph, CK_ROWS, MODE_ACCUM, h->xrecv, 0, yh, h->yh_plane), ph.r, h->nsm, st));
-            else
-                H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(ph), ph.n, h->d_blks, (const T *)h->xrecv, 0, yh,
-                                          h->yh_plane, nv, ph.r, st));
-        }
+        // the leaf-level group already ran on the comm stream in the p2p pull mode
+        if (!(p2p && !h->p2p_direct) && (rc = offdiag(h->coup_off_leaf, st)) != H2_OK) return rc;
+        if ((rc = offdiag(h->coup_off, st)) != H2_OK) return rc;
     }
     H2_MARK(6);
     // 5. downsweep transfers (alg:downsweep)
