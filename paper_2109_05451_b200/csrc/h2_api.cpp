@@ -343,6 +343,10 @@ struct h2_ctx {
     int cta_min_nv = 17;
     int nsm = 148;
     bool use_cta(int nv) const { return dtype == H2_F64 && nv >= cta_min_nv; }
+    // tcgen05 FP32 row engine (h2_umma.cuh) for the coupling rows at nv >= umma_min_nv
+    // (H2_ENGINE=warp: never; below it the SIMT engines)
+    int umma_min_nv = 5;
+    bool use_umma(int nv) const { return dtype == H2_F32 && nv >= umma_min_nv; }
     int launches_cta = 0;
 };
 
@@ -748,7 +752,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, dev);
         const char *en = getenv("H2_ENGINE");
-        if (en && !strcmp(en, "warp")) h->cta_min_nv = 1 << 30;
+        if (en && !strcmp(en, "warp")) { h->cta_min_nv = 1 << 30; h->umma_min_nv = 1 << 30; }
         else if (en && !strcmp(en, "cta")) h->cta_min_nv = 1;
     }
     // ---- operator arrays on the device; V and F re-laid out as V^T, F^T (operand order)
@@ -1593,15 +1597,20 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
         j.nv = nv;
         return j;
     };
+    const bool umma = !cta && h->use_umma(nv);
+    // one coupling-row launch on the engine of this nv (CTA-tile FP64 / tcgen05 FP32 / warp tasks)
+    auto rows = [&](int mode, const Phase &ph, const void *src, int64_t src_ld, void *dst, int64_t dst_ld,
+                    cudaStream_t s) -> cudaError_t {
+        if (cta) return launch_cta(cjob(ph, CK_ROWS, mode, src, src_ld, dst, dst_ld), ph.r, h->nsm, s);
+        if (umma)
+            return launch_umma_rows(mode, T0(ph), ph.n, h->d_blks, (const float *)src, src_ld, (float *)dst, dst_ld,
+                                    nv, h->nsm, s);
+        return launch_rows<T>(mode, T0(ph), ph.n, h->d_blks, (const T *)src, src_ld, (T *)dst, dst_ld, nv, ph.r, s);
+    };
     const bool p2p = nccl && h->p2p;
     auto offdiag = [&](const Phase *grp, cudaStream_t s) -> int {     // off-diagonal rows from xrecv
         for (int ci = 0; ci < 3; ++ci) {
-            const Phase &ph = grp[ci];
-            if (cta)
-                H2_CUDA(h, launch_cta(cjob(ph, CK_ROWS, MODE_ACCUM, h->xrecv, 0, yh, h->yh_plane), ph.r, h->nsm, s));
-            else
-                H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(ph), ph.n, h->d_blks, (const T *)h->xrecv, 0, yh,
-                                          h->yh_plane, nv, ph.r, s));
+            H2_CUDA(h, rows(MODE_ACCUM, grp[ci], h->xrecv, 0, yh, h->yh_plane, s));
         }
         return H2_OK;
     };
@@ -1670,14 +1679,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
         H2_CUDA(h, cudaStreamWaitEvent(h->s_comm, h->ev_upleaf, 0));
         if ((rc = pull(0)) != H2_OK) return rc;          // leaf level: after my "leaf x^ ready" signal
     }
-    for (const Phase &ph : h->coup_leaf) {
-        if (cta)
-            H2_CUDA(h, launch_cta(cjob(ph, CK_ROWS, MODE_WRITE, xh, h->xh_plane, yh, h->yh_plane), ph.r, h->nsm,
-                                  s_leafc));
-        else
-            H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
-                                      nv, ph.r, s_leafc));
-    }
+    for (const Phase &ph : h->coup_leaf) H2_CUDA(h, rows(MODE_WRITE, ph, xh, h->xh_plane, yh, h->yh_plane, s_leafc));
     H2_CUDA(h, cudaEventRecord(h->ev_leafc, s_leafc));
     if (p2p && !h->p2p_direct) {
         // the leaf-level off-diagonal blocks as soon as their x^ is pulled (most of the
@@ -1752,13 +1754,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     }
     H2_MARK(4);
     // 3. coupling multiply, diagonal part of the levels above the leaves (alg:mult)
-    for (const Phase &ph : h->coup_diag) {
-        if (cta)
-            H2_CUDA(h, launch_cta(cjob(ph, CK_ROWS, MODE_WRITE, xh, h->xh_plane, yh, h->yh_plane), ph.r, h->nsm, st));
-        else
-            H2_CUDA(h, launch_rows<T>(MODE_WRITE, T0(ph), ph.n, h->d_blks, xh, h->xh_plane, yh, h->yh_plane,
-                                      nv, ph.r, st));
-    }
+    for (const Phase &ph : h->coup_diag) H2_CUDA(h, rows(MODE_WRITE, ph, xh, h->xh_plane, yh, h->yh_plane, st));
     H2_MARK(5);
     // 4. off-diagonal part after the exchange (waitAll, alg:optimized_dist_mult line 11-12);
     //    it accumulates into leaf-level rows too, so the leaf coupling stream joins first
@@ -1770,13 +1766,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
             H2_CUDA(h, launch_p2p_wait(h->sig, g == 0 ? h->d_wait_xl : h->d_wait_xu, g == 0 ? h->n_wait_xl : h->n_wait_xu, st));
             for (const auto &pp : h->p2p_phases) {
                 if (pp.group != g) continue;
-                const T *src = (const T *)h->pmap[pp.owner].xh;
-                if (cta)
-                    H2_CUDA(h, launch_cta(cjob(pp.ph, CK_ROWS, MODE_ACCUM, src, h->xh_plane, yh, h->yh_plane), pp.ph.r,
-                                          h->nsm, st));
-                else
-                    H2_CUDA(h, launch_rows<T>(MODE_ACCUM, T0(pp.ph), pp.ph.n, h->d_blks, src, h->xh_plane, yh,
-                                              h->yh_plane, nv, pp.ph.r, st));
+                H2_CUDA(h, rows(MODE_ACCUM, pp.ph, h->pmap[pp.owner].xh, h->xh_plane, yh, h->yh_plane, st));
             }
         }
         H2_CUDA(h, launch_p2p_signal(h->sig, h->d_tgt_cx, h->n_tgt_cx, st));

@@ -168,4 +168,8 @@ template <typename T>
 cudaError_t launch_beta(const CallArgs<T> *args, int64_t n, int nv, cudaStream_t s);
 // rmax: the widest output tile of the job's tasks; nsm: SMs (grid = min(ntask, nsm))
 cudaError_t launch_cta(const CtaJob &j, int rmax, int nsm, cudaStream_t s);
+// tcgen05 FP32 row engine (h2_umma.cuh): 3xTF32 on kind::tf32 MMAs, accumulators in TMEM; tasks
+// with r, c <= 64, nv >= 5.  Same arguments as launch_rows<float> plus the SM count.
+cudaError_t launch_umma_rows(int mode, const Task *t, int ntask, const Blk *b, const float *src, int64_t src_ld,
+                             float *dst, int64_t dst_ld, int nv, int nsm, cudaStream_t s);
 }  // namespace h2

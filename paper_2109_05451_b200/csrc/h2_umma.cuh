@@ -1,0 +1,434 @@
+// h2_umma.cuh -- FP32 row tasks on the 5th-generation tensor cores (DESIGN.md §7 "tcgen05 engine").
+//
+//   y (r x nv) (+)= sum_b A_b (r x c) x_b (c x nv)      (coupling PAPER.md:328-331, transfers 263-270)
+//
+// in 3xTF32: every operand v is split v = hi + lo with hi = rn_tf32(v), lo = rn_tf32(v - hi), and
+// A x = A_lo x_hi + A_hi x_lo + A_hi x_hi (the dropped A_lo x_lo is ~2^-22 of the product), so the
+// result carries FP32 accuracy (north_star: FP32 runs <= 1e-5 against the FP64 oracle) while the
+// products run on tcgen05.mma.kind::tf32 with the accumulator in TMEM.
+//
+// One CTA per SM, warp-specialised, one output node (x one chunk of N <= 64 vectors) at a time:
+//   warp 4      PRODUCER   bulk copies (cp.async.bulk, the TMA engine) of A_b -- r x c contiguous,
+//                          column-major -- and of each x_b vector into an NR-stage raw ring,
+//                          completing on raw_full[s] by transaction count;
+//   warps 6-9   CONVERTERS split every element into hi / lo and write both into an NC-stage
+//                          operand ring in the K-major canonical no-swizzle layout (A transposed:
+//                          each thread gathers 4 columns of one row), then fence.proxy.async so the
+//                          tensor cores see the generic-proxy stores, and free the raw stage;
+//   warp 5      MMA        one thread issues 3 tcgen05.mma (M=64, N, K=8, both operands from shared
+//                          memory) per 8 columns into one of two TMEM accumulators, fresh per
+//                          block, and commits to op_empty[s] and acc_full[b];
+//   warps 0-3   EPILOGUE   tcgen05.ld the block's partial product (warp w reads TMEM lanes
+//                          32w..32w+31; an M=64 accumulator keeps rows 16w..16w+15 in the first 16)
+//                          and add it to the running sum in registers with IEEE FP32 adds -- the
+//                          tensor cores' own accumulation is not round-to-nearest and its bias over
+//                          a whole coupling row measured 1.6e-5 on cfg5 (3xTF32 warp engine); per
+//                          block it stays ~1e-6 -- then store / accumulate y.
+// (MN-major A straight from the column-major copy would skip the transpose, but kind::tf32 with
+// an MN-major no-swizzle descriptor returned zeros on this B200 (tools/umma_probe.cu).)
+// A_b is read from HBM once per (task, vector chunk).  Tasks are walked in the same order by every
+// role (static round robin over persistent CTAs), so only the block's padded column count crosses
+// the ring.
+#pragma once
+#include "h2_internal.h"
+
+namespace h2 {
+namespace umma {
+
+constexpr int MM = 64;                 // UMMA M: output rows per tile (tasks with r <= 64)
+constexpr int KC = 64;                 // max block columns
+constexpr int W_PROD = 4, W_MMA = 5, W_CONV0 = 6, NCONV = 8, NEPI = 4, NWARPS = 14;
+
+template <int N>
+struct Cfg {
+    static constexpr int AEL = MM * KC;             // floats of an A tile
+    static constexpr int XEL = N * KC;              // floats of an x tile
+    static constexpr int XLDR = KC + 4;             // raw x row pitch (272 B: conflict-free 16 B reads)
+    static constexpr int RAW = AEL + N * XLDR;      // raw stage: A as in HBM (ld r), x vectors (ld XLDR)
+    static constexpr int OPS = 2 * (AEL + XEL);     // operand stage: A hi, A lo, x hi, x lo
+    static constexpr int NR = N <= 32 ? 4 : 2;
+    static constexpr int NC = 2;
+    static constexpr int TCOLS = 2 * N < 32 ? 32 : 2 * N;   // two accumulator buffers
+    static constexpr size_t SMEM = (size_t)(NR * RAW + NC * OPS) * sizeof(float) + 512;
+};
+
+// K-major canonical no-swizzle layout (core matrix = 8 rows x 16 bytes): element (row, j) of an
+// operand with KC columns; 4-column chunks at 128 B (LBO), 8-row groups at KC * 32 B (SBO); the MMA
+// of columns [8 ks, 8 ks + 8) starts at ks * 256 B.  Rows are output rows (A) or vectors (x).
+__device__ __forceinline__ int k_off(int row, int j) { return (row >> 3) * (KC * 8) + (j >> 2) * 32 + (row & 7) * 4 + (j & 3); }
+constexpr uint32_t KSTEP_BYTES = 256, LBO = 128, SBO = KC * 32;
+
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo)
+{
+    return (uint64_t)((addr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | ((uint64_t)1 << 46);     // version 1, SWIZZLE_NONE
+}
+// kind::tf32 instruction descriptor: D F32, A/B TF32, both K-major, N, M
+template <int N>
+__host__ __device__ constexpr uint32_t idesc()
+{
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(MM >> 4) << 24);
+}
+
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp4(float *dst, const float *src, bool valid)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(su32(dst)), "l"(src), "r"(valid ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(float *dst, const float *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t *b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_init(uint64_t *b, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t *b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_arrive_cp(uint64_t *b)
+{
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t *b, uint32_t parity)
+{
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra W_%=;\n}\n" ::"r"(su32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc)
+{
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+                 ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void commit(uint64_t *b)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t ta, float *v)
+{
+    uint32_t r[16];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t ta, float *v)
+{
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+// Round to the nearest TF32 value (ties away from zero) on the bit pattern: add half a TF32 ulp to
+// the magnitude, clear the 13 dropped mantissa bits (2 integer ops; cvt.rna.tf32.f32 lowers to a
+// branchy NaN-aware sequence).  Finite inputs only -- the operands of a matvec.
+__device__ __forceinline__ float tf32_rn(float v) { return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xffffe000u); }
+__device__ __forceinline__ void split4(const float4 &v, float4 &h, float4 &l)
+{
+    h.x = tf32_rn(v.x); l.x = tf32_rn(v.x - h.x);
+    h.y = tf32_rn(v.y); l.y = tf32_rn(v.y - h.y);
+    h.z = tf32_rn(v.z); l.z = tf32_rn(v.z - h.z);
+    h.w = tf32_rn(v.w); l.w = tf32_rn(v.w - h.w);
+}
+
+// Output row held by TMEM lane L of an M = 64 accumulator, -1 if none: rows 16q .. 16q + 15 sit in
+// lanes 32q .. 32q + 15 (measured, tools/umma_probe.cu), so every epilogue warp holds 16 rows.
+__device__ __forceinline__ int lane_row(int L) { return (L & 31) < 16 ? (L >> 5) * 16 + (L & 31) : -1; }
+
+}  // namespace umma
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(umma::NWARPS * 32, 1)
+k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks, const float *__restrict__ src,
+            int64_t src_ld, float *__restrict__ dst, int64_t dst_ld, int nv)
+{
+    using namespace umma;
+    using C = Cfg<N>;
+    constexpr int NR = C::NR, NC = C::NC;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *ops = reinterpret_cast<float *>(smem_raw);                  // NC operand stages (MMA reads)
+    float *raw = ops + NC * C::OPS;                                    // NR raw stages (cp.async lands)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(raw + NR * C::RAW);
+    uint64_t *raw_full = bars, *raw_empty = bars + NR, *op_full = bars + 2 * NR, *op_empty = op_full + NC;
+    uint64_t *acc_full = op_empty + NC, *acc_empty = acc_full + 2;
+    int4 *meta = reinterpret_cast<int4 *>(acc_empty + 2);              // per raw stage: c, A ld, x rows, c8
+    uint32_t *tbase_p = reinterpret_cast<uint32_t *>(meta + NR);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int G = gridDim.x;
+    const int nch = (nv + N - 1) / N;
+    const int nwork = ntask * nch;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NR; ++i) {
+            mb_init(raw_full + i, 1);        // producer lane 0 (expect_tx, or after its 4-byte copies)
+            mb_init(raw_empty + i, NCONV);
+        }
+        for (int i = 0; i < NC; ++i) {
+            mb_init(op_full + i, NCONV);
+            mb_init(op_empty + i, 1);        // tcgen05.commit
+        }
+        for (int i = 0; i < 2; ++i) {
+            mb_init(acc_full + i, 1);
+            mb_init(acc_empty + i, NEPI);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (wid == W_MMA) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tbase_p)),
+                     "n"(C::TCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tbase_p;
+
+    if (wid == W_PROD) {
+        // ===================================================================== producer
+        // A_b (r x c, contiguous) as one bulk copy and each x vector as one bulk copy when sizes and
+        // addresses are 16-byte multiples (the coupling: r = c = k, x^ planes); 4-byte cp.async
+        // otherwise (odd ranks), then a plain arrive once those landed.
+        int it = 0;
+        for (int w = blockIdx.x; w < nwork; w += G) {
+            const int t = w / nch, n0 = (w - t * nch) * N;
+            const int nvc = min(N, nv - n0);
+            const Task tk = tasks[t];
+            const int r = tk.r, c = tk.c, c8 = (c + 7) & ~7;
+            for (int bi = 0; bi < tk.nblk; ++bi, ++it) {
+                const int s = it % NR;
+                if (it >= NR) mb_wait(raw_empty + s, ((it / NR) - 1) & 1);
+                const Blk b = blks[tk.blk0 + bi];
+                const float *A = static_cast<const float *>(b.A);
+                const int64_t ld = b.xld ? (int64_t)b.xld : src_ld;
+                const float *x = src + b.x + (int64_t)n0 * ld;
+                const int xr = b.xrows;
+                float *As = raw + s * C::RAW, *Xs = As + C::AEL;
+                const bool abulk = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && !((r * c) & 3) && !(r & 3);
+                const bool xbulk = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && !(ld & 3) && !(xr & 3) && xr > 0;
+                if (lane == 0) meta[s] = make_int4(c, abulk ? r : MM, xr, c8);
+                if (abulk && xbulk) {
+                    if (lane == 0) mb_expect_tx(raw_full + s, (uint32_t)(r * c + nvc * xr) * 4u);
+                    __syncwarp();
+                    if (lane == 0) bulk_g2s(As, A, (uint32_t)(r * c) * 4u, raw_full + s);
+                    for (int n = lane; n < nvc; n += 32)
+                        bulk_g2s(Xs + n * C::XLDR, x + (int64_t)n * ld, (uint32_t)xr * 4u, raw_full + s);
+                } else {
+                    const int la = abulk ? r : MM;
+                    for (int q = lane; q < c * r; q += 32) {
+                        const int m = q % r, j = q / r;
+                        cp4(As + j * la + m, A + (int64_t)j * r + m, true);
+                    }
+                    for (int q = lane; q < nvc * xr; q += 32) {
+                        const int j = q % xr, n = q / xr;
+                        cp4(Xs + n * C::XLDR + j, x + (int64_t)n * ld + j, true);
+                    }
+                    asm volatile("cp.async.wait_all;\n" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mb_arrive(raw_full + s);
+                }
+            }
+        }
+    } else if (wid >= W_CONV0) {
+        // ===================================================================== converters
+        const int ct = threadIdx.x - W_CONV0 * 32;              // 0 .. NCONV * 32 - 1
+        constexpr int CJ = NCONV * 32 / MM;                     // 4-column chunk groups (4)
+        const int cm = ct & (MM - 1), cjh = ct / MM;            // A: row, first 4-column chunk
+        int it = 0;
+        for (int w = blockIdx.x; w < nwork; w += G) {
+            const Task tk = tasks[w / nch];
+            for (int bi = 0; bi < tk.nblk; ++bi, ++it) {
+                const int rs = it % NR, cs = it % NC;
+                mb_wait(raw_full + rs, (it / NR) & 1);
+                if (it >= NC) mb_wait(op_empty + cs, ((it / NC) - 1) & 1);
+                const int4 mt = meta[rs];
+                const int c = mt.x, la = mt.y, xr = mt.z, c8 = mt.w;
+                const float *Ar = raw + rs * C::RAW, *Xr = Ar + C::AEL;
+                float *Ah = ops + cs * C::OPS, *Al = Ah + C::AEL, *Xh = Al + C::AEL, *Xl = Xh + C::XEL;
+                {
+                // A: thread = (row m, every CJ-th 4-column chunk); a warp reads 32 consecutive rows of
+                // one column per LDS (conflict-free) and writes 32 rows' 16-byte chunks (8 distinct
+                // banks per phase).  Columns >= c are zero (x rows there are zero too, but 0 x stale
+                // could be NaN); rows >= r are zero.
+                if (la == MM && c == KC) {
+                    // full 64 x 64 block (every coupling block of a rank-64 level): constant offsets,
+                    // all loads of the thread's 16 columns in flight at once
+                    const float *ap = Ar + cm;
+#pragma unroll
+                    for (int i = 0; i < KC / (4 * CJ); ++i) {
+                        const int j = 4 * (cjh + CJ * i);
+                        float4 v = make_float4(ap[(j + 0) * MM], ap[(j + 1) * MM], ap[(j + 2) * MM], ap[(j + 3) * MM]);
+                        float4 h, l;
+                        split4(v, h, l);
+                        const int o = k_off(cm, j);
+                        *reinterpret_cast<float4 *>(Ah + o) = h;
+                        *reinterpret_cast<float4 *>(Al + o) = l;
+                    }
+                } else {
+                    const bool mrow = cm < la;
+                    for (int j = 4 * cjh; j < c8; j += 4 * CJ) {
+                        float4 v;
+                        v.x = (mrow && j + 0 < c) ? Ar[(j + 0) * la + cm] : 0.f;
+                        v.y = (mrow && j + 1 < c) ? Ar[(j + 1) * la + cm] : 0.f;
+                        v.z = (mrow && j + 2 < c) ? Ar[(j + 2) * la + cm] : 0.f;
+                        v.w = (mrow && j + 3 < c) ? Ar[(j + 3) * la + cm] : 0.f;
+                        float4 h, l;
+                        split4(v, h, l);
+                        const int o = k_off(cm, j);
+                        *reinterpret_cast<float4 *>(Ah + o) = h;
+                        *reinterpret_cast<float4 *>(Al + o) = l;
+                    }
+                }
+                }
+                // x: vector-fastest over (vector, 4-row chunk); rows >= xr are zero (vectors >= nvc are
+                // stale: their output columns are never stored)
+                const int nq = c8 >> 2;
+                for (int q = ct; q < N * nq; q += NCONV * 32) {
+                    const int n = q % N, j = 4 * (q / N);
+                    float4 v = *reinterpret_cast<const float4 *>(Xr + n * C::XLDR + j);
+                    if (j + 4 > xr) {
+                        if (j + 0 >= xr) v.x = 0.f;
+                        if (j + 1 >= xr) v.y = 0.f;
+                        if (j + 2 >= xr) v.z = 0.f;
+                        if (j + 3 >= xr) v.w = 0.f;
+                    }
+                    float4 h, l;
+                    split4(v, h, l);
+                    const int o = k_off(n, j);
+                    *reinterpret_cast<float4 *>(Xh + o) = h;
+                    *reinterpret_cast<float4 *>(Xl + o) = l;
+                }
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    mb_arrive(raw_empty + rs);
+                    mb_arrive(op_full + cs);
+                }
+            }
+        }
+    } else if (wid == W_MMA) {
+        // ===================================================================== MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t ID = idesc<N>();
+            const uint32_t ops_a = su32(ops);
+            int it = 0;
+            for (int w = blockIdx.x; w < nwork; w += G) {
+                const Task tk = tasks[w / nch];
+                const int ksn = ((tk.c + 7) & ~7) >> 3;
+                for (int bi = 0; bi < tk.nblk; ++bi, ++it) {
+                    const int cs = it % NC, ab = it & 1;
+                    mb_wait(op_full + cs, (it / NC) & 1);
+                    if (it >= 2) mb_wait(acc_empty + ab, ((it >> 1) - 1) & 1);
+                    tc_fence_after();
+                    const uint32_t hA = ops_a + (uint32_t)(cs * C::OPS) * 4u;
+                    const uint32_t lA = hA + C::AEL * 4u, hX = lA + C::AEL * 4u, lX = hX + C::XEL * 4u;
+                    const uint32_t d = tmem + (uint32_t)(ab * N);
+                    for (int k = 0; k < ksn; ++k) {
+                        const uint64_t ah = sdesc(hA + k * KSTEP_BYTES, LBO, SBO);
+                        const uint64_t al = sdesc(lA + k * KSTEP_BYTES, LBO, SBO);
+                        const uint64_t xh = sdesc(hX + k * KSTEP_BYTES, LBO, SBO);
+                        const uint64_t xl = sdesc(lX + k * KSTEP_BYTES, LBO, SBO);
+                        mma_tf32(d, al, xh, ID, k > 0);        // small terms first
+                        mma_tf32(d, ah, xl, ID, 1);
+                        mma_tf32(d, ah, xh, ID, 1);
+                    }
+                    commit(op_empty + cs);
+                    commit(acc_full + ab);
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ===================================================================== epilogue (warps 0-3)
+        const int row = lane_row(threadIdx.x);           // -1: this TMEM lane holds no output row
+        const uint32_t tl = tmem + ((uint32_t)(wid * 32) << 16);
+        int it = 0;
+        for (int w = blockIdx.x; w < nwork; w += G) {
+            const int t = w / nch, n0 = (w - t * nch) * N;
+            const int nvc = min(N, nv - n0);
+            const Task tk = tasks[t];
+            const bool live = row >= 0 && row < tk.r;
+            float *out = dst + tk.out + row + (int64_t)n0 * dst_ld;
+            float acc[N];
+#pragma unroll
+            for (int n = 0; n < N; ++n) acc[n] = (MODE == MODE_ACCUM && live && n < nvc) ? out[(int64_t)n * dst_ld] : 0.f;
+            for (int bi = 0; bi < tk.nblk; ++bi, ++it) {
+                const int ab = it & 1;
+                mb_wait(acc_full + ab, (it >> 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int q = 0; q < N; q += 16) {
+                    float v[16];
+                    if constexpr (N >= 16) tmem_ld16(tl + (uint32_t)(ab * N + q), v);
+                    else tmem_ld8(tl + (uint32_t)(ab * N + q), v);
+#pragma unroll
+                    for (int i = 0; i < (N >= 16 ? 16 : N); ++i) acc[q + i] += v[i];
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mb_arrive(acc_empty + ab);
+            }
+            if (live) {
+#pragma unroll
+                for (int n = 0; n < N; ++n)
+                    if (n < nvc) out[(int64_t)n * dst_ld] = acc[n];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (wid == W_MMA) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(C::TCOLS));
+    }
+}
+
+// Launcher: N from nv (8 / 16 / 32 / 64-vector chunks), one CTA per SM (persistent).
+cudaError_t launch_umma_rows(int mode, const Task *t, int ntask, const Blk *b, const float *src, int64_t src_ld,
+                             float *dst, int64_t dst_ld, int nv, int nsm, cudaStream_t s)
+{
+    if (ntask == 0) return cudaSuccess;
+    cudaError_t err = cudaSuccess;
+    auto go = [&](auto nt) {
+        constexpr int N = decltype(nt)::value;
+        using C = umma::Cfg<N>;
+        auto kw = k_umma_rows<N, MODE_WRITE>;
+        auto ka = k_umma_rows<N, MODE_ACCUM>;
+        static cudaError_t attr = [&] {
+            cudaError_t e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+            return e == cudaSuccess ? cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) : e;
+        }();
+        if ((err = attr) != cudaSuccess) return;
+        const int nwork = ntask * ((nv + N - 1) / N);
+        const int grid = nwork < nsm ? nwork : nsm;
+        if (mode == MODE_WRITE) kw<<<grid, umma::NWARPS * 32, C::SMEM, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv);
+        else                    ka<<<grid, umma::NWARPS * 32, C::SMEM, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv);
+        err = cudaGetLastError();
+    };
+    if (nv <= 8) go(std::integral_constant<int, 8>{});
+    else if (nv <= 16) go(std::integral_constant<int, 16>{});
+    else if (nv <= 32) go(std::integral_constant<int, 32>{});
+    else go(std::integral_constant<int, 64>{});
+    return err;
+}
+
+}  // namespace h2

@@ -224,12 +224,18 @@ def test_matvec_ld_larger_leading_dimensions():
     assert np.all(pad == 123.0)
 
 
+@pytest.mark.parametrize("engine", ["warp", "tcgen05"])
 @pytest.mark.parametrize("N,m,k,nv,eta,seed", [
     (3000, 32, 16, 5, 0.9, 61), (5000, 64, 25, 8, 0.9, 62), (5000, 64, 25, 16, 0.9, 63),
-    (4000, 64, 36, 17, 0.9, 64), (4000, 64, 64, 16, 1.1, 65), (2500, 48, 40, 33, 0.9, 66)])
-def test_fp32_tensor_engine(N, m, k, nv, eta, seed):
-    """FP32 at nv >= 5 runs the 3xTF32 tensor engine (Tf3): within 1e-5 of the FP64 oracle on the
-    FP32-rounded operator and vectors, ragged leaves, nv inside and across the 8/16-vector chunks."""
+    (4000, 64, 36, 17, 0.9, 64), (4000, 64, 64, 16, 1.1, 65), (2500, 48, 40, 33, 0.9, 66),
+    (3000, 64, 64, 64, 1.1, 67), (3000, 64, 64, 41, 1.1, 68)])
+def test_fp32_tensor_engine(engine, N, m, k, nv, eta, seed, monkeypatch):
+    """FP32 at nv >= 5 runs 3xTF32 on the tensor cores -- the coupling rows on tcgen05.mma (TMEM
+    accumulators, h2_umma.cuh) by default, everything on the mma.sync warp engine (Tf3) with
+    H2_ENGINE=warp: within 1e-5 of the FP64 oracle on the FP32-rounded operator and vectors, ragged
+    leaves, unaligned ranks (k = 25: 4-byte copies), nv inside and across the 8/16/32/64 chunks."""
+    if engine == "warp":
+        monkeypatch.setenv("H2_ENGINE", "warp")
     h = random_case(N, m, lambda l: k, seed, eta=eta).astype(np.float32)
     X = make_xy(h.perm, nv, seed, -1.0, 1.0).astype(np.float32).astype(np.float64)
     Y0 = make_xy(h.perm, nv, seed + 1, -1.0, 1.0, stream=1).astype(np.float32).astype(np.float64)

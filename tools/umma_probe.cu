@@ -27,7 +27,7 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int amaj, int bm
 }
 
 // mode 0: A K-major, mode 1: A MN-major.  B always K-major (N x K).
-__global__ void probe(const float *A, const float *B, float *out, int mode, int M)
+__global__ void probe(const float *A, const float *B, float *out, int mode, int M, int swap)
 {
     __shared__ __align__(1024) float As[128 * 8];
     __shared__ __align__(1024) float Bs[16 * 8];
@@ -59,7 +59,7 @@ __global__ void probe(const float *A, const float *B, float *out, int mode, int 
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t tm = tbase;
     if (tid == 0) {
-        const uint64_t da = mode == 0 ? sdesc(su32(As), 128, 256) : sdesc(su32(As), 128 * 16, 128);
+        const uint64_t da = mode == 0 ? sdesc(su32(As), 128, 256) : (swap ? sdesc(su32(As), 128, 128 * 16) : sdesc(su32(As), 128 * 16, 128));
         const uint64_t db = sdesc(su32(Bs), 128, 256);
         const uint32_t id = idesc_tf32(M, 16, mode, 0);
         asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -90,18 +90,19 @@ int main()
     cudaMalloc(&dA, sizeof hA); cudaMalloc(&dB, sizeof hB); cudaMalloc(&dO, sizeof hO);
     int fails = 0;
     for (int M : {64, 128})
-    for (int mode = 0; mode < 2; ++mode) {
-        for (int m = 0; m < M; ++m) for (int k = 0; k < 8; ++k) hA[m * 8 + k] = (float)((m * 3 + k * 7) % 11 - 5);
+    for (int mode = 0; mode < 3; ++mode) {
+        const int swap = mode == 2;
+        for (int m = 0; m < M; ++m) for (int k = 0; k < 8; ++k) hA[m * 8 + k] = k == 0 ? (float)(m + 1) : (float)((m * 3 + k * 7) % 11 - 5);
         for (int n = 0; n < 16; ++n) for (int k = 0; k < 8; ++k) hB[n * 8 + k] = (float)((n * 5 + k * 3) % 7 - 3);
         cudaMemcpy(dA, hA, sizeof hA, cudaMemcpyHostToDevice);
         cudaMemcpy(dB, hB, sizeof hB, cudaMemcpyHostToDevice);
         cudaMemset(dO, 0xff, sizeof hO);
-        probe<<<1, 128>>>(dA, dB, dO, mode, M);
+        probe<<<1, 128>>>(dA, dB, dO, mode ? 1 : 0, M, swap);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { printf("M=%d mode %d: %s\n", M, mode, cudaGetErrorString(e)); return 1; }
         cudaMemcpy(hO, dO, sizeof hO, cudaMemcpyDeviceToHost);
         // map each expected row to the TMEM lane holding it
-        printf("M=%d A-%s: row->lane:", M, mode ? "MN" : "K");
+        printf("M=%d A-%s: row->lane:", M, mode == 0 ? "K" : (swap ? "MN(lbo/sbo swapped)" : "MN"));
         int bad = 0;
         for (int m = 0; m < M; ++m) {
             int lane = -1;
@@ -115,10 +116,31 @@ int main()
                 if (ok) lane = l;
             }
             if (lane < 0) ++bad;
-            if (m < 20 || m % 16 == 0) printf(" %d:%d", m, lane);
+            if (m < 20 || m % 8 == 0 || m == M - 1) printf(" %d:%d", m, lane);
         }
         printf("  (%d rows not found)\n", bad);
         fails += bad;
+    }
+    // MN-major decode: A[m][k] = m + 128 k, B = identity (n = k < 8) -> D[m][n] = the A element the
+    // tensor core read for (m, n); print it as (row, col)
+    for (int swap = 0; swap < 2; ++swap) {
+        const int M = 64;
+        for (int m = 0; m < 128; ++m) for (int k = 0; k < 8; ++k) hA[m * 8 + k] = (float)(m + 128 * k);
+        for (int n = 0; n < 16; ++n) for (int k = 0; k < 8; ++k) hB[n * 8 + k] = (n == k) ? 1.f : 0.f;
+        cudaMemcpy(dA, hA, sizeof hA, cudaMemcpyHostToDevice);
+        cudaMemcpy(dB, hB, sizeof hB, cudaMemcpyHostToDevice);
+        probe<<<1, 128>>>(dA, dB, dO, 1, M, swap);
+        cudaDeviceSynchronize();
+        cudaMemcpy(hO, dO, sizeof hO, cudaMemcpyDeviceToHost);
+        printf("MN decode swap=%d (lane: read (row,col) for col 0..7):\n", swap);
+        for (int l : {0, 1, 2, 3, 4, 5, 8, 15, 32, 33}) {
+            printf("  lane %3d:", l);
+            for (int n = 0; n < 8; ++n) {
+                const int v = (int)hO[l * 16 + n];
+                printf(" (%d,%d)", v % 128, v / 128);
+            }
+            printf("\n");
+        }
     }
     // rounding probe: A = 1 + 3*2^-12 (between two TF32 values, nearer the upper), B = 1
     {
@@ -131,7 +153,7 @@ int main()
         hB[0] = 1.f;
         cudaMemcpy(dA, hA, sizeof hA, cudaMemcpyHostToDevice);
         cudaMemcpy(dB, hB, sizeof hB, cudaMemcpyHostToDevice);
-        probe<<<1, 128>>>(dA, dB, dO, 0, M);
+        probe<<<1, 128>>>(dA, dB, dO, 0, M, 0);
         cudaDeviceSynchronize();
         cudaMemcpy(hO, dO, sizeof hO, cudaMemcpyDeviceToHost);
         printf("rounding: 1+3*2^-12 -> 1 + %g ulp(2^-10); 1+2^-12 -> 1 + %g; -(1+3*2^-12) -> -(1 + %g)\n",
