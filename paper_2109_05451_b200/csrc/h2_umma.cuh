@@ -2,10 +2,12 @@
 //
 //   y (r x nv) (+)= sum_b A_b (r x c) x_b (c x nv)      (coupling PAPER.md:328-331, transfers 263-270)
 //
-// in 3xTF32: every operand v is split v = hi + lo with hi = rn_tf32(v), lo = rn_tf32(v - hi), and
-// A x = A_lo x_hi + A_hi x_lo + A_hi x_hi (the dropped A_lo x_lo is ~2^-22 of the product), so the
-// result carries FP32 accuracy (north_star: FP32 runs <= 1e-5 against the FP64 oracle) while the
-// products run on tcgen05.mma.kind::tf32 with the accumulator in TMEM.
+// in split TF32: every operand v is split v = hi + lo with hi = rn_tf32(v), lo = rn_tf32(v - hi)
+// (hi + lo reproduces v to ~2^-22), and ONE tcgen05.mma.kind::tf32 per 8 columns computes all four
+// products: the operand tiles are stacked, A' = [A_hi; A_lo] (M = 128) and x' = [x_hi, x_lo]
+// (N = 2 nv), so D' = A' x' holds A_hi x_hi, A_hi x_lo, A_lo x_hi, A_lo x_lo in its four quadrants and
+// y = their sum carries FP32 accuracy (north_star: FP32 runs <= 1e-5 against the FP64 oracle).
+// (Three separate M = 64 MMAs per 8 columns -- 3xTF32 -- were issue-bound: ~94 cycles per MMA.)
 //
 // One CTA per SM, warp-specialised, one output node (x one chunk of N <= 64 vectors) at a time:
 //   warp 4      PRODUCER   bulk copies (cp.async.bulk, the TMA engine) of A_b -- r x c contiguous,
@@ -15,21 +17,24 @@
 //                          operand ring in the K-major canonical no-swizzle layout (A transposed:
 //                          each thread gathers 4 columns of one row), then fence.proxy.async so the
 //                          tensor cores see the generic-proxy stores, and free the raw stage;
-//   warp 5      MMA        one thread issues 3 tcgen05.mma (M=64, N, K=8, both operands from shared
-//                          memory) per 8 columns into one of two TMEM accumulators, fresh per
-//                          block, and commits to op_empty[s] and acc_full[b];
-//   warps 0-3   EPILOGUE   tcgen05.ld the block's partial product (warp w reads TMEM lanes
-//                          32w..32w+31; an M=64 accumulator keeps rows 16w..16w+15 in the first 16)
-//                          and add it to the running sum in registers with IEEE FP32 adds -- the
-//                          tensor cores' own accumulation is not round-to-nearest and its bias over
-//                          a whole coupling row measured 1.6e-5 on cfg5 (3xTF32 warp engine); per
-//                          block it stays ~1e-6 -- then store / accumulate y.
+//   warp 5      MMA        one elected thread issues one tcgen05.mma (M=128, N=2 nv, K=8, both
+//                          operands from shared memory) per 8 columns, k-step k into partial
+//                          accumulator k % NACC of one of NB TMEM buffers (independent chains),
+//                          fresh per block, and commits to op_empty[s] and acc_full[b] (NB buffers);
+//   warps 0-3   EPILOGUE   tcgen05.ld the block's partial products (warp w reads TMEM lanes
+//                          32w..32w+31: warps 0-1 hold the A_hi rows, 2-3 the A_lo rows) and add
+//                          both column halves to a running sum in registers with IEEE FP32 adds --
+//                          the tensor cores' own accumulation is not round-to-nearest and its bias
+//                          over a whole coupling row measured 1.6e-5 on cfg5 (3xTF32 warp engine);
+//                          per block it stays ~1e-6 -- then, per task, the A_lo half hands its sums
+//                          to the A_hi half through shared memory, which stores / accumulates y.
 // (MN-major A straight from the column-major copy would skip the transpose, but kind::tf32 with
 // an MN-major no-swizzle descriptor returned zeros on this B200 (tools/umma_probe.cu).)
 // A_b is read from HBM once per (task, vector chunk).  Tasks are walked in the same order by every
 // role (static round robin over persistent CTAs), so only the block's padded column count crosses
 // the ring.
 #pragma once
+#include <cuda.h>
 #include "h2_internal.h"
 
 namespace h2 {
@@ -46,10 +51,17 @@ struct Cfg {
     static constexpr int XLDR = KC + 4;             // raw x row pitch (272 B: conflict-free 16 B reads)
     static constexpr int RAW = AEL + N * XLDR;      // raw stage: A as in HBM (ld r), x vectors (ld XLDR)
     static constexpr int OPS = 2 * (AEL + XEL);     // operand stage: A hi, A lo, x hi, x lo
-    static constexpr int NR = N <= 32 ? 4 : 2;
+    static constexpr int NR = N <= 16 ? 6 : (N <= 32 ? 4 : 2);
     static constexpr int NC = 2;
-    static constexpr int TCOLS = 2 * N < 32 ? 32 : 2 * N;   // two accumulator buffers
-    static constexpr size_t SMEM = (size_t)(NR * RAW + NC * OPS) * sizeof(float) + 512;
+    // accumulators per block: k-step k accumulates into partial k % NACC, so the MMAs of a block
+    // form NACC independent chains -- dependent MMAs on one accumulator serialise on the MMA
+    // latency (measured: a 2-chain block of 8 M=128 x N=32 MMAs took ~1 us)
+    static constexpr int NACC = N <= 16 ? 8 : (N <= 32 ? 4 : 2);
+    // accumulator buffers in flight (MMA of block b waits for the epilogue to drain block b - NB)
+    static constexpr int NB = 512 / (NACC * 2 * N) < 4 ? 512 / (NACC * 2 * N) : 4;   // >= 2
+    static constexpr int TCOLS = NB * NACC * 2 * N; // buffers x NACC partials x 2N columns (128..512)
+    static constexpr int CMB = 64 * N;              // floats: the A_lo half's sums handed to the A_hi half
+    static constexpr size_t SMEM = (size_t)(NR * RAW + NC * OPS + CMB) * sizeof(float) + 512;
 };
 
 // K-major canonical no-swizzle layout (core matrix = 8 rows x 16 bytes): element (row, j) of an
@@ -64,14 +76,17 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
            ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | ((uint64_t)1 << 46);     // version 1, SWIZZLE_NONE
 }
 // kind::tf32 instruction descriptor: D F32, A/B TF32, both K-major, N, M
-template <int N>
+template <int M, int N>
 __host__ __device__ constexpr uint32_t idesc()
 {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
-           ((uint32_t)(MM >> 4) << 24);
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp16(float *dst, const float *src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp4(float *dst, const float *src, bool valid)
 {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(su32(dst)), "l"(src), "r"(valid ? 4 : 0)
@@ -81,6 +96,15 @@ __device__ __forceinline__ void bulk_g2s(float *dst, const float *src, uint32_t 
 {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                  ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
+}
+// 4-D tiled tensor copy (the x^ operand: see make_xmap) completing on an mbarrier
+__device__ __forceinline__ void tensor4_g2s(float *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                            uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
+                 ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+                   "r"(su32(bar)) : "memory");
 }
 __device__ __forceinline__ void mb_expect_tx(uint64_t *b, uint32_t bytes)
 {
@@ -107,16 +131,52 @@ __device__ __forceinline__ void mb_wait(uint64_t *b, uint32_t parity)
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+// issued by the whole (converged) warp: one elected lane executes the MMA / commit
 __device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc)
 {
-    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+    asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
                  ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc) : "memory");
 }
+// The 8 MMAs of a full 64-column block in one asm statement: one elect, descriptors advanced by
+// 256 B (+16 in the address field) per k-step, k-step k into partial k % NACC (fresh for k < NACC),
+// partials PCOLS TMEM columns apart.  One statement per MMA cost ~48 cycles of issue each (elect +
+// vote + moves on the uniform datapath, tools/umma_rate.cu) against a 16-cycle execution floor.
+template <int NACC, int PCOLS>
+__device__ __forceinline__ void mma8_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t id)
+{
+    asm volatile(
+        "{\n.reg .pred e, f, p<8>;\n.reg .b32 d<8>;\n.reg .b64 a<8>, b<8>;\n"
+        "setp.ne.b32 f, 0, 0;\nelect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 p1, %11, 0;\nsetp.ne.b32 p2, %12, 0;\nsetp.ne.b32 p3, %13, 0;\nsetp.ne.b32 p4, %14, 0;\n"
+        "setp.ne.b32 p5, %15, 0;\nsetp.ne.b32 p6, %16, 0;\nsetp.ne.b32 p7, %17, 0;\n"
+        "add.u32 d0, %0, 0;\nadd.u32 d1, %0, %4;\nadd.u32 d2, %0, %5;\nadd.u32 d3, %0, %6;\n"
+        "add.u32 d4, %0, %7;\nadd.u32 d5, %0, %8;\nadd.u32 d6, %0, %9;\nadd.u32 d7, %0, %10;\n"
+        "add.s64 a0, %1, 0;\nadd.s64 a1, %1, 16;\nadd.s64 a2, %1, 32;\nadd.s64 a3, %1, 48;\n"
+        "add.s64 a4, %1, 64;\nadd.s64 a5, %1, 80;\nadd.s64 a6, %1, 96;\nadd.s64 a7, %1, 112;\n"
+        "add.s64 b0, %2, 0;\nadd.s64 b1, %2, 16;\nadd.s64 b2, %2, 32;\nadd.s64 b3, %2, 48;\n"
+        "add.s64 b4, %2, 64;\nadd.s64 b5, %2, 80;\nadd.s64 b6, %2, 96;\nadd.s64 b7, %2, 112;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d0], a0, b0, %3, f;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], a1, b1, %3, p1;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d2], a2, b2, %3, p2;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d3], a3, b3, %3, p3;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d4], a4, b4, %3, p4;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d5], a5, b5, %3, p5;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d6], a6, b6, %3, p6;\n"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [d7], a7, b7, %3, p7;\n}\n"
+        ::"r"(d), "l"(a), "l"(b), "r"(id),
+          "n"((1 % NACC) * PCOLS), "n"((2 % NACC) * PCOLS), "n"((3 % NACC) * PCOLS), "n"((4 % NACC) * PCOLS),
+          "n"((5 % NACC) * PCOLS), "n"((6 % NACC) * PCOLS), "n"((7 % NACC) * PCOLS),
+          "n"(1 >= NACC), "n"(2 >= NACC), "n"(3 >= NACC), "n"(4 >= NACC), "n"(5 >= NACC), "n"(6 >= NACC),
+          "n"(7 >= NACC)
+        : "memory");
+}
+
 __device__ __forceinline__ void commit(uint64_t *b)
 {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(b))
-                 : "memory");
+    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n"
+                 ::"r"(su32(b)) : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t ta, float *v)
 {
@@ -128,6 +188,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t ta, float *v)
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t ta, float *v)
+{
+    tmem_ld16(ta, v);
+    tmem_ld16(ta + 16u, v + 16);
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t ta, float *v)
 {
@@ -151,16 +216,14 @@ __device__ __forceinline__ void split4(const float4 &v, float4 &h, float4 &l)
     h.w = tf32_rn(v.w); l.w = tf32_rn(v.w - h.w);
 }
 
-// Output row held by TMEM lane L of an M = 64 accumulator, -1 if none: rows 16q .. 16q + 15 sit in
-// lanes 32q .. 32q + 15 (measured, tools/umma_probe.cu), so every epilogue warp holds 16 rows.
-__device__ __forceinline__ int lane_row(int L) { return (L & 31) < 16 ? (L >> 5) * 16 + (L & 31) : -1; }
 
 }  // namespace umma
 
 template <int N, int MODE>
 __global__ void __launch_bounds__(umma::NWARPS * 32, 1)
 k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks, const float *__restrict__ src,
-            int64_t src_ld, float *__restrict__ dst, int64_t dst_ld, int nv)
+            int64_t src_ld, float *__restrict__ dst, int64_t dst_ld, int nv, const __grid_constant__ CUtensorMap tmx,
+            int use_tm)
 {
     using namespace umma;
     using C = Cfg<N>;
@@ -170,8 +233,8 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
     float *raw = ops + NC * C::OPS;                                    // NR raw stages (cp.async lands)
     uint64_t *bars = reinterpret_cast<uint64_t *>(raw + NR * C::RAW);
     uint64_t *raw_full = bars, *raw_empty = bars + NR, *op_full = bars + 2 * NR, *op_empty = op_full + NC;
-    uint64_t *acc_full = op_empty + NC, *acc_empty = acc_full + 2;
-    int4 *meta = reinterpret_cast<int4 *>(acc_empty + 2);              // per raw stage: c, A ld, x rows, c8
+    uint64_t *acc_full = op_empty + NC, *acc_empty = acc_full + C::NB;
+    int4 *meta = reinterpret_cast<int4 *>(acc_empty + C::NB);              // per raw stage: c, A ld, x rows, c8
     uint32_t *tbase_p = reinterpret_cast<uint32_t *>(meta + NR);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int G = gridDim.x;
@@ -187,7 +250,7 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
             mb_init(op_full + i, NCONV);
             mb_init(op_empty + i, 1);        // tcgen05.commit
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < C::NB; ++i) {
             mb_init(acc_full + i, 1);
             mb_init(acc_empty + i, NEPI);
         }
@@ -225,13 +288,22 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
                 float *As = raw + s * C::RAW, *Xs = As + C::AEL;
                 const bool abulk = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && !((r * c) & 3) && !(r & 3);
                 const bool xbulk = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && !(ld & 3) && !(xr & 3) && xr > 0;
-                if (lane == 0) meta[s] = make_int4(c, abulk ? r : MM, xr, c8);
-                if (abulk && xbulk) {
-                    if (lane == 0) mb_expect_tx(raw_full + s, (uint32_t)(r * c + nvc * xr) * 4u);
+                // x^ straight into the K-major layout with ONE tensor copy (all N vectors) when it
+                // comes from the launch's source plane; else one bulk copy per vector into [n][XLDR].
+                // (The TMA engine serialises requests at ~125 cycles each: 17 requests per block --
+                // A plus 16 vectors -- paced the kernel at ~2 us per block.)
+                const bool xtm = use_tm && !b.xld && !(b.x & 3) && xr == c && !(n0 & 7);
+                if (lane == 0) meta[s] = make_int4(c, abulk ? r : MM, xr, c8 | (xtm ? 0x10000 : 0));
+                if (abulk && (xtm || xbulk)) {
+                    if (lane == 0) {
+                        mb_expect_tx(raw_full + s, (uint32_t)(r * c) * 4u + (xtm ? (uint32_t)C::XEL * 4u : (uint32_t)(nvc * xr) * 4u));
+                        bulk_g2s(As, A, (uint32_t)(r * c) * 4u, raw_full + s);
+                        if (xtm) tensor4_g2s(Xs, &tmx, 0, 0, (int)(b.x >> 2), n0 >> 3, raw_full + s);
+                    }
                     __syncwarp();
-                    if (lane == 0) bulk_g2s(As, A, (uint32_t)(r * c) * 4u, raw_full + s);
-                    for (int n = lane; n < nvc; n += 32)
-                        bulk_g2s(Xs + n * C::XLDR, x + (int64_t)n * ld, (uint32_t)xr * 4u, raw_full + s);
+                    if (!xtm)
+                        for (int n = lane; n < nvc; n += 32)
+                            bulk_g2s(Xs + n * C::XLDR, x + (int64_t)n * ld, (uint32_t)xr * 4u, raw_full + s);
                 } else {
                     const int la = abulk ? r : MM;
                     for (int q = lane; q < c * r; q += 32) {
@@ -261,7 +333,8 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
                 mb_wait(raw_full + rs, (it / NR) & 1);
                 if (it >= NC) mb_wait(op_empty + cs, ((it / NC) - 1) & 1);
                 const int4 mt = meta[rs];
-                const int c = mt.x, la = mt.y, xr = mt.z, c8 = mt.w;
+                const int c = mt.x, la = mt.y, xr = mt.z, c8 = mt.w & 0xffff;
+                const bool xk = mt.w >> 16;
                 const float *Ar = raw + rs * C::RAW, *Xr = Ar + C::AEL;
                 float *Ah = ops + cs * C::OPS, *Al = Ah + C::AEL, *Xh = Al + C::AEL, *Xl = Xh + C::XEL;
                 {
@@ -299,6 +372,24 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
                     }
                 }
                 }
+                if (xk) {
+                    // x already in the K-major layout (tensor copy): split in place, rows >= xr zero
+                    for (int q = ct; q < C::XEL / 4; q += NCONV * 32) {
+                        const int j = 4 * ((q & 127) >> 3);
+                        if (j >= c8) continue;
+                        float4 v = *reinterpret_cast<const float4 *>(Xr + 4 * q);
+                        if (j + 4 > xr) {
+                            if (j + 0 >= xr) v.x = 0.f;
+                            if (j + 1 >= xr) v.y = 0.f;
+                            if (j + 2 >= xr) v.z = 0.f;
+                            if (j + 3 >= xr) v.w = 0.f;
+                        }
+                        float4 h, l;
+                        split4(v, h, l);
+                        *reinterpret_cast<float4 *>(Xh + 4 * q) = h;
+                        *reinterpret_cast<float4 *>(Xl + 4 * q) = l;
+                    }
+                } else {
                 // x: vector-fastest over (vector, 4-row chunk); rows >= xr are zero (vectors >= nvc are
                 // stale: their output columns are never stored)
                 const int nq = c8 >> 2;
@@ -317,6 +408,7 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
                     *reinterpret_cast<float4 *>(Xh + o) = h;
                     *reinterpret_cast<float4 *>(Xl + o) = l;
                 }
+                }
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 __syncwarp();
                 if (lane == 0) {
@@ -326,72 +418,80 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
             }
         }
     } else if (wid == W_MMA) {
-        // ===================================================================== MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t ID = idesc<N>();
-            const uint32_t ops_a = su32(ops);
-            int it = 0;
-            for (int w = blockIdx.x; w < nwork; w += G) {
-                const Task tk = tasks[w / nch];
-                const int ksn = ((tk.c + 7) & ~7) >> 3;
-                for (int bi = 0; bi < tk.nblk; ++bi, ++it) {
-                    const int cs = it % NC, ab = it & 1;
-                    mb_wait(op_full + cs, (it / NC) & 1);
-                    if (it >= 2) mb_wait(acc_empty + ab, ((it >> 1) - 1) & 1);
-                    tc_fence_after();
-                    const uint32_t hA = ops_a + (uint32_t)(cs * C::OPS) * 4u;
-                    const uint32_t lA = hA + C::AEL * 4u, hX = lA + C::AEL * 4u, lX = hX + C::XEL * 4u;
-                    const uint32_t d = tmem + (uint32_t)(ab * N);
-                    for (int k = 0; k < ksn; ++k) {
-                        const uint64_t ah = sdesc(hA + k * KSTEP_BYTES, LBO, SBO);
-                        const uint64_t al = sdesc(lA + k * KSTEP_BYTES, LBO, SBO);
-                        const uint64_t xh = sdesc(hX + k * KSTEP_BYTES, LBO, SBO);
-                        const uint64_t xl = sdesc(lX + k * KSTEP_BYTES, LBO, SBO);
-                        mma_tf32(d, al, xh, ID, k > 0);        // small terms first
-                        mma_tf32(d, ah, xl, ID, 1);
-                        mma_tf32(d, ah, xh, ID, 1);
-                    }
-                    commit(op_empty + cs);
-                    commit(acc_full + ab);
+        // ===================================================================== MMA issuer (whole warp)
+        constexpr uint32_t ID = idesc<128, 2 * N>();
+        const uint32_t ops_a = su32(ops);
+        int it = 0;
+        for (int w = blockIdx.x; w < nwork; w += G) {
+            const Task tk = tasks[w / nch];
+            const int ksn = ((tk.c + 7) & ~7) >> 3;
+            for (int bi = 0; bi < tk.nblk; ++bi, ++it) {
+                const int cs = it % NC, ab = it % C::NB;
+                mb_wait(op_full + cs, (it / NC) & 1);
+                if (it >= C::NB) mb_wait(acc_empty + ab, ((it / C::NB) - 1) & 1);
+                tc_fence_after();
+                const uint32_t hA = ops_a + (uint32_t)(cs * C::OPS) * 4u;     // [A_hi; A_lo], 128 rows
+                const uint32_t hX = hA + 2 * C::AEL * 4u;                     // [x_hi, x_lo], 2N rows
+                const uint32_t d0 = tmem + (uint32_t)(ab * C::NACC * 2 * N);
+                if (ksn == 8) {
+                    mma8_tf32<C::NACC, 2 * N>(d0, sdesc(hA, LBO, SBO), sdesc(hX, LBO, SBO), ID);
+                } else {
+                    for (int k = 0; k < ksn; ++k)
+                        mma_tf32(d0 + (uint32_t)((k % C::NACC) * 2 * N), sdesc(hA + k * KSTEP_BYTES, LBO, SBO),
+                                 sdesc(hX + k * KSTEP_BYTES, LBO, SBO), ID, k >= C::NACC);
                 }
+                commit(op_empty + cs);
+                commit(acc_full + ab);
             }
         }
-        __syncwarp();
     } else {
         // ===================================================================== epilogue (warps 0-3)
-        const int row = lane_row(threadIdx.x);           // -1: this TMEM lane holds no output row
+        const int row = threadIdx.x & 63, half = threadIdx.x >> 6;   // TMEM lane = M row: A_hi / A_lo half
         const uint32_t tl = tmem + ((uint32_t)(wid * 32) << 16);
+        float *cmb = reinterpret_cast<float *>(smem_raw + (size_t)(NC * C::OPS + NR * C::RAW) * 4 + 512);
         int it = 0;
         for (int w = blockIdx.x; w < nwork; w += G) {
             const int t = w / nch, n0 = (w - t * nch) * N;
             const int nvc = min(N, nv - n0);
             const Task tk = tasks[t];
-            const bool live = row >= 0 && row < tk.r;
+            const bool live = row < tk.r;
             float *out = dst + tk.out + row + (int64_t)n0 * dst_ld;
             float acc[N];
 #pragma unroll
-            for (int n = 0; n < N; ++n) acc[n] = (MODE == MODE_ACCUM && live && n < nvc) ? out[(int64_t)n * dst_ld] : 0.f;
+            for (int n = 0; n < N; ++n)
+                acc[n] = (MODE == MODE_ACCUM && half == 0 && live && n < nvc) ? out[(int64_t)n * dst_ld] : 0.f;
+            const int npart = min((((int)tk.c + 7) >> 3), C::NACC);
             for (int bi = 0; bi < tk.nblk; ++bi, ++it) {
-                const int ab = it & 1;
-                mb_wait(acc_full + ab, (it >> 1) & 1);
+                const int ab = it % C::NB;
+                mb_wait(acc_full + ab, (it / C::NB) & 1);
                 tc_fence_after();
+                for (int a = 0; a < npart; ++a) {
+                    const uint32_t ta = tl + (uint32_t)((ab * C::NACC + a) * 2 * N);
 #pragma unroll
-                for (int q = 0; q < N; q += 16) {
-                    float v[16];
-                    if constexpr (N >= 16) tmem_ld16(tl + (uint32_t)(ab * N + q), v);
-                    else tmem_ld8(tl + (uint32_t)(ab * N + q), v);
+                    for (int q = 0; q < N; q += 16) {
+                        float v[16], u[16];
+                        if constexpr (N >= 16) { tmem_ld16(ta + (uint32_t)q, v); tmem_ld16(ta + (uint32_t)(N + q), u); }
+                        else { tmem_ld8(ta + (uint32_t)q, v); tmem_ld8(ta + (uint32_t)(N + q), u); }
 #pragma unroll
-                    for (int i = 0; i < (N >= 16 ? 16 : N); ++i) acc[q + i] += v[i];
+                        for (int i = 0; i < (N >= 16 ? 16 : N); ++i) acc[q + i] += v[i] + u[i];
+                    }
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mb_arrive(acc_empty + ab);
             }
-            if (live) {
+            // the A_lo half hands its sums to the A_hi half (conflict-free: row fastest)
+            if (half == 1) {
+#pragma unroll
+                for (int n = 0; n < N; ++n) cmb[n * 64 + row] = acc[n];
+            }
+            asm volatile("bar.sync 1, 128;\n" ::: "memory");
+            if (half == 0 && live) {
 #pragma unroll
                 for (int n = 0; n < N; ++n)
-                    if (n < nvc) out[(int64_t)n * dst_ld] = acc[n];
+                    if (n < nvc) out[(int64_t)n * dst_ld] = acc[n] + cmb[n * 64 + row];
             }
+            asm volatile("bar.sync 1, 128;\n" ::: "memory");
         }
     }
     tc_fence_before();
@@ -400,6 +500,34 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(C::TCOLS));
     }
+}
+
+// Tensor map of an x^ plane workspace for one N-vector chunk: 4-D view (j % 4, n % 8, j / 4, n / 8)
+// with strides (4 B, ld, 16 B, 8 ld) so a {4, 8, 16, N / 8} box lands in shared memory in exactly the
+// K-major canonical layout of k_off (row = vector).  Needs nv % 8 == 0 (no plane past the last one
+// is addressed) and 16-byte aligned planes.
+template <int N>
+static bool make_xmap(CUtensorMap *m, const float *src, int64_t ld, int nv)
+{
+    using Encode = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode encode = [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<Encode>(fn);
+    }();
+    if (!encode || !src || (nv & 7) || (ld & 3) || ld <= 0 || (reinterpret_cast<uintptr_t>(src) & 15)) return false;
+    const cuuint64_t dims[4] = {4, 8, (cuuint64_t)(ld / 4), (cuuint64_t)(nv / 8)};
+    const cuuint64_t strides[3] = {(cuuint64_t)ld * 4, 16, (cuuint64_t)ld * 32};
+    const cuuint32_t box[4] = {4, 8, (cuuint32_t)(umma::KC / 4), (cuuint32_t)(N / 8)};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(src), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // Launcher: N from nv (8 / 16 / 32 / 64-vector chunks), one CTA per SM (persistent).
@@ -420,8 +548,11 @@ cudaError_t launch_umma_rows(int mode, const Task *t, int ntask, const Blk *b, c
         if ((err = attr) != cudaSuccess) return;
         const int nwork = ntask * ((nv + N - 1) / N);
         const int grid = nwork < nsm ? nwork : nsm;
-        if (mode == MODE_WRITE) kw<<<grid, umma::NWARPS * 32, C::SMEM, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv);
-        else                    ka<<<grid, umma::NWARPS * 32, C::SMEM, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv);
+        alignas(64) CUtensorMap tm;
+        memset(&tm, 0, sizeof tm);
+        const int use_tm = (N >= 8 && make_xmap<N>(&tm, src, src_ld, nv)) ? 1 : 0;
+        if (mode == MODE_WRITE) kw<<<grid, umma::NWARPS * 32, C::SMEM, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv, tm, use_tm);
+        else                    ka<<<grid, umma::NWARPS * 32, C::SMEM, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv, tm, use_tm);
         err = cudaGetLastError();
     };
     if (nv <= 8) go(std::integral_constant<int, 8>{});
