@@ -56,7 +56,7 @@ struct Cfg {
     // accumulators per block: k-step k accumulates into partial k % NACC, so the MMAs of a block
     // form NACC independent chains -- dependent MMAs on one accumulator serialise on the MMA
     // latency (measured: a 2-chain block of 8 M=128 x N=32 MMAs took ~1 us)
-    static constexpr int NACC = N <= 16 ? 8 : (N <= 32 ? 4 : 2);
+    static constexpr int NACC = 2;
     // accumulator buffers in flight (MMA of block b waits for the epilogue to drain block b - NB)
     static constexpr int NB = 512 / (NACC * 2 * N) < 4 ? 512 / (NACC * 2 * N) : 4;   // >= 2
     static constexpr int TCOLS = NB * NACC * 2 * N; // buffers x NACC partials x 2N columns (128..512)
