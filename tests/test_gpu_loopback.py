@@ -37,6 +37,9 @@ CASES = {
     "rand-k25-nv20-chunks": lambda: (_rand(5000, 64, 25, 0.9, 8), 20, "f64"),
     "rand-k64-nv64": lambda: (_rand(4000, 64, 64, 1.1, 10), 64, "f64"),
     "rand-k16-fp32-nv5": lambda: (_rand(4000, 32, 16, 0.9, 9), 5, "f32"),
+    # tcgen05 FP32 coupling with the x^ tensor map (k = 64, nv % 8 == 0) and the off-diagonal
+    # blocks from the received x^ (per-vector bulk copies)
+    "rand-k64-fp32-nv16": lambda: (_rand(4000, 64, 64, 1.1, 13), 16, "f32"),
     "top-tree-eta3": lambda: (_rand(5000, 32, 16, 3.0, 7), 2, "f64"),
     "top-tree-root-block": lambda: (with_root_coupling(_rand(3000, 32, 12, 0.9, 12)), 4, "f64"),
 }
