@@ -402,6 +402,10 @@ def run_leg(leg, args, P, rank, dev, pkg, torch, dist, want_cpu, samplers, laten
                     "coupling_diag": "k_cta<coupling rows>", "coupling_leaf": "k_cta<coupling rows>",
                     "coupling_offdiag": "k_cta<coupling rows, off-diagonal>", "down_transfer": "k_cta<downsweep levels>",
                     "leaf_u": "k_cta<leaves: expansion + dense + epilogue>", "dense": "k_cta<leaves: expansion + dense + epilogue>"})
+    if dtype == "f32" and min(nvs) >= 5 and os.environ.get("H2_ENGINE") != "warp":   # tcgen05 engine
+        kof.update({"coupling_diag": "k_umma<rows> (tcgen05)", "coupling_leaf": "k_umma<rows> (tcgen05)",
+                    "coupling_offdiag": "k_umma<rows> (tcgen05)",
+                    "leaf_u": "k_umma<leaf> (tcgen05; + leaf-level E rows)", "dense": "k_umma<leaf> (tcgen05; + leaf-level E rows)"})
     if name.endswith(":sym"):
         kof.update({"coupling_diag": "k_sym_rows", "coupling_leaf": "k_sym_rows", "leaf_u": "k_sym_leaf",
                     "dense": "k_sym_leaf"})

@@ -278,6 +278,7 @@ struct h2_ctx {
     Blk *d_blks = nullptr;
     PackSeg *d_segs = nullptr;
     Phase up_leaf, coup_off[3], coup_off_leaf[3], leaf, dense;   // off-diagonal: upper levels / leaf level
+    Phase leafE;                     // leaf-level transfers y^_t += E_t y^_p as rows (tcgen05 leaf path)
     std::vector<Phase> up_lv, top_up_lv, coup_diag, coup_leaf, down_lv;
     struct Stage { TreeStage st; int nctas; int r; };
     std::vector<Stage> up_stages, top_stages, down_stages;
@@ -348,6 +349,10 @@ struct h2_ctx {
     int umma_min_nv = 5;
     bool use_umma(int nv) const { return dtype == H2_F32 && nv >= umma_min_nv; }
     int launches_cta = 0;
+    // tcgen05 FP32 leaf path: device slot of the per-call X tensor map (FP32 handles)
+    void *d_xmap = nullptr;
+    int launches_umma = 0;
+    bool use_umma_leaf(int nv) const { return use_umma(nv) && d_xmap && leaf.r <= 64; }
 };
 
 namespace {
@@ -738,6 +743,11 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         h->dargs = dalloc(h, sizeof(CallArgs<double>), err);
         if (!h->dargs) H2_TRY(cuda_fail(h, err, "cudaMalloc(args)"));
         H2_TRYC(cudaMemset(h->dargs, 0, sizeof(CallArgs<double>)));
+        if (h->dtype == H2_F32) {
+            h->d_xmap = dalloc(h, 256, err);
+            if (!h->d_xmap) H2_TRY(cuda_fail(h, err, "cudaMalloc(xmap)"));
+            H2_TRYC(cudaMemset(h->d_xmap, 0, 256));
+        }
         int least = 0, greatest = 0;
         H2_TRYC(cudaDeviceGetStreamPriorityRange(&least, &greatest));
         // the tree sweeps (captured on cap_stream) get the highest priority, the leaf-level
@@ -1248,6 +1258,16 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             tk.nblk = (int32_t)(blks.size() - tk.blk0);
             tasks.push_back(tk);
         }
+        // the same E blocks as row tasks y^_t += E_t y^_p (the tcgen05 FP32 leaf path applies the
+        // leaf-level transfer before its U + dense kernel)
+        h->leafE.t0 = tasks.size();
+        h->leafE.n = hasE ? (int)nleaf : 0;
+        h->leafE.r = kq;
+        if (hasE)
+            for (int64_t t = 0; t < nleaf; ++t) {
+                const Task &lt = tasks[h->leaf.t0 + t];
+                tasks.push_back(Task{h->yh_base[q] + t * kq, lt.blk0, 1, (uint8_t)kq, (uint8_t)k[q - 1], (uint8_t)kq, 0});
+            }
     }
     // (7) dense near field + epilogue (Y = alpha A_de X + beta Y), one task per leaf
     {
@@ -1468,6 +1488,7 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
     // CTA engine: k_set_args, up_leaf, one launch per coupling class / transfer level, the leaves
     h->launches_cta = 3 + (int)h->coup_leaf.size() + (int)h->up_lv.size() + (int)h->coup_diag.size() +
                       (int)h->down_lv.size() + dist;
+    h->launches_umma = h->launches_per_call + 1 + (h->leafE.n ? 1 : 0);   // + k_set_xmap, + the E rows
     *out = h;
     return H2_OK;
 #undef H2_TRY
@@ -1574,7 +1595,9 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     const bool nccl = L.P > 1 && part == PART_ALL;
     // profiling (and loopback groups) serialize the side stream onto the main one so every
     // phase's events bracket only its own kernels (clean per-kernel durations for the roofline)
-    cudaStream_t s_leafc = (h->prof || h->group) ? st : h->s_leafc;
+    // H2_SIDE_STREAM=0: the leaf coupling on the main stream too (A/B switch)
+    static const bool side = [] { const char *e = getenv("H2_SIDE_STREAM"); return !(e && e[0] == '0'); }();
+    cudaStream_t s_leafc = (h->prof || h->group || !side) ? st : h->s_leafc;
     // CTA-tile engine (FP64, nv >= cta_min_nv): the same tasks, one CTA per output node
     const bool cta = h->use_cta(nv);
     auto cjob = [&](const Phase &ph, int kind, int mode, const void *src, int64_t src_ld, void *dst,
@@ -1803,6 +1826,12 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
         CtaJob j = cjob(h->leaf, CK_LEAF, MODE_WRITE, nullptr, 0, nullptr, 0);
         j.dtasks = T0(h->dense);
         H2_CUDA(h, launch_cta(j, std::max(h->leaf.r, kq), h->nsm, st));
+    } else if (h->use_umma_leaf(nv)) {
+        // FP32 on tcgen05: y^_t += E_t y^_p as rows, then U y^_t + dense row with the X tensor map
+        if (h->leafE.n) H2_CUDA(h, rows(MODE_ACCUM, h->leafE, yh, h->yh_plane, yh, h->yh_plane, st));
+        H2_CUDA(h, launch_umma_leaf(T0(h->leaf), T0(h->dense), h->leaf.n, h->d_blks, (const float *)yh, h->yh_plane,
+                                    (const CallArgs<float> *)h->dargs, (const float *)h->hrecv, h->d_xmap, nv,
+                                    h->nsm, st));
     } else {
         H2_CUDA(h, launch_leaf_dense<T>(T0(h->leaf), T0(h->dense), h->leaf.n, h->d_blks, yh, h->yh_plane, args,
                                         (const T *)h->hrecv, nv, kq, kp, h->leaf.r, st));
@@ -1862,6 +1891,7 @@ int run_matvec(h2_ctx *h, T alpha, const T *X, int64_t ldx, T beta, T *Y, int64_
     }
     H2_DBG("rank %d: matvec nv=%d warm=%d graph=%d", h->L.p, nv, (int)h->warm[nv], (int)(h->graph[nv] != nullptr));
     H2_CUDA(h, launch_set_args<T>((CallArgs<T> *)h->dargs, X, ldx, Y, ldy, alpha, beta, st));
+    if (h->use_umma_leaf(nv)) H2_CUDA(h, launch_set_xmap(h->d_xmap, (const float *)X, ldx, nv, st));
     if (h->prof || !h->warm[nv]) {
         h->warm[nv] = true;            // first call per nv runs eagerly (sets kernel attributes)
         return enqueue<T>(h, nv, st);
@@ -1990,6 +2020,7 @@ int group_matvec(h2_ctx *const *hs, int P, T alpha, const void *const *X, T beta
         }
         H2_CUDA(h, launch_set_args<T>((CallArgs<T> *)h->dargs, (const T *)X[o], h->n_local, (T *)Y[o], h->n_local,
                                       alpha, beta, st));
+        if (h->use_umma_leaf(nv)) H2_CUDA(h, launch_set_xmap(h->d_xmap, (const float *)X[o], h->n_local, nv, st));
         int rc = enqueue<T>(h, nv, st, PART_UP);
         if (rc != H2_OK) return rc;
     }
@@ -2044,7 +2075,7 @@ extern "C" int h2_stats(h2_handle h, int nv, double *flops, double *bytes, doubl
         for (const auto &pr : h->peers) x += (double)(pr.xr_cnt + pr.hr_cnt) * nv * h->esz;
         *xchg_bytes = x;
     }
-    if (launches) *launches = h->use_cta(nv) ? h->launches_cta : h->launches_per_call;
+    if (launches) *launches = h->use_cta(nv) ? h->launches_cta : (h->use_umma_leaf(nv) ? h->launches_umma : h->launches_per_call);
     return H2_OK;
 }
 

@@ -172,4 +172,11 @@ cudaError_t launch_cta(const CtaJob &j, int rmax, int nsm, cudaStream_t s);
 // with r, c <= 64, nv >= 5.  Same arguments as launch_rows<float> plus the SM count.
 cudaError_t launch_umma_rows(int mode, const Task *t, int ntask, const Blk *b, const float *src, int64_t src_ld,
                              float *dst, int64_t dst_ld, int nv, int nsm, cudaStream_t s);
+// The fused-leaf form (U y^_t + dense row, alpha/beta epilogue into Y; the leaf-level E transfer
+// already applied to y^ by a rows launch).  xmap: 256-byte device slot holding the X tensor map
+// and its valid flag, written per call by launch_set_xmap (before the captured graph).
+cudaError_t launch_umma_leaf(const Task *lt, const Task *dt, int ntask, const Blk *b, const float *yh, int64_t yh_ld,
+                             const CallArgs<float> *args, const float *halo, const void *xmap, int nv, int nsm,
+                             cudaStream_t s);
+cudaError_t launch_set_xmap(void *dmap, const float *X, int64_t ldx, int nv, cudaStream_t s);
 }  // namespace h2

@@ -1147,7 +1147,9 @@ static inline void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    // H2_PDL=0: plain stream order (A/B switch)
+    static const bool pdl = [] { const char *e = getenv("H2_PDL"); return !(e && e[0] == '0'); }();
+    cfg.numAttrs = pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

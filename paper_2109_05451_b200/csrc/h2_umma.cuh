@@ -219,27 +219,122 @@ __device__ __forceinline__ void split4(const float4 &v, float4 &h, float4 &l)
 
 }  // namespace umma
 
-template <int N, int MODE>
+// One launch's work description (kernel parameter).  Rows (LEAF = false): task t = output node
+// tasks[t], blocks blks[blk0 .. blk0 + nblk), x from src (plane ld src_ld, or per-block xld), output
+// dst (+)= .  Leaf (LEAF = true): task t = leaf tasks[t] ([E][U]; E already applied to y^ by a
+// rows launch) and dense row dtasks[t]; block 0 is U_t (x = y^_t from src), blocks 1.. the dense
+// row (x = rows of the caller's X, or of the halo); output Y = alpha (U y^_t + sum D x) + beta Y.
+struct UJob {
+    const Task *tasks;
+    const Task *dtasks;
+    const Blk *blks;
+    int ntask;
+    int nv;
+    const float *src;          // rows: x^ plane; leaf: y^ plane
+    int64_t src_ld;
+    float *dst;                // rows
+    int64_t dst_ld;
+    const CallArgs<float> *args;   // leaf: X, Y, ldx, ldy, alpha, beta
+    const float *halo;             // leaf: x rows received from peers (Blk::x < 0)
+    const CUtensorMap *xmap;       // leaf: tensor map of X in global memory (written per call, followed by
+                                   // an int: valid for this call), or null
+    int use_tm;                    // the kernel-parameter map (of src) is valid
+};
+
+namespace umma {
+struct BInfo {
+    const float *A;
+    const float *x;
+    int64_t ld;
+    int r, c, xr;
+    int tm;        // 0: no tensor copy, 1: the src map (kernel parameter), 2: the X map (global)
+    int tc2;       // tensor coordinate of the block's first x row (row / 4)
+};
+
+template <bool LEAF>
+__device__ __forceinline__ int nblocks(const UJob &j, const Task &tk, int t)
+{
+    return LEAF ? 1 + j.dtasks[t].nblk : tk.nblk;
+}
+
+// block bi of task t (vector chunk n0): operand addresses, shape, and which tensor map carries x
+template <bool LEAF>
+__device__ __forceinline__ BInfo block_info(const UJob &j, const Task &tk, int t, int bi, int n0, bool xmap_ok)
+{
+    BInfo o;
+    if (!LEAF) {
+        const Blk b = j.blks[tk.blk0 + bi];
+        o.A = static_cast<const float *>(b.A);
+        o.r = tk.r;
+        o.c = tk.c;
+        o.ld = b.xld ? (int64_t)b.xld : j.src_ld;
+        o.x = j.src + b.x + (int64_t)n0 * o.ld;
+        o.xr = b.xrows;
+        o.tm = (j.use_tm && !b.xld && !(b.x & 3) && b.xrows == o.c) ? 1 : 0;
+        o.tc2 = (int)(b.x >> 2);
+        return o;
+    }
+    if (bi == 0) {
+        const Blk b = j.blks[tk.blk0 + ((tk.flags & TF_HAS_E) ? 1 : 0)];
+        o.A = static_cast<const float *>(b.A);
+        o.r = tk.r;
+        o.c = b.xrows;
+        o.ld = j.src_ld;
+        o.x = j.src + b.x + (int64_t)n0 * o.ld;
+        o.xr = b.xrows;
+        o.tm = (j.use_tm && !(b.x & 3)) ? 1 : 0;
+        o.tc2 = (int)(b.x >> 2);
+        return o;
+    }
+    const Task dk = j.dtasks[t];
+    const Blk b = j.blks[dk.blk0 + bi - 1];
+    o.A = static_cast<const float *>(b.A);
+    o.r = dk.r;
+    o.c = dk.c;
+    o.xr = b.xrows;
+    if (b.x >= 0) {
+        o.ld = j.args->ldx;
+        o.x = j.args->X + b.x + (int64_t)n0 * o.ld;
+        o.tm = (xmap_ok && !(b.x & 3) && b.xrows == o.c) ? 2 : 0;
+        o.tc2 = (int)(b.x >> 2);
+    } else {
+        o.ld = b.xld;
+        o.x = j.halo + (-b.x - 1) + (int64_t)n0 * o.ld;
+        o.tm = 0;
+        o.tc2 = 0;
+    }
+    return o;
+}
+
+template <bool LEAF>
+__device__ __forceinline__ int block_c(const UJob &j, const Task &tk, int t, int bi)
+{
+    if (!LEAF) return tk.c;
+    if (bi == 0) return j.blks[tk.blk0 + ((tk.flags & TF_HAS_E) ? 1 : 0)].xrows;
+    return j.dtasks[t].c;
+}
+}  // namespace umma
+
+template <int N, int MODE, bool LEAF>
 __global__ void __launch_bounds__(umma::NWARPS * 32, 1)
-k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks, const float *__restrict__ src,
-            int64_t src_ld, float *__restrict__ dst, int64_t dst_ld, int nv, const __grid_constant__ CUtensorMap tmx,
-            int use_tm)
+k_umma(const __grid_constant__ UJob j, const __grid_constant__ CUtensorMap tmx)
 {
     using namespace umma;
     using C = Cfg<N>;
     constexpr int NR = C::NR, NC = C::NC;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float *ops = reinterpret_cast<float *>(smem_raw);                  // NC operand stages (MMA reads)
-    float *raw = ops + NC * C::OPS;                                    // NR raw stages (cp.async lands)
+    float *raw = ops + NC * C::OPS;                                    // NR raw stages (copies land)
     uint64_t *bars = reinterpret_cast<uint64_t *>(raw + NR * C::RAW);
     uint64_t *raw_full = bars, *raw_empty = bars + NR, *op_full = bars + 2 * NR, *op_empty = op_full + NC;
     uint64_t *acc_full = op_empty + NC, *acc_empty = acc_full + C::NB;
-    int4 *meta = reinterpret_cast<int4 *>(acc_empty + C::NB);              // per raw stage: c, A ld, x rows, c8
+    int4 *meta = reinterpret_cast<int4 *>(acc_empty + C::NB);          // per raw stage: c, A ld, x rows, c8
     uint32_t *tbase_p = reinterpret_cast<uint32_t *>(meta + NR);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int G = gridDim.x;
+    const int nv = j.nv;
     const int nch = (nv + N - 1) / N;
-    const int nwork = ntask * nch;
+    const int nwork = j.ntask * nch;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NR; ++i) {
@@ -268,37 +363,44 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
 
     if (wid == W_PROD) {
         // ===================================================================== producer
-        // A_b (r x c, contiguous) as one bulk copy and each x vector as one bulk copy when sizes and
-        // addresses are 16-byte multiples (the coupling: r = c = k, x^ planes); 4-byte cp.async
-        // otherwise (odd ranks), then a plain arrive once those landed.
+        // A_b (r x c, contiguous) as one bulk copy; x either as ONE tensor copy of all N vectors
+        // straight into the K-major layout (plane sources, the caller's X through the per-call
+        // map), or one bulk copy per vector into [n][XLDR] (received rows), or 4-byte cp.async
+        // (odd shapes), then a plain arrive once those landed.  (The TMA engine serialises
+        // requests at ~125 cycles each: 17 requests per block -- A plus 16 vectors -- paced the
+        // kernel at ~2 us per block.)
+        bool xmap_ok = false;
+        if (LEAF && j.xmap) {
+            xmap_ok = *reinterpret_cast<const volatile int *>(reinterpret_cast<const char *>(j.xmap) + 128) != 0;
+            if (xmap_ok && lane == 0)
+                asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(j.xmap) : "memory");
+        }
+        __syncwarp();
         int it = 0;
         for (int w = blockIdx.x; w < nwork; w += G) {
             const int t = w / nch, n0 = (w - t * nch) * N;
             const int nvc = min(N, nv - n0);
-            const Task tk = tasks[t];
-            const int r = tk.r, c = tk.c, c8 = (c + 7) & ~7;
-            for (int bi = 0; bi < tk.nblk; ++bi, ++it) {
+            const Task tk = j.tasks[t];
+            const int nb = nblocks<LEAF>(j, tk, t);
+            for (int bi = 0; bi < nb; ++bi, ++it) {
                 const int s = it % NR;
                 if (it >= NR) mb_wait(raw_empty + s, ((it / NR) - 1) & 1);
-                const Blk b = blks[tk.blk0 + bi];
-                const float *A = static_cast<const float *>(b.A);
-                const int64_t ld = b.xld ? (int64_t)b.xld : src_ld;
-                const float *x = src + b.x + (int64_t)n0 * ld;
-                const int xr = b.xrows;
+                const BInfo bk = block_info<LEAF>(j, tk, t, bi, n0, xmap_ok);
+                const int r = bk.r, c = bk.c, c8 = (c + 7) & ~7, xr = bk.xr;
+                const float *A = bk.A, *x = bk.x;
+                const int64_t ld = bk.ld;
                 float *As = raw + s * C::RAW, *Xs = As + C::AEL;
                 const bool abulk = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && !((r * c) & 3) && !(r & 3);
                 const bool xbulk = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && !(ld & 3) && !(xr & 3) && xr > 0;
-                // x^ straight into the K-major layout with ONE tensor copy (all N vectors) when it
-                // comes from the launch's source plane; else one bulk copy per vector into [n][XLDR].
-                // (The TMA engine serialises requests at ~125 cycles each: 17 requests per block --
-                // A plus 16 vectors -- paced the kernel at ~2 us per block.)
-                const bool xtm = use_tm && !b.xld && !(b.x & 3) && xr == c && !(n0 & 7);
+                const int xtm = (n0 & 7) ? 0 : bk.tm;
                 if (lane == 0) meta[s] = make_int4(c, abulk ? r : MM, xr, c8 | (xtm ? 0x10000 : 0));
                 if (abulk && (xtm || xbulk)) {
                     if (lane == 0) {
-                        mb_expect_tx(raw_full + s, (uint32_t)(r * c) * 4u + (xtm ? (uint32_t)C::XEL * 4u : (uint32_t)(nvc * xr) * 4u));
+                        mb_expect_tx(raw_full + s, (uint32_t)(r * c) * 4u +
+                                                       (xtm ? (uint32_t)C::XEL * 4u : (uint32_t)(nvc * xr) * 4u));
                         bulk_g2s(As, A, (uint32_t)(r * c) * 4u, raw_full + s);
-                        if (xtm) tensor4_g2s(Xs, &tmx, 0, 0, (int)(b.x >> 2), n0 >> 3, raw_full + s);
+                        if (xtm == 1) tensor4_g2s(Xs, &tmx, 0, 0, bk.tc2, n0 >> 3, raw_full + s);
+                        else if (xtm == 2) tensor4_g2s(Xs, j.xmap, 0, 0, bk.tc2, n0 >> 3, raw_full + s);
                     }
                     __syncwarp();
                     if (!xtm)
@@ -307,12 +409,12 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
                 } else {
                     const int la = abulk ? r : MM;
                     for (int q = lane; q < c * r; q += 32) {
-                        const int m = q % r, j = q / r;
-                        cp4(As + j * la + m, A + (int64_t)j * r + m, true);
+                        const int m = q % r, jj = q / r;
+                        cp4(As + jj * la + m, A + (int64_t)jj * r + m, true);
                     }
                     for (int q = lane; q < nvc * xr; q += 32) {
-                        const int j = q % xr, n = q / xr;
-                        cp4(Xs + n * C::XLDR + j, x + (int64_t)n * ld + j, true);
+                        const int jj = q % xr, n = q / xr;
+                        cp4(Xs + n * C::XLDR + jj, x + (int64_t)n * ld + jj, true);
                     }
                     asm volatile("cp.async.wait_all;\n" ::: "memory");
                     __syncwarp();
@@ -327,8 +429,10 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
         const int cm = ct & (MM - 1), cjh = ct / MM;            // A: row, first 4-column chunk
         int it = 0;
         for (int w = blockIdx.x; w < nwork; w += G) {
-            const Task tk = tasks[w / nch];
-            for (int bi = 0; bi < tk.nblk; ++bi, ++it) {
+            const int t = w / nch;
+            const Task tk = j.tasks[t];
+            const int nb = nblocks<LEAF>(j, tk, t);
+            for (int bi = 0; bi < nb; ++bi, ++it) {
                 const int rs = it % NR, cs = it % NC;
                 mb_wait(raw_full + rs, (it / NR) & 1);
                 if (it >= NC) mb_wait(op_empty + cs, ((it / NC) - 1) & 1);
@@ -337,7 +441,6 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
                 const bool xk = mt.w >> 16;
                 const float *Ar = raw + rs * C::RAW, *Xr = Ar + C::AEL;
                 float *Ah = ops + cs * C::OPS, *Al = Ah + C::AEL, *Xh = Al + C::AEL, *Xl = Xh + C::XEL;
-                {
                 // A: thread = (row m, every CJ-th 4-column chunk); a warp reads 32 consecutive rows of
                 // one column per LDS (conflict-free) and writes 32 rows' 16-byte chunks (8 distinct
                 // banks per phase).  Columns >= c are zero (x rows there are zero too, but 0 x stale
@@ -348,41 +451,40 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
                     const float *ap = Ar + cm;
 #pragma unroll
                     for (int i = 0; i < KC / (4 * CJ); ++i) {
-                        const int j = 4 * (cjh + CJ * i);
-                        float4 v = make_float4(ap[(j + 0) * MM], ap[(j + 1) * MM], ap[(j + 2) * MM], ap[(j + 3) * MM]);
+                        const int jj = 4 * (cjh + CJ * i);
+                        float4 v = make_float4(ap[(jj + 0) * MM], ap[(jj + 1) * MM], ap[(jj + 2) * MM], ap[(jj + 3) * MM]);
                         float4 h, l;
                         split4(v, h, l);
-                        const int o = k_off(cm, j);
+                        const int o = k_off(cm, jj);
                         *reinterpret_cast<float4 *>(Ah + o) = h;
                         *reinterpret_cast<float4 *>(Al + o) = l;
                     }
                 } else {
                     const bool mrow = cm < la;
-                    for (int j = 4 * cjh; j < c8; j += 4 * CJ) {
+                    for (int jj = 4 * cjh; jj < c8; jj += 4 * CJ) {
                         float4 v;
-                        v.x = (mrow && j + 0 < c) ? Ar[(j + 0) * la + cm] : 0.f;
-                        v.y = (mrow && j + 1 < c) ? Ar[(j + 1) * la + cm] : 0.f;
-                        v.z = (mrow && j + 2 < c) ? Ar[(j + 2) * la + cm] : 0.f;
-                        v.w = (mrow && j + 3 < c) ? Ar[(j + 3) * la + cm] : 0.f;
+                        v.x = (mrow && jj + 0 < c) ? Ar[(jj + 0) * la + cm] : 0.f;
+                        v.y = (mrow && jj + 1 < c) ? Ar[(jj + 1) * la + cm] : 0.f;
+                        v.z = (mrow && jj + 2 < c) ? Ar[(jj + 2) * la + cm] : 0.f;
+                        v.w = (mrow && jj + 3 < c) ? Ar[(jj + 3) * la + cm] : 0.f;
                         float4 h, l;
                         split4(v, h, l);
-                        const int o = k_off(cm, j);
+                        const int o = k_off(cm, jj);
                         *reinterpret_cast<float4 *>(Ah + o) = h;
                         *reinterpret_cast<float4 *>(Al + o) = l;
                     }
                 }
-                }
                 if (xk) {
                     // x already in the K-major layout (tensor copy): split in place, rows >= xr zero
                     for (int q = ct; q < C::XEL / 4; q += NCONV * 32) {
-                        const int j = 4 * ((q & 127) >> 3);
-                        if (j >= c8) continue;
+                        const int jj = 4 * ((q & 127) >> 3);
+                        if (jj >= c8) continue;
                         float4 v = *reinterpret_cast<const float4 *>(Xr + 4 * q);
-                        if (j + 4 > xr) {
-                            if (j + 0 >= xr) v.x = 0.f;
-                            if (j + 1 >= xr) v.y = 0.f;
-                            if (j + 2 >= xr) v.z = 0.f;
-                            if (j + 3 >= xr) v.w = 0.f;
+                        if (jj + 4 > xr) {
+                            if (jj + 0 >= xr) v.x = 0.f;
+                            if (jj + 1 >= xr) v.y = 0.f;
+                            if (jj + 2 >= xr) v.z = 0.f;
+                            if (jj + 3 >= xr) v.w = 0.f;
                         }
                         float4 h, l;
                         split4(v, h, l);
@@ -390,24 +492,24 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
                         *reinterpret_cast<float4 *>(Xl + 4 * q) = l;
                     }
                 } else {
-                // x: vector-fastest over (vector, 4-row chunk); rows >= xr are zero (vectors >= nvc are
-                // stale: their output columns are never stored)
-                const int nq = c8 >> 2;
-                for (int q = ct; q < N * nq; q += NCONV * 32) {
-                    const int n = q % N, j = 4 * (q / N);
-                    float4 v = *reinterpret_cast<const float4 *>(Xr + n * C::XLDR + j);
-                    if (j + 4 > xr) {
-                        if (j + 0 >= xr) v.x = 0.f;
-                        if (j + 1 >= xr) v.y = 0.f;
-                        if (j + 2 >= xr) v.z = 0.f;
-                        if (j + 3 >= xr) v.w = 0.f;
+                    // x: vector-fastest over (vector, 4-row chunk); rows >= xr are zero (vectors >= nvc
+                    // are stale: their output columns are never stored)
+                    const int nq = c8 >> 2;
+                    for (int q = ct; q < N * nq; q += NCONV * 32) {
+                        const int n = q % N, jj = 4 * (q / N);
+                        float4 v = *reinterpret_cast<const float4 *>(Xr + n * C::XLDR + jj);
+                        if (jj + 4 > xr) {
+                            if (jj + 0 >= xr) v.x = 0.f;
+                            if (jj + 1 >= xr) v.y = 0.f;
+                            if (jj + 2 >= xr) v.z = 0.f;
+                            if (jj + 3 >= xr) v.w = 0.f;
+                        }
+                        float4 h, l;
+                        split4(v, h, l);
+                        const int o = k_off(n, jj);
+                        *reinterpret_cast<float4 *>(Xh + o) = h;
+                        *reinterpret_cast<float4 *>(Xl + o) = l;
                     }
-                    float4 h, l;
-                    split4(v, h, l);
-                    const int o = k_off(n, j);
-                    *reinterpret_cast<float4 *>(Xh + o) = h;
-                    *reinterpret_cast<float4 *>(Xl + o) = l;
-                }
                 }
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 __syncwarp();
@@ -423,9 +525,11 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
         const uint32_t ops_a = su32(ops);
         int it = 0;
         for (int w = blockIdx.x; w < nwork; w += G) {
-            const Task tk = tasks[w / nch];
-            const int ksn = ((tk.c + 7) & ~7) >> 3;
-            for (int bi = 0; bi < tk.nblk; ++bi, ++it) {
+            const int t = w / nch;
+            const Task tk = j.tasks[t];
+            const int nb = nblocks<LEAF>(j, tk, t);
+            for (int bi = 0; bi < nb; ++bi, ++it) {
+                const int ksn = ((block_c<LEAF>(j, tk, t, bi) + 7) & ~7) >> 3;
                 const int cs = it % NC, ab = it % C::NB;
                 mb_wait(op_full + cs, (it / NC) & 1);
                 if (it >= C::NB) mb_wait(acc_empty + ab, ((it / C::NB) - 1) & 1);
@@ -453,15 +557,19 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
         for (int w = blockIdx.x; w < nwork; w += G) {
             const int t = w / nch, n0 = (w - t * nch) * N;
             const int nvc = min(N, nv - n0);
-            const Task tk = tasks[t];
-            const bool live = row < tk.r;
-            float *out = dst + tk.out + row + (int64_t)n0 * dst_ld;
+            const Task tk = j.tasks[t];
+            const int nb = nblocks<LEAF>(j, tk, t);
+            const bool live = row < (LEAF ? (int)tk.rows : (int)tk.r);
+            float *out;
+            int64_t old;
+            if (LEAF) { old = j.args->ldy; out = j.args->Y + tk.out + row + (int64_t)n0 * old; }
+            else      { old = j.dst_ld; out = j.dst + tk.out + row + (int64_t)n0 * old; }
             float acc[N];
 #pragma unroll
             for (int n = 0; n < N; ++n)
-                acc[n] = (MODE == MODE_ACCUM && half == 0 && live && n < nvc) ? out[(int64_t)n * dst_ld] : 0.f;
-            const int npart = min((((int)tk.c + 7) >> 3), C::NACC);
-            for (int bi = 0; bi < tk.nblk; ++bi, ++it) {
+                acc[n] = (!LEAF && MODE == MODE_ACCUM && half == 0 && live && n < nvc) ? out[(int64_t)n * old] : 0.f;
+            for (int bi = 0; bi < nb; ++bi, ++it) {
+                const int npart = min((block_c<LEAF>(j, tk, t, bi) + 7) >> 3, C::NACC);
                 const int ab = it % C::NB;
                 mb_wait(acc_full + ab, (it / C::NB) & 1);
                 tc_fence_after();
@@ -487,9 +595,20 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
             }
             asm volatile("bar.sync 1, 128;\n" ::: "memory");
             if (half == 0 && live) {
+                if (LEAF) {
+                    const float alpha = j.args->alpha, beta = j.args->beta;
 #pragma unroll
-                for (int n = 0; n < N; ++n)
-                    if (n < nvc) out[(int64_t)n * dst_ld] = acc[n] + cmb[n * 64 + row];
+                    for (int n = 0; n < N; ++n)
+                        if (n < nvc) {
+                            float *p = out + (int64_t)n * old;
+                            const float v = acc[n] + cmb[n * 64 + row];
+                            *p = (beta == 0.f) ? alpha * v : fmaf(alpha, v, beta * *p);
+                        }
+                } else {
+#pragma unroll
+                    for (int n = 0; n < N; ++n)
+                        if (n < nvc) out[(int64_t)n * old] = acc[n] + cmb[n * 64 + row];
+                }
             }
             asm volatile("bar.sync 1, 128;\n" ::: "memory");
         }
@@ -502,12 +621,12 @@ k_umma_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ b
     }
 }
 
-// Tensor map of an x^ plane workspace for one N-vector chunk: 4-D view (j % 4, n % 8, j / 4, n / 8)
-// with strides (4 B, ld, 16 B, 8 ld) so a {4, 8, 16, N / 8} box lands in shared memory in exactly the
-// K-major canonical layout of k_off (row = vector).  Needs nv % 8 == 0 (no plane past the last one
-// is addressed) and 16-byte aligned planes.
-template <int N>
-static bool make_xmap(CUtensorMap *m, const float *src, int64_t ld, int nv)
+// Tensor map of an x^ plane workspace (or of the caller's X: the same column-major form) for one
+// N-vector chunk: 4-D view (j % 4, n % 8, j / 4, n / 8) with strides (4 B, ld, 16 B, 8 ld) so a
+// {4, 8, 16, N / 8} box lands in shared memory in exactly the K-major canonical layout of k_off
+// (row = vector).  Needs nv % 8 == 0 (no plane past the last one is addressed) and 16-byte
+// aligned planes.
+static bool make_xmap(CUtensorMap *m, const float *src, int64_t ld, int nv, int N)
 {
     using Encode = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                 const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
@@ -530,36 +649,93 @@ static bool make_xmap(CUtensorMap *m, const float *src, int64_t ld, int nv)
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Launcher: N from nv (8 / 16 / 32 / 64-vector chunks), one CTA per SM (persistent).
-cudaError_t launch_umma_rows(int mode, const Task *t, int ntask, const Blk *b, const float *src, int64_t src_ld,
-                             float *dst, int64_t dst_ld, int nv, int nsm, cudaStream_t s)
+static inline int umma_chunk(int nv) { return nv <= 8 ? 8 : (nv <= 16 ? 16 : (nv <= 32 ? 32 : 64)); }
+
+template <bool LEAF>
+static cudaError_t launch_umma(int mode, UJob j, int nsm, cudaStream_t s)
 {
-    if (ntask == 0) return cudaSuccess;
+    if (j.ntask == 0) return cudaSuccess;
     cudaError_t err = cudaSuccess;
     auto go = [&](auto nt) {
         constexpr int N = decltype(nt)::value;
         using C = umma::Cfg<N>;
-        auto kw = k_umma_rows<N, MODE_WRITE>;
-        auto ka = k_umma_rows<N, MODE_ACCUM>;
+        auto kw = k_umma<N, MODE_WRITE, LEAF>;
+        auto ka = k_umma<N, MODE_ACCUM, LEAF>;
         static cudaError_t attr = [&] {
             cudaError_t e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
             return e == cudaSuccess ? cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) : e;
         }();
         if ((err = attr) != cudaSuccess) return;
-        const int nwork = ntask * ((nv + N - 1) / N);
+        const int nwork = j.ntask * ((j.nv + N - 1) / N);
         const int grid = nwork < nsm ? nwork : nsm;
         alignas(64) CUtensorMap tm;
         memset(&tm, 0, sizeof tm);
-        const int use_tm = (N >= 8 && make_xmap<N>(&tm, src, src_ld, nv)) ? 1 : 0;
-        if (mode == MODE_WRITE) kw<<<grid, umma::NWARPS * 32, C::SMEM, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv, tm, use_tm);
-        else                    ka<<<grid, umma::NWARPS * 32, C::SMEM, s>>>(t, ntask, b, src, src_ld, dst, dst_ld, nv, tm, use_tm);
+        j.use_tm = make_xmap(&tm, j.src, j.src_ld, j.nv, N) ? 1 : 0;
+        if (mode == MODE_WRITE || LEAF) kw<<<grid, umma::NWARPS * 32, C::SMEM, s>>>(j, tm);
+        else                            ka<<<grid, umma::NWARPS * 32, C::SMEM, s>>>(j, tm);
         err = cudaGetLastError();
     };
-    if (nv <= 8) go(std::integral_constant<int, 8>{});
-    else if (nv <= 16) go(std::integral_constant<int, 16>{});
-    else if (nv <= 32) go(std::integral_constant<int, 32>{});
-    else go(std::integral_constant<int, 64>{});
+    switch (umma_chunk(j.nv)) {
+    case 8: go(std::integral_constant<int, 8>{}); break;
+    case 16: go(std::integral_constant<int, 16>{}); break;
+    case 32: go(std::integral_constant<int, 32>{}); break;
+    default: go(std::integral_constant<int, 64>{}); break;
+    }
     return err;
+}
+
+cudaError_t launch_umma_rows(int mode, const Task *t, int ntask, const Blk *b, const float *src, int64_t src_ld,
+                             float *dst, int64_t dst_ld, int nv, int nsm, cudaStream_t s)
+{
+    UJob j{};
+    j.tasks = t;
+    j.blks = b;
+    j.ntask = ntask;
+    j.nv = nv;
+    j.src = src;
+    j.src_ld = src_ld;
+    j.dst = dst;
+    j.dst_ld = dst_ld;
+    return launch_umma<false>(mode, j, nsm, s);
+}
+
+cudaError_t launch_umma_leaf(const Task *lt, const Task *dt, int ntask, const Blk *b, const float *yh, int64_t yh_ld,
+                             const CallArgs<float> *args, const float *halo, const void *xmap, int nv, int nsm,
+                             cudaStream_t s)
+{
+    UJob j{};
+    j.tasks = lt;
+    j.dtasks = dt;
+    j.blks = b;
+    j.ntask = ntask;
+    j.nv = nv;
+    j.src = yh;
+    j.src_ld = yh_ld;
+    j.args = args;
+    j.halo = halo;
+    j.xmap = static_cast<const CUtensorMap *>(xmap);
+    return launch_umma<true>(MODE_WRITE, j, nsm, s);
+}
+
+// Per call, before the (captured) matvec: the X tensor map written into device memory by a
+// one-thread kernel (stream-ordered: no host buffer reuse race), released to the tensormap proxy.
+__global__ void k_set_xmap(CUtensorMap *dst, const __grid_constant__ CUtensorMap m, int valid)
+{
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(&m);
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+    for (int i = threadIdx.x; i < (int)(sizeof(CUtensorMap) / 16); i += blockDim.x) d4[i] = s4[i];
+    if (threadIdx.x == 0) reinterpret_cast<int *>(dst)[32] = valid;
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("fence.proxy.tensormap::generic.release.gpu;\n" ::: "memory");
+}
+
+cudaError_t launch_set_xmap(void *dmap, const float *X, int64_t ldx, int nv, cudaStream_t s)
+{
+    alignas(64) CUtensorMap m;
+    memset(&m, 0, sizeof m);
+    const int valid = make_xmap(&m, X, ldx, nv, umma_chunk(nv)) ? 1 : 0;
+    k_set_xmap<<<1, 8, 0, s>>>(static_cast<CUtensorMap *>(dmap), m, valid);
+    return cudaGetLastError();
 }
 
 }  // namespace h2
