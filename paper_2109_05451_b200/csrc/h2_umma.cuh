@@ -251,68 +251,22 @@ struct BInfo {
     int tc2;       // tensor coordinate of the block's first x row (row / 4)
 };
 
+__device__ __forceinline__ Blk shfl_blk(const Blk &b, int src)
+{
+    Blk o;
+    o.A = reinterpret_cast<const void *>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(b.A), src));
+    o.x = __shfl_sync(0xffffffffu, b.x, src);
+    o.xrows = __shfl_sync(0xffffffffu, b.xrows, src);
+    o.xld = __shfl_sync(0xffffffffu, b.xld, src);
+    return o;
+}
+
 template <bool LEAF>
 __device__ __forceinline__ int nblocks(const UJob &j, const Task &tk, int t)
 {
     return LEAF ? 1 + j.dtasks[t].nblk : tk.nblk;
 }
 
-// block bi of task t (vector chunk n0): operand addresses, shape, and which tensor map carries x
-template <bool LEAF>
-__device__ __forceinline__ BInfo block_info(const UJob &j, const Task &tk, int t, int bi, int n0, bool xmap_ok)
-{
-    BInfo o;
-    if (!LEAF) {
-        const Blk b = j.blks[tk.blk0 + bi];
-        o.A = static_cast<const float *>(b.A);
-        o.r = tk.r;
-        o.c = tk.c;
-        o.ld = b.xld ? (int64_t)b.xld : j.src_ld;
-        o.x = j.src + b.x + (int64_t)n0 * o.ld;
-        o.xr = b.xrows;
-        o.tm = (j.use_tm && !b.xld && !(b.x & 3) && b.xrows == o.c) ? 1 : 0;
-        o.tc2 = (int)(b.x >> 2);
-        return o;
-    }
-    if (bi == 0) {
-        const Blk b = j.blks[tk.blk0 + ((tk.flags & TF_HAS_E) ? 1 : 0)];
-        o.A = static_cast<const float *>(b.A);
-        o.r = tk.r;
-        o.c = b.xrows;
-        o.ld = j.src_ld;
-        o.x = j.src + b.x + (int64_t)n0 * o.ld;
-        o.xr = b.xrows;
-        o.tm = (j.use_tm && !(b.x & 3)) ? 1 : 0;
-        o.tc2 = (int)(b.x >> 2);
-        return o;
-    }
-    const Task dk = j.dtasks[t];
-    const Blk b = j.blks[dk.blk0 + bi - 1];
-    o.A = static_cast<const float *>(b.A);
-    o.r = dk.r;
-    o.c = dk.c;
-    o.xr = b.xrows;
-    if (b.x >= 0) {
-        o.ld = j.args->ldx;
-        o.x = j.args->X + b.x + (int64_t)n0 * o.ld;
-        o.tm = (xmap_ok && !(b.x & 3) && b.xrows == o.c) ? 2 : 0;
-        o.tc2 = (int)(b.x >> 2);
-    } else {
-        o.ld = b.xld;
-        o.x = j.halo + (-b.x - 1) + (int64_t)n0 * o.ld;
-        o.tm = 0;
-        o.tc2 = 0;
-    }
-    return o;
-}
-
-template <bool LEAF>
-__device__ __forceinline__ int block_c(const UJob &j, const Task &tk, int t, int bi)
-{
-    if (!LEAF) return tk.c;
-    if (bi == 0) return j.blks[tk.blk0 + ((tk.flags & TF_HAS_E) ? 1 : 0)].xrows;
-    return j.dtasks[t].c;
-}
 }  // namespace umma
 
 template <int N, int MODE, bool LEAF>
@@ -329,7 +283,8 @@ k_umma(const __grid_constant__ UJob j, const __grid_constant__ CUtensorMap tmx)
     uint64_t *raw_full = bars, *raw_empty = bars + NR, *op_full = bars + 2 * NR, *op_empty = op_full + NC;
     uint64_t *acc_full = op_empty + NC, *acc_empty = acc_full + C::NB;
     int4 *meta = reinterpret_cast<int4 *>(acc_empty + C::NB);          // per raw stage: c, A ld, x rows, c8
-    uint32_t *tbase_p = reinterpret_cast<uint32_t *>(meta + NR);
+    int *opmeta = reinterpret_cast<int *>(meta + NR);                  // per operand stage: k-steps (0: end)
+    uint32_t *tbase_p = reinterpret_cast<uint32_t *>(opmeta + NC);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int G = gridDim.x;
     const int nv = j.nv;
@@ -376,17 +331,68 @@ k_umma(const __grid_constant__ UJob j, const __grid_constant__ CUtensorMap tmx)
                 asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(j.xmap) : "memory");
         }
         __syncwarp();
+        // descriptors are fetched ahead -- the next work item's task (and dense row) while this one
+        // streams, and the Blk of 32 blocks at a time (one per lane, broadcast by shuffles) -- so
+        // the producer's per-block work is a few register operations and the copies (dependent
+        // descriptor loads from L2 per block measured ~1 us per block on the single producer warp)
+        const float *X = nullptr;
+        int64_t ldx = 0;
+        if (LEAF) { X = j.args->X; ldx = j.args->ldx; }
+        const Task none{};
+        Task tn = blockIdx.x < nwork ? j.tasks[blockIdx.x / nch] : none;
+        Task dn = (LEAF && blockIdx.x < nwork) ? j.dtasks[blockIdx.x / nch] : none;
         int it = 0;
         for (int w = blockIdx.x; w < nwork; w += G) {
             const int t = w / nch, n0 = (w - t * nch) * N;
             const int nvc = min(N, nv - n0);
-            const Task tk = j.tasks[t];
-            const int nb = nblocks<LEAF>(j, tk, t);
-            for (int bi = 0; bi < nb; ++bi, ++it) {
+            const Task tk = tn, dk = dn;
+            if (w + G < nwork) {
+                tn = j.tasks[(w + G) / nch];
+                if (LEAF) dn = j.dtasks[(w + G) / nch];
+            }
+            const int nb = LEAF ? 1 + dk.nblk : tk.nblk;
+            const int64_t ublk = tk.blk0 + ((LEAF && (tk.flags & TF_HAS_E)) ? 1 : 0);
+            for (int s0 = 0; s0 < nb; s0 += 32) {
+                Blk mine{};
+                {
+                    const int q = s0 + lane;
+                    if (q < nb) mine = j.blks[LEAF ? (q == 0 ? ublk : dk.blk0 + q - 1) : tk.blk0 + q];
+                }
+                const int s1 = min(nb, s0 + 32);
+                for (int bi = s0; bi < s1; ++bi, ++it) {
+                const Blk b = shfl_blk(mine, bi - s0);
                 const int s = it % NR;
                 if (it >= NR) mb_wait(raw_empty + s, ((it / NR) - 1) & 1);
-                const BInfo bk = block_info<LEAF>(j, tk, t, bi, n0, xmap_ok);
-                const int r = bk.r, c = bk.c, c8 = (c + 7) & ~7, xr = bk.xr;
+                BInfo bk;
+                bk.A = static_cast<const float *>(b.A);
+                bk.xr = b.xrows;
+                bk.tc2 = (int)(b.x >> 2);
+                if (!LEAF) {
+                    bk.r = tk.r;
+                    bk.c = tk.c;
+                    bk.ld = b.xld ? (int64_t)b.xld : j.src_ld;
+                    bk.x = j.src + b.x + (int64_t)n0 * bk.ld;
+                    bk.tm = (j.use_tm && !b.xld && !(b.x & 3) && b.xrows == bk.c) ? 1 : 0;
+                } else if (bi == 0) {
+                    bk.r = tk.r;
+                    bk.c = b.xrows;
+                    bk.ld = j.src_ld;
+                    bk.x = j.src + b.x + (int64_t)n0 * bk.ld;
+                    bk.tm = (j.use_tm && !(b.x & 3)) ? 1 : 0;
+                } else {
+                    bk.r = dk.r;
+                    bk.c = dk.c;
+                    if (b.x >= 0) {
+                        bk.ld = ldx;
+                        bk.x = X + b.x + (int64_t)n0 * ldx;
+                        bk.tm = (xmap_ok && !(b.x & 3) && b.xrows == bk.c) ? 2 : 0;
+                    } else {
+                        bk.ld = b.xld;
+                        bk.x = j.halo + (-b.x - 1) + (int64_t)n0 * bk.ld;
+                        bk.tm = 0;
+                    }
+                }
+                const int r = bk.r, c = bk.c, c8 = max(16, (c + 7) & ~7), xr = bk.xr;   // >= 2 k-steps
                 const float *A = bk.A, *x = bk.x;
                 const int64_t ld = bk.ld;
                 float *As = raw + s * C::RAW, *Xs = As + C::AEL;
@@ -420,23 +426,35 @@ k_umma(const __grid_constant__ UJob j, const __grid_constant__ CUtensorMap tmx)
                     __syncwarp();
                     if (lane == 0) mb_arrive(raw_full + s);
                 }
+                }
             }
+        }
+        // end of this CTA's block stream: converters and the MMA warp need no task descriptors
+        const int s = it % NR;
+        if (it >= NR) mb_wait(raw_empty + s, ((it / NR) - 1) & 1);
+        if (lane == 0) {
+            meta[s] = make_int4(-1, 0, 0, 0);
+            mb_arrive(raw_full + s);
         }
     } else if (wid >= W_CONV0) {
         // ===================================================================== converters
         const int ct = threadIdx.x - W_CONV0 * 32;              // 0 .. NCONV * 32 - 1
         constexpr int CJ = NCONV * 32 / MM;                     // 4-column chunk groups (4)
         const int cm = ct & (MM - 1), cjh = ct / MM;            // A: row, first 4-column chunk
-        int it = 0;
-        for (int w = blockIdx.x; w < nwork; w += G) {
-            const int t = w / nch;
-            const Task tk = j.tasks[t];
-            const int nb = nblocks<LEAF>(j, tk, t);
-            for (int bi = 0; bi < nb; ++bi, ++it) {
+        for (int it = 0;; ++it) {
+            {
                 const int rs = it % NR, cs = it % NC;
                 mb_wait(raw_full + rs, (it / NR) & 1);
                 if (it >= NC) mb_wait(op_empty + cs, ((it / NC) - 1) & 1);
                 const int4 mt = meta[rs];
+                if (mt.x < 0) {                                  // end marker: pass it on
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (ct == 0) opmeta[cs] = 0;
+                        mb_arrive(op_full + cs);
+                    }
+                    break;
+                }
                 const int c = mt.x, la = mt.y, xr = mt.z, c8 = mt.w & 0xffff;
                 const bool xk = mt.w >> 16;
                 const float *Ar = raw + rs * C::RAW, *Xr = Ar + C::AEL;
@@ -514,6 +532,7 @@ k_umma(const __grid_constant__ UJob j, const __grid_constant__ CUtensorMap tmx)
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 __syncwarp();
                 if (lane == 0) {
+                    if (ct == 0) opmeta[cs] = c8 >> 3;
                     mb_arrive(raw_empty + rs);
                     mb_arrive(op_full + cs);
                 }
@@ -523,15 +542,12 @@ k_umma(const __grid_constant__ UJob j, const __grid_constant__ CUtensorMap tmx)
         // ===================================================================== MMA issuer (whole warp)
         constexpr uint32_t ID = idesc<128, 2 * N>();
         const uint32_t ops_a = su32(ops);
-        int it = 0;
-        for (int w = blockIdx.x; w < nwork; w += G) {
-            const int t = w / nch;
-            const Task tk = j.tasks[t];
-            const int nb = nblocks<LEAF>(j, tk, t);
-            for (int bi = 0; bi < nb; ++bi, ++it) {
-                const int ksn = ((block_c<LEAF>(j, tk, t, bi) + 7) & ~7) >> 3;
+        for (int it = 0;; ++it) {
+            {
                 const int cs = it % NC, ab = it % C::NB;
                 mb_wait(op_full + cs, (it / NC) & 1);
+                const int ksn = opmeta[cs];
+                if (ksn == 0) break;                              // end marker
                 if (it >= C::NB) mb_wait(acc_empty + ab, ((it / C::NB) - 1) & 1);
                 tc_fence_after();
                 const uint32_t hA = ops_a + (uint32_t)(cs * C::OPS) * 4u;     // [A_hi; A_lo], 128 rows
@@ -569,10 +585,11 @@ k_umma(const __grid_constant__ UJob j, const __grid_constant__ CUtensorMap tmx)
             for (int n = 0; n < N; ++n)
                 acc[n] = (!LEAF && MODE == MODE_ACCUM && half == 0 && live && n < nvc) ? out[(int64_t)n * old] : 0.f;
             for (int bi = 0; bi < nb; ++bi, ++it) {
-                const int npart = min((block_c<LEAF>(j, tk, t, bi) + 7) >> 3, C::NACC);
+                constexpr int npart = C::NACC;                  // every block has >= NACC k-steps
                 const int ab = it % C::NB;
                 mb_wait(acc_full + ab, (it / C::NB) & 1);
                 tc_fence_after();
+#pragma unroll
                 for (int a = 0; a < npart; ++a) {
                     const uint32_t ta = tl + (uint32_t)((ab * C::NACC + a) * 2 * N);
 #pragma unroll
