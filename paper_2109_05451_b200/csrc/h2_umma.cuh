@@ -51,8 +51,8 @@ struct Cfg {
     static constexpr int XLDR = KC + 4;             // raw x row pitch (272 B: conflict-free 16 B reads)
     static constexpr int RAW = AEL + N * XLDR;      // raw stage: A as in HBM (ld r), x vectors (ld XLDR)
     static constexpr int OPS = 2 * (AEL + XEL);     // operand stage: A hi, A lo, x hi, x lo
-    static constexpr int NR = N <= 16 ? 6 : (N <= 32 ? 4 : 2);
-    static constexpr int NC = 2;
+    static constexpr int NR = N <= 32 ? 4 : 2;
+    static constexpr int NC = N <= 16 ? 3 : 2;
     // accumulators per block: k-step k accumulates into partial k % NACC, so the MMAs of a block
     // form NACC independent chains -- dependent MMAs on one accumulator serialise on the MMA
     // latency (measured: a 2-chain block of 8 M=128 x N=32 MMAs took ~1 us)
