@@ -35,12 +35,12 @@ sys.path.insert(0, ROOT)
 
 METRIC = "H2 matvec GFLOP/s per GPU and ms/matvec (nv=1,16,64) at 1/2/4/8 B200"
 # a workload name with ":sym" = the same workload on the symmetric-storage path (H2_SYMMETRIC,
-# nv = 1 legs only: SURVEY.md §8(f) NEXT-2)
+# nv = 1 legs only: SURVEY.md §8(f) NEXT-2); ":f32" / ":f64" = one precision of a workload
 SUITES = {
-    "suite": (["cfg2"], ["cfg3", "cfg2:sym", "cfg1"]),
+    "suite": (["cfg2"], ["cfg3", "cfg5:f32", "cfg2:sym", "cfg1"]),
     "cfg2sym": (["cfg2:sym"], []), "cfg4sym": (["cfg4:sym"], []),
     "cfg1": (["cfg1"], []), "cfg2": (["cfg2"], []), "cfg3": (["cfg3"], []), "cfg3s": (["cfg3s"], []),
-    "cfg4": (["cfg4"], []), "cfg5": (["cfg5"], []),
+    "cfg4": (["cfg4"], []), "cfg5": (["cfg5"], []), "cfg5f32": (["cfg5:f32"], []),
 }
 CPU_BUDGET_S = 12.0          # oracle seconds per leg for the cpu_baseline sample
 
@@ -135,6 +135,8 @@ def legs_of(name):
     c = CONFIGS[base]
     if opt == "sym":
         return [(name, dt, (1,)) for dt in c["dtypes"]]
+    if opt in ("f32", "f64"):                 # one precision of a multi-precision workload
+        return [(name, opt, tuple(c["nvs"]))]
     return [(name, dt, tuple(c["nvs"])) for dt in c["dtypes"]]
 
 
