@@ -220,6 +220,24 @@ int h2_pcg(h2_handle K, double scale, const double *diag, const int64_t *C_rowpt
            const double *C_val, const double *b, double *u, double rtol, int maxit, int *iters,
            double *res_hist);
 
+/* ---- Basis orthogonalization (first step) -----------
+ * h2_orthogonalize: in place on the handle's device operator, the QR upsweep of both basis trees
+ *   -- leaves U_t = Q_t R_t (thin Householder QR, diag R >= 0), then per level
+ *   [R_c1 E_c1; R_c2 E_c2] = Q_p R_p with the new transfers E'_c = the halves of Q_p (the same for
+ *   V with F) -- and every coupling block re-expressed, S'_ts = R^U_t S_ts (R^V_s)^T.  The operator
+ *   is unchanged (up to rounding) and every implied level basis has orthonormal columns: the
+ *   pre-processing step of the paper's algebraic recompression.  FP64, one GPU, full storage,
+ *   m <= 128, k^l <= 64, k^q <= m, k^{l-1} <= 2 k^l; synchronous.  Captured matvec graphs stay
+ *   valid (same arrays, new values).  H2_ERR_ARG when unsupported.
+ * h2_export: copy one operator array of the handle to host memory (count elements, checked):
+ *   H2_EXPORT_S  coupling blocks of `level` (k^l x k^l each, column-major, h2_desc CSR order;
+ *                one GPU, full storage), H2_EXPORT_U leaf bases (m x k^q per leaf),
+ *   H2_EXPORT_VT leaf bases stored transposed (k^q x m per leaf), H2_EXPORT_E transfers of `level`
+ *   (k^l x k^{l-1} per node), H2_EXPORT_FT transfers F stored transposed (k^{l-1} x k^l). */
+enum { H2_EXPORT_S = 0, H2_EXPORT_U = 1, H2_EXPORT_VT = 2, H2_EXPORT_E = 3, H2_EXPORT_FT = 4 };
+int h2_orthogonalize(h2_handle h);
+int h2_export(h2_handle h, int what, int level, void *host, int64_t count);
+
 /* Release device memory, the NCCL communicator and streams.  NULL is a no-op. */
 int h2_destroy(h2_handle h);
 

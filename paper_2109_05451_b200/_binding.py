@@ -18,7 +18,9 @@ H2_SYMMETRIC = 1
 EXPORTS = ["h2_create", "h2_matvec", "h2_matvec_ld", "h2_matvec_host", "h2_set_stream", "h2_stats",
            "h2_group_create", "h2_group_matvec", "h2_file_info", "h2_create_from_file", "h2_group_create_from_file", "h2_n_local", "h2_fd_diag", "h2_pcg",
            "h2_set_profiling", "h2_phase_times", "h2_phase_stats",
-           "h2_plan_counts", "h2_plan_census", "h2_destroy", "h2_nccl_unique_id", "h2_last_error", "h2_version"]
+           "h2_plan_counts", "h2_plan_census", "h2_destroy", "h2_nccl_unique_id", "h2_last_error", "h2_version",
+           "h2_orthogonalize", "h2_export"]
+H2_EXPORT_S, H2_EXPORT_U, H2_EXPORT_VT, H2_EXPORT_E, H2_EXPORT_FT = 0, 1, 2, 3, 4
 PHASES = ["up_leaf", "up_transfer", "exchange_top", "coupling_diag", "coupling_offdiag",
           "down_transfer", "leaf_u", "dense", "coupling_leaf"]
 KERNEL_OF_PHASE = {"up_leaf": "k_up_leaf", "up_transfer": "k_sweep<WRITE>", "exchange_top": "k_pack + k_tree",
@@ -74,6 +76,8 @@ def load_library(path=None):
         "h2_phase_times": ([vp, C.POINTER(d), C.POINTER(C.c_int64)], i32),
         "h2_phase_stats": ([vp, i32, C.POINTER(d), C.POINTER(d)], i32),
         "h2_destroy": ([vp], i32),
+        "h2_orthogonalize": ([vp], i32),
+        "h2_export": ([vp, i32, i32, vp, i64], i32),
         "h2_group_create_from_file": ([C.c_char_p, i32, i32, C.POINTER(vp)], i32),
         "h2_n_local": ([vp, C.POINTER(C.c_int64)], i32),
         "h2_file_info": ([C.c_char_p, C.POINTER(C.c_int64)], i32),
@@ -344,6 +348,16 @@ class H2Operator:
         _check(self._lib.h2_plan_counts(self.handle, c))
         keys = ["diag_S", "offdiag_S", "root_S", "diag_D", "offdiag_D", "peers", "recv_nodes", "recv_leaves"]
         return dict(zip(keys, list(c)))
+
+    def orthogonalize(self):
+        """Basis orthogonalization in place (h2_orthogonalize; FP64, one GPU, full storage)."""
+        _check(self._lib.h2_orthogonalize(self.handle))
+
+    def export(self, what, level, count):
+        """Host copy (1-D, count elements) of one operator array (h2_export; H2_EXPORT_*)."""
+        out = np.empty(int(count), dtype=self.np_dtype)
+        _check(self._lib.h2_export(self.handle, int(what), int(level), out.ctypes.data, int(count)))
+        return out
 
     def close(self):
         if getattr(self, "handle", None):

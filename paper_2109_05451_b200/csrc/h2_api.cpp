@@ -352,6 +352,9 @@ struct h2_ctx {
     // tcgen05 FP32 leaf path: device slot of the per-call X tensor map (FP32 handles)
     void *d_xmap = nullptr;
     int launches_umma = 0;
+    // basis orthogonalization (h2_orthogonalize; one GPU, full storage): (t, s) of every coupling
+    // block per level, in the device S[l] order
+    std::vector<std::vector<int2>> orth_pairs;
     bool use_umma_leaf(int nv) const { return use_umma(nv) && d_xmap && leaf.r <= 64; }
 };
 
@@ -801,6 +804,12 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
         } else {
             H2_TRY(put_array(h, d->mem, d->S[l], nb * k[l] * k[l], &h->S[l]));
             ops_stored += (double)nb * k[l] * k[l];
+            if (P == 1) {
+                if (h->orth_pairs.empty()) h->orth_pairs.resize(q + 1);
+                for (int64_t t = 0; t < L.held(l); ++t)
+                    for (int64_t b = d->S_rowptr[l][t]; b < d->S_rowptr[l][t + 1]; ++b)
+                        h->orth_pairs[l].push_back(make_int2((int)t, d->S_col[l][b]));
+            }
         }
     }
     const int64_t nD = d->D_rowptr[nleaf];
@@ -2179,6 +2188,70 @@ extern "C" int h2_plan_counts(h2_handle h, int64_t counts[8])
 {
     if (!h || !counts) return fail(H2_ERR_ARG, "NULL argument");
     memcpy(counts, h->counts, sizeof(h->counts));
+    return H2_OK;
+}
+
+extern "C" int h2_orthogonalize(h2_handle h)
+{
+    if (!h) return fail(H2_ERR_ARG, "handle is NULL");
+    if (h->sticky) return fail(H2_ERR_STATE, "handle unusable after an earlier CUDA/NCCL error");
+    if (h->L.P != 1 || h->dtype != H2_F64 || h->sym || h->group || (int)h->orth_pairs.size() != h->L.q + 1)
+        return fail(H2_ERR_ARG, "h2_orthogonalize: FP64, one GPU, full (non-symmetric) storage only");
+    const int q = h->L.q;
+    std::vector<const int2 *> pairs(q + 1, nullptr);
+    std::vector<int2 *> owned;
+    std::vector<int64_t> nblk(q + 1, 0);
+    std::vector<double *> E(q + 1, nullptr), Ft(q + 1, nullptr), S(q + 1, nullptr);
+    cudaError_t err = cudaStreamSynchronize(h->stream);
+    for (int l = 0; l <= q && err == cudaSuccess; ++l) {
+        nblk[l] = (int64_t)h->orth_pairs[l].size();
+        E[l] = (double *)h->E[l];
+        Ft[l] = (double *)h->Ft[l];
+        S[l] = (double *)h->S[l];
+        if (!nblk[l]) continue;
+        int2 *d = nullptr;
+        err = cudaMalloc(&d, sizeof(int2) * nblk[l]);
+        if (err != cudaSuccess) break;
+        owned.push_back(d);
+        pairs[l] = d;
+        err = cudaMemcpy(d, h->orth_pairs[l].data(), sizeof(int2) * nblk[l], cudaMemcpyHostToDevice);
+    }
+    if (err == cudaSuccess)
+        err = orthogonalize_bases((double *)h->U, (double *)h->Vt, E, Ft, S, pairs, nblk, h->L.k.data(), q, h->L.m,
+                                  h->stream);
+    for (int2 *d : owned) cudaFree(d);
+    if (err == cudaErrorInvalidValue)
+        return fail(H2_ERR_ARG, "h2_orthogonalize: needs m <= 128, k <= 64, k^q <= m, k^{l-1} <= 2 k^l <= 128");
+    if (err != cudaSuccess) return cuda_fail(h, err, "h2_orthogonalize");
+    return H2_OK;
+}
+
+extern "C" int h2_export(h2_handle h, int what, int level, void *host, int64_t count)
+{
+    if (!h || !host) return fail(H2_ERR_ARG, "NULL argument");
+    if (h->sticky) return fail(H2_ERR_STATE, "handle unusable after an earlier CUDA/NCCL error");
+    const int q = h->L.q, m = h->L.m;
+    const int64_t nleaf = (int64_t)h->L.held(q);
+    const void *src = nullptr;
+    int64_t n = 0;
+    if (level < 0 || level > q) return fail(H2_ERR_ARG, "h2_export: level out of range");
+    const int64_t kl = h->L.k[level], kp = level ? h->L.k[level - 1] : 0;
+    switch (what) {
+    case H2_EXPORT_S:                                  // blocks in h2_desc CSR order (one GPU, full storage)
+        src = h->S[level];
+        n = (!h->sym && (int)h->orth_pairs.size() > level) ? (int64_t)h->orth_pairs[level].size() * kl * kl : -1;
+        break;
+    case H2_EXPORT_U:  src = h->U; n = nleaf * m * h->L.k[q]; break;
+    case H2_EXPORT_VT: src = h->Vt; n = nleaf * m * h->L.k[q]; break;
+    case H2_EXPORT_E:  src = level ? h->E[level] : nullptr; n = (int64_t)h->L.held(level) * kl * kp; break;
+    case H2_EXPORT_FT: src = level ? h->Ft[level] : nullptr; n = (int64_t)h->L.held(level) * kl * kp; break;
+    default: return fail(H2_ERR_ARG, "h2_export: unknown array");
+    }
+    if (n < 0) return fail(H2_ERR_ARG, "h2_export: coupling export needs one GPU and full storage");
+    if (!src || n != count) return fail(H2_ERR_ARG, "h2_export: count does not match the array (" + std::to_string(n) + ")");
+    cudaError_t err = cudaStreamSynchronize(h->stream);
+    if (err == cudaSuccess) err = cudaMemcpy(host, src, (size_t)n * h->esz, cudaMemcpyDeviceToHost);
+    if (err != cudaSuccess) return cuda_fail(h, err, "h2_export");
     return H2_OK;
 }
 

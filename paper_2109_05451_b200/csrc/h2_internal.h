@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <string>
+#include <vector>
 
 namespace h2 {
 
@@ -179,4 +180,9 @@ cudaError_t launch_umma_leaf(const Task *lt, const Task *dt, int ntask, const Bl
                              const CallArgs<float> *args, const float *halo, const void *xmap, int nv, int nsm,
                              cudaStream_t s);
 cudaError_t launch_set_xmap(void *dmap, const float *X, int64_t ldx, int nv, cudaStream_t s);
+// Basis orthogonalization in place (h2_k_orth.cu, NEXT-3 step 1): FP64, one GPU, full storage.
+// pairs[l][b] = (t, s) of coupling block b of level l.  Synchronous on s.
+cudaError_t orthogonalize_bases(double *U, double *Vt, const std::vector<double *> &E, const std::vector<double *> &Ft,
+                                const std::vector<double *> &S, const std::vector<const int2 *> &pairs,
+                                const std::vector<int64_t> &nblk, const int *k, int q, int m, cudaStream_t s);
 }  // namespace h2
