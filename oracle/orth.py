@@ -1,5 +1,6 @@
-"""Basis orthogonalization of an H² matrix (§"Algebraic Matrix Compression") —
-CPU oracle, TEST INFRASTRUCTURE (only tests/ may import it; the product path never does).
+"""Basis orthogonalization and the reweighing downsweep of an H² matrix (PAPER.md:540-608,
+§"Algebraic Matrix Compression") — CPU oracle, TEST INFRASTRUCTURE (only tests/ may import it; the
+product path never does).
 
 The paper's pre-processing step of the recompression: "Orthogonalizing a
 basis involves performing QR on the finest level basis and then going up the tree to compute new
@@ -80,3 +81,35 @@ def orthogonalize(h):
     g = copy.copy(h)
     g.U_leaf, g.V_leaf, g.E, g.F, g.S = U, V, E, F, S
     return g, RU, RV
+
+
+def reweigh_R(g):
+    """The reweighing downsweep of the recompression, on an H² matrix g whose
+    V basis is orthogonal (the output of orthogonalize): for every node i of every level, root to
+    leaves, the R factor of the stacked small matrix of Eq. (Btq),
+
+        B^l_i -> [ R^{l-1}_{i+} E^{lT}_i ; S^{lT}_{ij_1} ; ... ; S^{lT}_{ij_b} ]   (PAPER.md:575)
+
+    (the parent part absent at the root; an empty stack gives R = 0).  Returns R[l]: (2^l, k^l, k^l)
+    stored column-major (R^l_i = R[l][i].T, upper triangular, diag >= 0).  The new basis of level l
+    is U^l_i R^{lT}_i."""
+    q, k = g.q, g.ranks
+    R = [None] * (q + 1)
+    for l in range(q + 1):
+        kl = k[l]
+        R[l] = np.zeros((1 << l, kl, kl))
+        for i in range(1 << l):
+            parts = []
+            if l >= 1:
+                parts.append(R[l - 1][i >> 1].T @ g.E[l][i])            # R_{i+} (k^{l-1} sq) E_i^T
+            rp, col = g.S_rowptr[l], g.S_col[l]
+            for b in range(rp[i], rp[i + 1]):
+                parts.append(g.S[l][b])                                 # stored (k, k) col-major = S^T
+            if not parts:
+                continue
+            M = np.vstack(parts)
+            _, Ri = qr_pos(M)                                           # (min(rows, k), k)
+            Rf = np.zeros((kl, kl))
+            Rf[:Ri.shape[0]] = Ri
+            R[l][i] = Rf.T
+    return R

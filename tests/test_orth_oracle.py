@@ -59,3 +59,40 @@ def test_R_is_qr_of_explicit_basis(orth, which):
         Rr = R[l][i].T
         assert np.abs(Rr - Rt).max() <= 1e-10 * max(1.0, np.abs(Rt).max()), (l, i)
         assert np.allclose(np.tril(Rr, -1), 0.0) and (np.diag(Rr) >= 0).all()
+
+
+def _rows(h, l, i):
+    sh = h.q - l
+    return h.leaf_ptr[i << sh], h.leaf_ptr[(i + 1) << sh]
+
+
+def test_reweigh_R_is_cholesky_of_block_row_gram(orth):
+    """Reweighing downsweep: R^l_i^T R^l_i == B^l_iT B^l_i, with B^l_iT = U^lT_i
+    A^l_i built by brute force -- A^l_i = the rows of cluster i of every low-rank block at levels
+    <= l (the coarser blocks restricted to i's rows and the level-l blocks of row i) -- and, where
+    that Gram matrix is well conditioned, R^l_i == its Cholesky factor (unique, positive diagonal)."""
+    from oracle.orth import reweigh_R
+    _, g, _, _ = orth
+    R = reweigh_R(g)
+    UB, VB = explicit_bases(g, "U"), explicit_bases(g, "V")
+    A = np.zeros((g.N, g.N))
+    for l in range(g.q + 1):
+        rp, col = g.S_rowptr[l], g.S_col[l]
+        for t in range(len(rp) - 1):
+            r0, r1 = _rows(g, l, t)
+            for b in range(rp[t], rp[t + 1]):
+                s = col[b]
+                c0, c1 = _rows(g, l, s)
+                A[r0:r1, c0:c1] += UB[(l, t)] @ g.S[l][b].T @ VB[(l, s)].T
+        for i in range(1 << l):
+            r0, r1 = _rows(g, l, i)
+            Bt = UB[(l, i)].T @ A[r0:r1]                 # k x N
+            G = Bt @ Bt.T
+            Ri = R[l][i].T
+            scale = max(np.abs(G).max(), 1e-300)
+            assert np.abs(Ri.T @ Ri - G).max() <= 1e-10 * scale, (l, i)
+            assert np.allclose(np.tril(Ri, -1), 0.0) and (np.diag(Ri) >= 0).all()
+            w = np.linalg.eigvalsh(G)
+            if w.min() > 1e-8 * w.max():
+                Lc = np.linalg.cholesky(G)
+                assert np.abs(Ri - Lc.T).max() <= 1e-8 * max(1.0, np.abs(Lc).max()), (l, i)
