@@ -237,6 +237,14 @@ int h2_pcg(h2_handle K, double scale, const double *diag, const int64_t *C_rowpt
 enum { H2_EXPORT_S = 0, H2_EXPORT_U = 1, H2_EXPORT_VT = 2, H2_EXPORT_E = 3, H2_EXPORT_FT = 4 };
 int h2_orthogonalize(h2_handle h);
 int h2_export(h2_handle h, int what, int level, void *host, int64_t count);
+/* h2_reweigh: the reweighing downsweep of the recompression, root to leaves:
+ *   for every node i of level l the R factor of the stacked [R^{l-1}_{i+} E^{lT}_i ; S^{lT}_{ij} ...]
+ *   (Eq. Btq; the parent part absent at the root), so that R^{lT}_i R^l_i is the Gram matrix of the
+ *   block row's low-rank part and U^l_i R^{lT}_i is the reweighed basis.  Requires an orthogonal V
+ *   basis (call h2_orthogonalize first).  R_out: device memory, count = sum_l 2^l (k^l)^2 doubles,
+ *   levels concatenated from the root, each node's R column-major (upper triangular, diag >= 0).
+ *   FP64, one GPU, full storage, k^l <= 64; synchronous; the operator is not modified. */
+int h2_reweigh(h2_handle h, void *R_out, int64_t count);
 
 /* Release device memory, the NCCL communicator and streams.  NULL is a no-op. */
 int h2_destroy(h2_handle h);

@@ -19,7 +19,7 @@ EXPORTS = ["h2_create", "h2_matvec", "h2_matvec_ld", "h2_matvec_host", "h2_set_s
            "h2_group_create", "h2_group_matvec", "h2_file_info", "h2_create_from_file", "h2_group_create_from_file", "h2_n_local", "h2_fd_diag", "h2_pcg",
            "h2_set_profiling", "h2_phase_times", "h2_phase_stats",
            "h2_plan_counts", "h2_plan_census", "h2_destroy", "h2_nccl_unique_id", "h2_last_error", "h2_version",
-           "h2_orthogonalize", "h2_export"]
+           "h2_orthogonalize", "h2_export", "h2_reweigh"]
 H2_EXPORT_S, H2_EXPORT_U, H2_EXPORT_VT, H2_EXPORT_E, H2_EXPORT_FT = 0, 1, 2, 3, 4
 PHASES = ["up_leaf", "up_transfer", "exchange_top", "coupling_diag", "coupling_offdiag",
           "down_transfer", "leaf_u", "dense", "coupling_leaf"]
@@ -78,6 +78,7 @@ def load_library(path=None):
         "h2_destroy": ([vp], i32),
         "h2_orthogonalize": ([vp], i32),
         "h2_export": ([vp, i32, i32, vp, i64], i32),
+        "h2_reweigh": ([vp, vp, i64], i32),
         "h2_group_create_from_file": ([C.c_char_p, i32, i32, C.POINTER(vp)], i32),
         "h2_n_local": ([vp, C.POINTER(C.c_int64)], i32),
         "h2_file_info": ([C.c_char_p, C.POINTER(C.c_int64)], i32),
@@ -352,6 +353,14 @@ class H2Operator:
     def orthogonalize(self):
         """Basis orthogonalization in place (h2_orthogonalize; FP64, one GPU, full storage)."""
         _check(self._lib.h2_orthogonalize(self.handle))
+
+    def reweigh(self, R_out):
+        """Reweighing downsweep (h2_reweigh) into the device tensor R_out (sum_l 2^l k_l^2 doubles)."""
+        import torch
+        if not (isinstance(R_out, torch.Tensor) and R_out.is_cuda and R_out.dtype == torch.float64
+                and R_out.is_contiguous()):
+            raise ValueError("R_out must be a contiguous CUDA float64 tensor")
+        _check(self._lib.h2_reweigh(self.handle, C.c_void_p(R_out.data_ptr()), int(R_out.numel())))
 
     def export(self, what, level, count):
         """Host copy (1-D, count elements) of one operator array (h2_export; H2_EXPORT_*)."""

@@ -2226,6 +2226,42 @@ extern "C" int h2_orthogonalize(h2_handle h)
     return H2_OK;
 }
 
+extern "C" int h2_reweigh(h2_handle h, void *R_out, int64_t count)
+{
+    if (!h || !R_out) return fail(H2_ERR_ARG, "NULL argument");
+    if (h->sticky) return fail(H2_ERR_STATE, "handle unusable after an earlier CUDA/NCCL error");
+    if (h->L.P != 1 || h->dtype != H2_F64 || h->sym || h->group || (int)h->orth_pairs.size() != h->L.q + 1)
+        return fail(H2_ERR_ARG, "h2_reweigh: FP64, one GPU, full (non-symmetric) storage only");
+    const int q = h->L.q;
+    int64_t need = 0;
+    for (int l = 0; l <= q; ++l) need += ((int64_t)1 << l) * h->L.k[l] * h->L.k[l];
+    if (count != need) return fail(H2_ERR_ARG, "h2_reweigh: count must be sum_l 2^l k_l^2 = " + std::to_string(need));
+    std::vector<const int64_t *> rowptr(q + 1, nullptr);
+    std::vector<int64_t *> owned;
+    std::vector<int> maxb(q + 1, 0);
+    std::vector<double *> E(q + 1, nullptr), S(q + 1, nullptr);
+    cudaError_t err = cudaStreamSynchronize(h->stream);
+    for (int l = 0; l <= q && err == cudaSuccess; ++l) {
+        const int n = 1 << l;
+        std::vector<int64_t> rp(n + 1, 0);
+        for (const int2 &ts : h->orth_pairs[l]) rp[ts.x + 1]++;
+        for (int i = 0; i < n; ++i) { maxb[l] = std::max(maxb[l], (int)rp[i + 1]); rp[i + 1] += rp[i]; }
+        int64_t *d = nullptr;
+        err = cudaMalloc(&d, sizeof(int64_t) * (n + 1));
+        if (err != cudaSuccess) break;
+        owned.push_back(d);
+        rowptr[l] = d;
+        err = cudaMemcpy(d, rp.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice);
+        E[l] = (double *)h->E[l];
+        S[l] = (double *)h->S[l];
+    }
+    if (err == cudaSuccess) err = reweigh_downsweep(E, S, rowptr, maxb, h->L.k.data(), q, (double *)R_out, h->stream);
+    for (int64_t *d : owned) cudaFree(d);
+    if (err == cudaErrorInvalidValue) return fail(H2_ERR_ARG, "h2_reweigh: needs k <= 64");
+    if (err != cudaSuccess) return cuda_fail(h, err, "h2_reweigh");
+    return H2_OK;
+}
+
 extern "C" int h2_export(h2_handle h, int what, int level, void *host, int64_t count)
 {
     if (!h || !host) return fail(H2_ERR_ARG, "NULL argument");

@@ -185,4 +185,9 @@ cudaError_t launch_set_xmap(void *dmap, const float *X, int64_t ldx, int nv, cud
 cudaError_t orthogonalize_bases(double *U, double *Vt, const std::vector<double *> &E, const std::vector<double *> &Ft,
                                 const std::vector<double *> &S, const std::vector<const int2 *> &pairs,
                                 const std::vector<int64_t> &nblk, const int *k, int q, int m, cudaStream_t s);
+// Reweighing downsweep (h2_k_orth.cu, NEXT-3 step 2): R^l_i of every node, root to leaves, into
+// Rout (levels concatenated, 2^l x k^l x k^l column-major each); V must be orthogonal.
+cudaError_t reweigh_downsweep(const std::vector<double *> &E, const std::vector<double *> &S,
+                              const std::vector<const int64_t *> &rowptr, const std::vector<int> &maxb, const int *k,
+                              int q, double *Rout, cudaStream_t s);
 }  // namespace h2

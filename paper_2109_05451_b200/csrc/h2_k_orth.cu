@@ -27,24 +27,14 @@ __device__ __forceinline__ double warp_sum(double v)
     return v;
 }
 
-// Thin QR of a batch of R x C matrices (R >= C, R <= 128, C <= 64), element (i, j) of matrix b at
-// A + b * bs + i * rs + j * cs.  Overwrites A with the explicit Q (R x C) and writes R (C x C,
-// column-major) to Rout + b * C * C; diag(R) >= 0 (column signs of Q flipped to match).
-__global__ void __launch_bounds__(THREADS) k_qr(double *A, int64_t bs, int64_t rs, int64_t cs, int R, int C,
-                                               double *Rout)
+// Householder QR of the R x C column-major matrix a (ld R) in shared memory, in place: R in the
+// upper triangle, the reflectors v_j (v_j[j] = 1 implicit) below it, tau[j] their scalars
+// (LAPACK dgeqr2 / dlarfg conventions).  Whole CTA.
+__device__ void householder(double *a, int R, int C, double *tau, double *red)
 {
-    extern __shared__ double dyn[];
-    double *a = dyn, *q = dyn + R * C;     // column-major, ld R (2 R C doubles of dynamic smem)
-    __shared__ double tau[MAXC];
-    __shared__ double red[THREADS / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = THREADS / 32;
-    double *Ab = A + (int64_t)blockIdx.x * bs;
-    for (int e = tid; e < R * C; e += THREADS) {
-        const int i = e % R, j = e / R;
-        a[e] = Ab[i * rs + j * cs];
-    }
-    __syncthreads();
-    for (int j = 0; j < C; ++j) {
+    const int K = R < C ? R : C;
+    for (int j = 0; j < K; ++j) {
         // Householder vector of column j below the diagonal (LAPACK dlarfg convention)
         double s = 0.0;
         for (int i = j + 1 + tid; i < R; i += THREADS) s += a[i + j * R] * a[i + j * R];
@@ -75,6 +65,26 @@ __global__ void __launch_bounds__(THREADS) k_qr(double *A, int64_t bs, int64_t r
             }
         __syncthreads();
     }
+}
+
+// Thin QR of a batch of R x C matrices (R >= C, R <= 128, C <= 64), element (i, j) of matrix b at
+// A + b * bs + i * rs + j * cs.  Overwrites A with the explicit Q (R x C) and writes R (C x C,
+// column-major) to Rout + b * C * C; diag(R) >= 0 (column signs of Q flipped to match).
+__global__ void __launch_bounds__(THREADS) k_qr(double *A, int64_t bs, int64_t rs, int64_t cs, int R, int C,
+                                               double *Rout)
+{
+    extern __shared__ double dyn[];
+    double *a = dyn, *q = dyn + R * C;     // column-major, ld R (2 R C doubles of dynamic smem)
+    __shared__ double tau[MAXC];
+    __shared__ double red[THREADS / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = THREADS / 32;
+    double *Ab = A + (int64_t)blockIdx.x * bs;
+    for (int e = tid; e < R * C; e += THREADS) {
+        const int i = e % R, j = e / R;
+        a[e] = Ab[i * rs + j * cs];
+    }
+    __syncthreads();
+    householder(a, R, C, tau, red);
     // explicit Q = H_0 H_1 ... H_{C-1} [I; 0], reflectors applied last to first
     for (int e = tid; e < R * C; e += THREADS) {
         const int i = e % R, j = e / R;
@@ -164,6 +174,57 @@ __global__ void __launch_bounds__(THREADS) k_project(double *S, const int2 *pair
     }
 }
 
+// Reweighing downsweep step: R^l_i (kl x kl, column-major at Rl + i kl^2) <- the R
+// factor of a stack, for every node i of a level (one CTA each):
+//   fold < 0 (start):  stack = R^{l-1}_{i+} E_i^T (kp x kl; zero at the root: R <- 0);
+//   fold = f >= 0:     stack = [R^l_i ; S_{i b}^T] with b = rowptr[i] + f (rows without an f-th
+//                      block keep their R).
+// R is written sign-normalised (diag >= 0) and zero-padded to kl x kl.
+__global__ void __launch_bounds__(THREADS) k_rfold(double *Rl, const double *Rp, const double *E, const double *S,
+                                                  const int64_t *rowptr, int kl, int kp, int fold)
+{
+    extern __shared__ double dyn[];
+    __shared__ double tau[MAXC];
+    __shared__ double red[THREADS / 32];
+    const int i = blockIdx.x, tid = threadIdx.x;
+    double *Ri = Rl + (int64_t)i * kl * kl;
+    int rows;
+    double *a = dyn;
+    if (fold < 0) {
+        if (!Rp) {
+            for (int e = tid; e < kl * kl; e += THREADS) Ri[e] = 0.0;
+            return;
+        }
+        rows = kp;
+        const double *Rpi = Rp + (int64_t)(i >> 1) * kp * kp;            // R_{i+}: kp x kp upper
+        const double *Ei = E + (int64_t)i * kl * kp;                      // E_i: kl x kp column-major
+        for (int e = tid; e < kp * kl; e += THREADS) {
+            const int r = e % kp, c = e / kp;                             // (R_{i+} E_i^T)(r, c)
+            double v = 0.0;
+            for (int t = r; t < kp; ++t) v += Rpi[r + t * kp] * Ei[c + t * kl];
+            a[r + c * rows] = v;
+        }
+    } else {
+        const int64_t b = rowptr[i] + fold;
+        if (b >= rowptr[i + 1]) return;
+        rows = 2 * kl;
+        const double *Sb = S + b * kl * kl;                               // stored S (column-major)
+        for (int e = tid; e < kl * kl; e += THREADS) {
+            const int r = e % kl, c = e / kl;
+            a[r + c * rows] = Ri[e];                                      // current R (padded rows 0)
+            a[kl + r + c * rows] = Sb[c + r * kl];                        // S^T(r, c) = S(c, r)
+        }
+    }
+    __syncthreads();
+    householder(a, rows, kl, tau, red);
+    for (int e = tid; e < kl * kl; e += THREADS) {
+        const int r = e % kl, c = e / kl;
+        double v = 0.0;
+        if (r < rows && r <= c) v = (a[r + r * rows] < 0.0 ? -1.0 : 1.0) * a[r + c * rows];
+        Ri[e] = v;
+    }
+}
+
 }  // namespace orth
 
 // QR upsweep of one basis tree in place.  leaf: nleaf matrices m x kq, element (i, j) at
@@ -183,6 +244,31 @@ static cudaError_t orth_tree(double *leaf, int64_t lrs, int64_t lcs, int m, cons
         k_split<<<np, THREADS, 0, s>>>(W, kl, kp, T[l], trs[l], tcs[l]);
     }
     return cudaGetLastError();
+}
+
+cudaError_t reweigh_downsweep(const std::vector<double *> &E, const std::vector<double *> &S,
+                              const std::vector<const int64_t *> &rowptr, const std::vector<int> &maxb, const int *k,
+                              int q, double *Rout, cudaStream_t s)
+{
+    using namespace orth;
+    for (int l = 0; l <= q; ++l)
+        if (k[l] > MAXC || (l >= 1 && k[l - 1] > 2 * MAXC)) return cudaErrorInvalidValue;
+    cudaError_t err = cudaFuncSetAttribute(k_rfold, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(2 * MAXC * MAXC * sizeof(double)));
+    if (err != cudaSuccess) return err;
+    double *Rl = Rout, *Rp = nullptr;
+    for (int l = 0; l <= q && err == cudaSuccess; ++l) {
+        const int kl = k[l], kp = l ? k[l - 1] : 0, n = 1 << l;
+        const size_t sm = (size_t)std::max(2 * kl, kp) * kl * sizeof(double);
+        k_rfold<<<n, THREADS, sm, s>>>(Rl, Rp, l ? E[l] : nullptr, S[l], rowptr[l], kl, kp, -1);
+        for (int f = 0; f < maxb[l]; ++f)
+            k_rfold<<<n, THREADS, sm, s>>>(Rl, Rp, l ? E[l] : nullptr, S[l], rowptr[l], kl, kp, f);
+        err = cudaGetLastError();
+        Rp = Rl;
+        Rl += (size_t)n * kl * kl;
+    }
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    return err == cudaSuccess ? e2 : err;
 }
 
 cudaError_t orthogonalize_bases(double *U, double *Vt, const std::vector<double *> &E, const std::vector<double *> &Ft,

@@ -63,3 +63,36 @@ def test_orthogonalize_rejects_unsupported():
     with pytest.raises(H2Error):
         op.orthogonalize()
     op.close()
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_reweigh_parity(name):
+    """h2_reweigh after h2_orthogonalize vs the oracle's reweighing downsweep (pinned against the
+    brute-force block-row Gram matrices in test_orth_oracle.py): every R^l_i element by element
+    (rows whose stack is rank deficient compared through R^T R, the unique part)."""
+    import torch
+    from paper_2109_05451_b200 import operator_from_h2data
+    from oracle.orth import reweigh_R
+    h = CASES[name]()
+    g, _, _ = orthogonalize(h)
+    Rref = reweigh_R(g)
+    op = operator_from_h2data(h, nv_max=1)
+    op.orthogonalize()
+    n = sum((1 << l) * h.ranks[l] ** 2 for l in range(h.q + 1))
+    Rd = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+    op.reweigh(Rd)
+    R = Rd.cpu().numpy()
+    off = 0
+    for l in range(h.q + 1):
+        k = h.ranks[l]
+        got = R[off:off + (1 << l) * k * k].reshape(1 << l, k, k)
+        off += (1 << l) * k * k
+        for i in range(1 << l):
+            a, b = got[i].T, Rref[l][i].T
+            scale = max(np.abs(b).max(), 1e-300)
+            G = b.T @ b
+            assert np.abs(a.T @ a - G).max() <= 1e-10 * max(np.abs(G).max(), 1e-300), (l, i)
+            w = np.linalg.eigvalsh(G) if scale > 1e-300 else np.zeros(1)
+            if w.min() > 1e-8 * max(w.max(), 1e-300):
+                assert np.abs(a - b).max() <= 1e-9 * scale, (l, i)
+    op.close()
