@@ -1,4 +1,4 @@
-"""Time h2_orthogonalize (NEXT-3 step 1) on full-size workloads (dev / evidence tool).
+"""Time h2_orthogonalize and h2_reweigh (NEXT-3 steps 1-2) on full-size workloads (dev / evidence tool).
 
     python tools/bench_orth.py cfg2 cfg5        # FP64; prints one JSON line per workload
 """
@@ -21,14 +21,22 @@ for name in sys.argv[1:] or ["cfg2"]:
         fl += 2 * np_ * (qr(2 * k[l], k[l - 1]) + 2 * 2.0 * k[l] * k[l] * k[l - 1])
     fl += sum(4.0 * s.shape[0] * k[l] ** 3 for l, s in enumerate(h.S))
     bytes_ = 8 * 2 * (h.U_leaf.size + h.V_leaf.size + sum(e.size for e in h.E[1:]) * 2 + sum(s.size for s in h.S))
-    res = []
+    res, rw = [], []
+    nR = sum((1 << l) * k[l] ** 2 for l in range(q + 1))
     for rep in range(3):
         op = operator_from_h2data(h, nv_max=1)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         op.orthogonalize()
         res.append(time.perf_counter() - t0)
+        Rd = torch.empty(nR, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        op.reweigh(Rd)
+        rw.append(time.perf_counter() - t0)
+        del Rd
         op.close()
     t = min(res)
     print(json.dumps({"workload": name, "ms": t * 1e3, "ms_all": [r * 1e3 for r in res], "gflops": fl / t / 1e9,
-                      "gb_moved_min": bytes_ / 1e9, "gbs": bytes_ / t / 1e9, "leaves": 1 << q, "m": m, "k": k[q]}))
+                      "gb_moved_min": bytes_ / 1e9, "gbs": bytes_ / t / 1e9,
+                      "reweigh_ms": min(rw) * 1e3, "reweigh_ms_all": [r * 1e3 for r in rw], "leaves": 1 << q, "m": m, "k": k[q]}))
