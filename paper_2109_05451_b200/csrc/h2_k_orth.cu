@@ -289,11 +289,13 @@ cudaError_t orthogonalize_bases(double *U, double *Vt, const std::vector<double 
     if (err != cudaSuccess) return err;
     size_t wmax = 1;
     for (int l = 1; l <= q; ++l) wmax = std::max(wmax, (size_t)(1 << (l - 1)) * 2 * k[l] * k[l - 1]);
+    // stream-ordered pool allocations: the R workspaces (GBs at 2^15 leaves, k = 64) are reused
+    // across calls instead of mapped and unmapped each time
     for (int l = 0; l <= q && err == cudaSuccess; ++l) {
-        err = cudaMalloc(&RU[l], sizeof(double) * ((size_t)1 << l) * k[l] * k[l]);
-        if (err == cudaSuccess) err = cudaMalloc(&RV[l], sizeof(double) * ((size_t)1 << l) * k[l] * k[l]);
+        err = cudaMallocAsync(&RU[l], sizeof(double) * ((size_t)1 << l) * k[l] * k[l], s);
+        if (err == cudaSuccess) err = cudaMallocAsync(&RV[l], sizeof(double) * ((size_t)1 << l) * k[l] * k[l], s);
     }
-    if (err == cudaSuccess) err = cudaMalloc(&W, sizeof(double) * wmax);
+    if (err == cudaSuccess) err = cudaMallocAsync(&W, sizeof(double) * wmax, s);
     if (err == cudaSuccess) {
         // U tree: U (m x kq column-major), E[l] (kl x kp column-major)
         std::vector<int64_t> ers(q + 1, 1), ecs(q + 1), frs(q + 1), fcs(q + 1, 1);
@@ -308,10 +310,13 @@ cudaError_t orthogonalize_bases(double *U, double *Vt, const std::vector<double 
                 err = cudaGetLastError();
             }
     }
+    for (int l = 0; l <= q; ++l) {
+        if (RU[l]) cudaFreeAsync(RU[l], s);
+        if (RV[l]) cudaFreeAsync(RV[l], s);
+    }
+    if (W) cudaFreeAsync(W, s);
     cudaError_t e2 = cudaStreamSynchronize(s);
     if (err == cudaSuccess) err = e2;
-    for (int l = 0; l <= q; ++l) { cudaFree(RU[l]); cudaFree(RV[l]); }
-    cudaFree(W);
     return err;
 }
 
