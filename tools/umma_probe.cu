@@ -83,6 +83,62 @@ __global__ void probe(const float *A, const float *B, float *out, int mode, int 
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(tm));
 }
 
+__global__ void probe_sw128(const float *A, const float *B, float *out, int M, int variant)
+{
+    __shared__ __align__(1024) float As[128 * 8];
+    __shared__ __align__(1024) float Bs[16 * 8];
+    __shared__ uint32_t tbase;
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < M * 8; i += blockDim.x) {
+        const int m = i / 8, k = i % 8;
+        const int g = m / 32, mm = m % 32;                      // MN group, element within the 128 B row
+        const int chunk = mm / 4, w = mm % 4;
+        const int byte = g * 1024 + k * 128 + (((chunk ^ (k & 7)) * 16)) + w * 4;
+        As[byte / 4] = A[m * 8 + k];
+    }
+    for (int i = tid; i < 16 * 8; i += blockDim.x) {
+        const int n = i / 8, k = i % 8;
+        Bs[(n / 8) * 64 + (k / 4) * 32 + (n % 8) * 4 + (k % 4)] = B[n * 8 + k];
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(su32(&tbase)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tm = tbase;
+    if (tid == 0) {
+        uint64_t da = variant == 0 ? sdesc(su32(As), 1024, 8192) : sdesc(su32(As), 8192, 1024);
+        da |= (uint64_t)2 << 61;                                  // SWIZZLE_128B
+        const uint64_t db = sdesc(su32(Bs), 128, 256);
+        const uint32_t id = idesc_tf32(M, 16, 1, 0);
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+                     ::"r"(tm), "l"(da), "l"(db), "r"(id), "r"(0));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(&bar)));
+    }
+    asm volatile("{\n.reg .pred P;\nW2: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n@!P bra W2;\n}\n" ::"r"(su32(&bar)));
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    uint32_t v[16];
+    const uint32_t ta = tm + ((uint32_t)(warp * 32) << 16);
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                 : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+    for (int c = 0; c < 16; ++c) out[tid * 16 + c] = __uint_as_float(v[c]);
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(tm));
+}
+
 int main()
 {
     float hA[128 * 8], hB[16 * 8], hO[128 * 16];
@@ -140,6 +196,30 @@ int main()
                 printf(" (%d,%d)", v % 128, v / 128);
             }
             printf("\n");
+        }
+    }
+    // MN-major A with 128-byte swizzle: M = 128 (4 groups of 32), K = 8: atom (mgroup) = 8 K rows x
+    // 128 B, 16-byte chunk c of row r stored at chunk c ^ (r & 7); LBO = MN-group stride (1 KB),
+    // SBO = K-group stride (unused for K = 8)
+    {
+        const int M = 128;
+        for (int m = 0; m < 128; ++m) for (int k = 0; k < 8; ++k) hA[m * 8 + k] = (float)(m + 128 * k);
+        for (int n = 0; n < 16; ++n) for (int k = 0; k < 8; ++k) hB[n * 8 + k] = (n == k) ? 1.f : 0.f;
+        cudaMemcpy(dA, hA, sizeof hA, cudaMemcpyHostToDevice);
+        cudaMemcpy(dB, hB, sizeof hB, cudaMemcpyHostToDevice);
+        for (int variant = 0; variant < 2; ++variant) {
+            probe_sw128<<<1, 128>>>(dA, dB, dO, M, variant);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { printf("sw128 variant %d: %s\n", variant, cudaGetErrorString(e)); return 1; }
+            cudaMemcpy(hO, dO, sizeof hO, cudaMemcpyDeviceToHost);
+            int good = 0;
+            for (int l = 0; l < 128; ++l) {
+                bool ok = true;
+                for (int n = 0; n < 8 && ok; ++n) ok = hO[l * 16 + n] == hA[l * 8 + n];
+                good += ok;
+            }
+            printf("MN-major SW128 variant %d (lbo/sbo %s): %d of 128 rows correct; lane 0: (%g %g %g) lane 33: (%g %g)\n",
+                   variant, variant ? "swapped" : "LBO=MN", good, hO[0], hO[1], hO[2], hO[33 * 16], hO[33 * 16 + 1]);
         }
     }
     // rounding probe: A = 1 + 3*2^-12 (between two TF32 values, nearer the upper), B = 1
