@@ -12,6 +12,10 @@
 #include "h2_internal.h"
 
 namespace h2 {
+// CTAs per SM the sym kernels' registers are sized for (memory-latency-bound: more warps in flight)
+#ifndef SYM_MINB
+#define SYM_MINB 3
+#endif
 namespace sym {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -83,7 +87,7 @@ __device__ __forceinline__ void apply(T (&acc)[RPL], const Blk &b, int r, int c,
 // x^ and y^ share the plane layout, so Blk::x addresses both x^_s and y^_s and Task::out both y^_t
 // and x^_t.  y^ was zeroed before the launch.
 template <typename T, int RPL>
-__global__ void __launch_bounds__(256, 2) k_sym_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
+__global__ void __launch_bounds__(256, SYM_MINB) k_sym_rows(const Task *__restrict__ tasks, int ntask, const Blk *__restrict__ blks,
                                                   const T *__restrict__ xh, T *yh)
 {
     const int lane = threadIdx.x & 31;
@@ -102,7 +106,7 @@ __global__ void __launch_bounds__(256, 2) k_sym_rows(const Task *__restrict__ ta
 // Leaves: z = y^_t + E_t y^_parent ; Y_t += alpha (U_t z + sum_{s >= t} D_ts x_s) ;
 // Y_s += alpha D_ts^T x_t (s > t).  Y was scaled by beta before the launch.
 template <typename T, int RPL>
-__global__ void __launch_bounds__(256, 2) k_sym_leaf(const Task *__restrict__ ltasks, const Task *__restrict__ dtasks,
+__global__ void __launch_bounds__(256, SYM_MINB) k_sym_leaf(const Task *__restrict__ ltasks, const Task *__restrict__ dtasks,
                                                   int ntask, const Blk *__restrict__ blks, const T *__restrict__ yh,
                                                   const CallArgs<T> *__restrict__ args)
 {
