@@ -14,7 +14,7 @@
 namespace h2 {
 // CTAs per SM the sym kernels' registers are sized for (memory-latency-bound: more warps in flight)
 #ifndef SYM_MINB
-#define SYM_MINB 3
+#define SYM_MINB 4
 #endif
 namespace sym {
 
