@@ -95,8 +95,13 @@ __global__ void __launch_bounds__(256, SYM_MINB) k_sym_rows(const Task *__restri
         const Task tk = tasks[w];
         T acc[RPL] = {};
         const T *xt = xh + tk.out;
-        for (int bi = 0; bi < tk.nblk; ++bi)
-            sym::apply<T, RPL>(acc, blks[tk.blk0 + bi], tk.r, tk.c, xh, xt, tk.r, yh, T(1), lane);
+        // the next block's descriptor is loaded while this block streams (latency-bound kernel)
+        Blk nb = tk.nblk > 0 ? blks[tk.blk0] : Blk{};
+        for (int bi = 0; bi < tk.nblk; ++bi) {
+            const Blk b = nb;
+            if (bi + 1 < tk.nblk) nb = blks[tk.blk0 + bi + 1];
+            sym::apply<T, RPL>(acc, b, tk.r, tk.c, xh, xt, tk.r, yh, T(1), lane);
+        }
 #pragma unroll
         for (int ri = 0; ri < RPL; ++ri)
             if (lane + 32 * ri < tk.r) atomicAdd(yh + tk.out + lane + 32 * ri, acc[ri]);
@@ -142,8 +147,12 @@ __global__ void __launch_bounds__(256, SYM_MINB) k_sym_leaf(const Task *__restri
         sym::block<T, RPL, false>(acc, static_cast<const T *>(bU.A), tk.r, k, z[0], z[1], T(0), T(0), nullptr,
                                   alpha, lane);
         const T *xt = X + tk.out;
-        for (int bi = 0; bi < dk.nblk; ++bi)
-            sym::apply<T, RPL>(acc, blks[dk.blk0 + bi], dk.r, dk.c, X, xt, tk.rows, Y, alpha, lane);
+        Blk nb = dk.nblk > 0 ? blks[dk.blk0] : Blk{};
+        for (int bi = 0; bi < dk.nblk; ++bi) {
+            const Blk b = nb;
+            if (bi + 1 < dk.nblk) nb = blks[dk.blk0 + bi + 1];
+            sym::apply<T, RPL>(acc, b, dk.r, dk.c, X, xt, tk.rows, Y, alpha, lane);
+        }
 #pragma unroll
         for (int ri = 0; ri < RPL; ++ri)
             if (lane + 32 * ri < tk.rows) atomicAdd(Y + tk.out + lane + 32 * ri, alpha * acc[ri]);
