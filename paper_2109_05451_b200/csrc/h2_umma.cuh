@@ -2,8 +2,8 @@
 //
 //   y (r x nv) (+)= sum_b A_b (r x c) x_b (c x nv)      (coupling PAPER.md:328-331, transfers 263-270)
 //
-// in split TF32: every operand v is split v = hi + lo with hi = rn_tf32(v), lo = rn_tf32(v - hi)
-// (hi + lo reproduces v to ~2^-22), and ONE tcgen05.mma.kind::tf32 per 8 columns computes all four
+// in split TF32: every operand v is split v = hi + lo with hi = v truncated to TF32 and
+// lo = rn_tf32(v - hi) (hi + lo reproduces v to < 2^-21), and ONE tcgen05.mma.kind::tf32 per 8 columns computes all four
 // products: the operand tiles are stacked, A' = [A_hi; A_lo] (M = 128) and x' = [x_hi, x_lo]
 // (N = 2 nv), so D' = A' x' holds A_hi x_hi, A_hi x_lo, A_lo x_hi, A_lo x_lo in its four quadrants and
 // y = their sum carries FP32 accuracy (north_star: FP32 runs <= 1e-5 against the FP64 oracle).
@@ -208,12 +208,16 @@ __device__ __forceinline__ void tmem_ld8(uint32_t ta, float *v)
 // the magnitude, clear the 13 dropped mantissa bits (2 integer ops; cvt.rna.tf32.f32 lowers to a
 // branchy NaN-aware sequence).  Finite inputs only -- the operands of a matvec.
 __device__ __forceinline__ float tf32_rn(float v) { return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xffffe000u); }
+// hi = v truncated to TF32 (what the tensor core reads from v itself: measured truncation), lo =
+// the exact remainder rounded to TF32: |v - hi - lo| <= 2^-11 |lo| < 2^-21 |v| (one integer op
+// less per element than a round-to-nearest hi)
+__device__ __forceinline__ float tf32_tr(float v) { return __uint_as_float(__float_as_uint(v) & 0xffffe000u); }
 __device__ __forceinline__ void split4(const float4 &v, float4 &h, float4 &l)
 {
-    h.x = tf32_rn(v.x); l.x = tf32_rn(v.x - h.x);
-    h.y = tf32_rn(v.y); l.y = tf32_rn(v.y - h.y);
-    h.z = tf32_rn(v.z); l.z = tf32_rn(v.z - h.z);
-    h.w = tf32_rn(v.w); l.w = tf32_rn(v.w - h.w);
+    h.x = tf32_tr(v.x); l.x = tf32_rn(v.x - h.x);
+    h.y = tf32_tr(v.y); l.y = tf32_rn(v.y - h.y);
+    h.z = tf32_tr(v.z); l.z = tf32_rn(v.z - h.z);
+    h.w = tf32_tr(v.w); l.w = tf32_rn(v.w - h.w);
 }
 
 
