@@ -139,6 +139,61 @@ __global__ void probe_sw128(const float *A, const float *B, float *out, int M, i
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(tm));
 }
 
+__global__ void probe_ksw128(const float *A, const float *B, float *out, int M, int ks)
+{
+    __shared__ __align__(1024) float As[128 * 32];
+    __shared__ __align__(1024) float Bs[16 * 8];
+    __shared__ uint32_t tbase;
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    // rows of 128 B (32 K values); 16-byte chunk c of row r stored at chunk c ^ (r & 7)
+    for (int i = tid; i < M * 32; i += blockDim.x) {
+        const int m = i / 32, k = i % 32;
+        const int chunk = k / 4, w = k % 4;
+        As[m * 32 + ((chunk ^ (m & 7)) * 4) + w] = A[m * 32 + k];
+    }
+    for (int i = tid; i < 16 * 8; i += blockDim.x) {
+        const int n = i / 8, k = i % 8;
+        Bs[(n / 8) * 64 + (k / 4) * 32 + (n % 8) * 4 + (k % 4)] = B[n * 8 + k];
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(su32(&tbase)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tm = tbase;
+    if (tid == 0) {
+        uint64_t da = sdesc(su32(As) + ks * 32, 16, 1024);       // SBO = 8 rows x 128 B
+        da |= (uint64_t)2 << 61;                                  // SWIZZLE_128B
+        const uint64_t db = sdesc(su32(Bs), 128, 256);
+        const uint32_t id = idesc_tf32(M, 16, 0, 0);
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+                     ::"r"(tm), "l"(da), "l"(db), "r"(id), "r"(0));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(&bar)));
+    }
+    asm volatile("{\n.reg .pred P;\nW3: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n@!P bra W3;\n}\n" ::"r"(su32(&bar)));
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    uint32_t v[16];
+    const uint32_t ta = tm + ((uint32_t)(warp * 32) << 16);
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                 : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+    for (int c = 0; c < 16; ++c) out[tid * 16 + c] = __uint_as_float(v[c]);
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(tm));
+}
+
 int main()
 {
     float hA[128 * 8], hB[16 * 8], hO[128 * 16];
@@ -220,6 +275,32 @@ int main()
             }
             printf("MN-major SW128 variant %d (lbo/sbo %s): %d of 128 rows correct; lane 0: (%g %g %g) lane 33: (%g %g)\n",
                    variant, variant ? "swapped" : "LBO=MN", good, hO[0], hO[1], hO[2], hO[33 * 16], hO[33 * 16 + 1]);
+        }
+    }
+    // K-major A with 128-byte swizzle (the GEMM layout): A = 128 (M) x 32 (K) per atom row; one MMA
+    // with K = 8 at K offset koff (start address + 32 B per 8-column step inside the 128 B row)
+    {
+        const int M = 128;
+        static float hA2[128 * 32];
+        for (int m = 0; m < 128; ++m) for (int k = 0; k < 32; ++k) hA2[m * 32 + k] = (float)(m + 128 * k);
+        float *dA2;
+        cudaMalloc(&dA2, sizeof hA2);
+        cudaMemcpy(dA2, hA2, sizeof hA2, cudaMemcpyHostToDevice);
+        for (int n = 0; n < 16; ++n) for (int k = 0; k < 8; ++k) hB[n * 8 + k] = (n == k) ? 1.f : 0.f;
+        cudaMemcpy(dB, hB, sizeof hB, cudaMemcpyHostToDevice);
+        for (int ks = 0; ks < 4; ++ks) {
+            probe_ksw128<<<1, 128>>>(dA2, dB, dO, M, ks);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { printf("ksw128: %s\n", cudaGetErrorString(e)); return 1; }
+            cudaMemcpy(hO, dO, sizeof hO, cudaMemcpyDeviceToHost);
+            int good = 0;
+            for (int l = 0; l < 128; ++l) {
+                bool ok = true;
+                for (int n = 0; n < 8 && ok; ++n) ok = hO[l * 16 + n] == hA2[l * 32 + ks * 8 + n];
+                good += ok;
+            }
+            printf("K-major SW128 k-step %d: %d of 128 rows correct (lane 1 col 0: %g want %g)\n", ks, good, hO[16],
+                   hA2[32 + ks * 8]);
         }
     }
     // rounding probe: A = 1 + 3*2^-12 (between two TF32 values, nearer the upper), B = 1
