@@ -10,17 +10,19 @@
 // (Three separate M = 64 MMAs per 8 columns -- 3xTF32 -- were issue-bound: ~94 cycles per MMA.)
 //
 // One CTA per SM, warp-specialised, one output node (x one chunk of N <= 64 vectors) at a time:
-//   warp 4      PRODUCER   bulk copies (cp.async.bulk, the TMA engine) of A_b -- r x c contiguous,
-//                          column-major -- and of each x_b vector into an NR-stage raw ring,
-//                          completing on raw_full[s] by transaction count;
-//   warps 6-9   CONVERTERS split every element into hi / lo and write both into an NC-stage
+//   warp 4      PRODUCER   per block ONE bulk copy (cp.async.bulk, the TMA engine) of A_b -- r x c
+//                          contiguous, column-major -- and ONE 4-D tensor copy of x_b (all N vectors,
+//                          landing in the K-major layout; per-vector bulk copies for received rows)
+//                          into an NR-stage raw ring, completing on raw_full[s] by transaction count;
+//                          task / block descriptors fetched ahead (32 per warp load)
+//   warps 6-13  CONVERTERS split every element into hi / lo and write both into an NC-stage
 //                          operand ring in the K-major canonical no-swizzle layout (A transposed:
 //                          each thread gathers 4 columns of one row), then fence.proxy.async so the
 //                          tensor cores see the generic-proxy stores, and free the raw stage;
-//   warp 5      MMA        one elected thread issues one tcgen05.mma (M=128, N=2 nv, K=8, both
-//                          operands from shared memory) per 8 columns, k-step k into partial
-//                          accumulator k % NACC of one of NB TMEM buffers (independent chains),
-//                          fresh per block, and commits to op_empty[s] and acc_full[b] (NB buffers);
+//   warp 5      MMA        the whole warp, one elected lane issuing all 8 tcgen05.mma (M=128,
+//                          N=2 nv, K=8, both operands from shared memory) of a block in one asm
+//                          statement, k-step k into partial accumulator k % NACC of one of NB TMEM
+//                          buffers, fresh per block; commits to op_empty[s] and acc_full[b];
 //   warps 0-3   EPILOGUE   tcgen05.ld the block's partial products (warp w reads TMEM lanes
 //                          32w..32w+31: warps 0-1 hold the A_hi rows, 2-3 the A_lo rows) and add
 //                          both column halves to a running sum in registers with IEEE FP32 adds --
@@ -29,10 +31,11 @@
 //                          per block it stays ~1e-6 -- then, per task, the A_lo half hands its sums
 //                          to the A_hi half through shared memory, which stores / accumulates y.
 // (MN-major A straight from the column-major copy would skip the transpose, but kind::tf32 with
-// an MN-major no-swizzle descriptor returned zeros on this B200 (tools/umma_probe.cu).)
-// A_b is read from HBM once per (task, vector chunk).  Tasks are walked in the same order by every
-// role (static round robin over persistent CTAs), so only the block's padded column count crosses
-// the ring.
+// an MN-major descriptor -- no swizzle or 128-byte swizzle -- returned zeros on this B200
+// (tools/umma_probe.cu).)
+// A_b is read from HBM once per (task, vector chunk).  The converters and the MMA warp consume a
+// descriptor-free block stream (an end marker closes it); the producer and the epilogue walk the
+// task list in the same order (static round robin over persistent CTAs).
 #pragma once
 #include <cuda.h>
 #include "h2_internal.h"
@@ -83,10 +86,6 @@ __host__ __device__ constexpr uint32_t idesc()
 }
 
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void cp16(float *dst, const float *src)
-{
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(dst)), "l"(src) : "memory");
-}
 __device__ __forceinline__ void cp4(float *dst, const float *src, bool valid)
 {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(su32(dst)), "l"(src), "r"(valid ? 4 : 0)
@@ -188,11 +187,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t ta, float *v)
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t ta, float *v)
-{
-    tmem_ld16(ta, v);
-    tmem_ld16(ta + 16u, v + 16);
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t ta, float *v)
 {
