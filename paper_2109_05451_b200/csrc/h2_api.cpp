@@ -322,6 +322,9 @@ struct h2_ctx {
     ncclComm_t comm = nullptr;
     // e2e staging
     void *dX = nullptr, *dY = nullptr;
+    // h2_matvec_host pipeline: copy streams (host-to-device, device-to-host) and per-chunk events
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_x[2] = {}, ev_y[2] = {};
     // per-call arguments (device CallArgs<T>) and the captured graphs, one per nv
     void *dargs = nullptr;
     cudaStream_t cap_stream = nullptr;
@@ -426,7 +429,10 @@ int release(h2_ctx *h)
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     if (h->s_comm) cudaStreamDestroy(h->s_comm);
     if (h->s_leafc) cudaStreamDestroy(h->s_leafc);
-    for (cudaEvent_t e : {h->ev_packed, h->ev_recv, h->ev_fork, h->ev_halo, h->ev_upleaf, h->ev_leafc})
+    if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
+    if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
+    for (cudaEvent_t e : {h->ev_packed, h->ev_recv, h->ev_fork, h->ev_halo, h->ev_upleaf, h->ev_leafc, h->ev_x[0],
+                          h->ev_x[1], h->ev_y[0], h->ev_y[1]})
         if (e) cudaEventDestroy(e);
     delete h;
     return H2_OK;
@@ -1964,11 +1970,55 @@ extern "C" int h2_matvec_host(h2_handle h, double alpha, const void *X, double b
         h->dY = dalloc(h, (size_t)h->n_local * h->nv_max * h->esz, err);
         if (!h->dX || !h->dY) return cuda_fail(h, err, "cudaMalloc(e2e staging)");
     }
-    H2_CUDA(h, cudaMemcpyAsync(h->dX, X, bytes, cudaMemcpyHostToDevice, h->stream));
-    if (beta != 0.0) H2_CUDA(h, cudaMemcpyAsync(h->dY, Y, bytes, cudaMemcpyHostToDevice, h->stream));
-    rc = h2_matvec_ld(h, alpha, h->dX, h->n_local, beta, h->dY, h->n_local, nv);
-    if (rc != H2_OK) return rc;
-    H2_CUDA(h, cudaMemcpyAsync(Y, h->dY, bytes, cudaMemcpyDeviceToHost, h->stream));
+    // Large calls (>= 16 vectors and >= 32 MB each way) run in two vector chunks so the
+    // host-to-device copy of chunk 1 overlaps the matvec of chunk 0 and the device-to-host copy of
+    // chunk 0 overlaps the matvec of chunk 1 (copy engines on their own streams, event-ordered);
+    // chunk sizes multiples of 8 (the FP32 tensor-map path).  Smaller calls: copy, matvec, copy.
+    const char *emb = getenv("H2_E2E_MIN_MB");          // threshold override (tests)
+    const size_t min_bytes = (size_t)(emb ? atol(emb) : 32) << 20;
+    const int nc = (nv >= 16 && bytes >= min_bytes) ? 2 : 1;
+    if (nc == 1) {
+        H2_CUDA(h, cudaMemcpyAsync(h->dX, X, bytes, cudaMemcpyHostToDevice, h->stream));
+        if (beta != 0.0) H2_CUDA(h, cudaMemcpyAsync(h->dY, Y, bytes, cudaMemcpyHostToDevice, h->stream));
+        rc = h2_matvec_ld(h, alpha, h->dX, h->n_local, beta, h->dY, h->n_local, nv);
+        if (rc != H2_OK) return rc;
+        H2_CUDA(h, cudaMemcpyAsync(Y, h->dY, bytes, cudaMemcpyDeviceToHost, h->stream));
+        H2_CUDA(h, cudaStreamSynchronize(h->stream));
+        return H2_OK;
+    }
+    if (!h->s_h2d) {
+        H2_CUDA(h, cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+        H2_CUDA(h, cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            H2_CUDA(h, cudaEventCreateWithFlags(&h->ev_x[i], cudaEventDisableTiming));
+            H2_CUDA(h, cudaEventCreateWithFlags(&h->ev_y[i], cudaEventDisableTiming));
+        }
+    }
+    const int v0 = ((nv / 2 + 7) / 8) * 8;                 // first chunk: half, rounded up to 8
+    const int cv[2] = {0, v0}, cn[2] = {v0, nv - v0};
+    const size_t vb = (size_t)h->n_local * h->esz;         // bytes per vector
+    // the copy streams start after whatever the handle's stream has queued (dX / dY reuse)
+    H2_CUDA(h, cudaEventRecord(h->ev_y[1], h->stream));
+    H2_CUDA(h, cudaStreamWaitEvent(h->s_h2d, h->ev_y[1], 0));
+    for (int c = 0; c < 2; ++c) {
+        const size_t off = (size_t)cv[c] * vb, cb = (size_t)cn[c] * vb;
+        H2_CUDA(h, cudaMemcpyAsync((char *)h->dX + off, (const char *)X + off, cb, cudaMemcpyHostToDevice, h->s_h2d));
+        if (beta != 0.0)
+            H2_CUDA(h, cudaMemcpyAsync((char *)h->dY + off, (const char *)Y + off, cb, cudaMemcpyHostToDevice,
+                                       h->s_h2d));
+        H2_CUDA(h, cudaEventRecord(h->ev_x[c], h->s_h2d));
+    }
+    for (int c = 0; c < 2; ++c) {
+        const size_t off = (size_t)cv[c] * vb, cb = (size_t)cn[c] * vb;
+        H2_CUDA(h, cudaStreamWaitEvent(h->stream, h->ev_x[c], 0));
+        rc = h2_matvec_ld(h, alpha, (const char *)h->dX + off, h->n_local, beta, (char *)h->dY + off, h->n_local,
+                          cn[c]);
+        if (rc != H2_OK) return rc;
+        H2_CUDA(h, cudaEventRecord(h->ev_y[c], h->stream));
+        H2_CUDA(h, cudaStreamWaitEvent(h->s_d2h, h->ev_y[c], 0));
+        H2_CUDA(h, cudaMemcpyAsync((char *)Y + off, (const char *)h->dY + off, cb, cudaMemcpyDeviceToHost, h->s_d2h));
+    }
+    H2_CUDA(h, cudaStreamSynchronize(h->s_d2h));
     H2_CUDA(h, cudaStreamSynchronize(h->stream));
     return H2_OK;
 }
