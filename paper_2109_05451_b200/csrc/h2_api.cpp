@@ -1367,7 +1367,9 @@ static int create_impl(const h2_desc *d, int nv_max, const void *nccl_unique_id,
             // barriers between its levels: 1 launch instead of J), the tiny top levels (<= TOPN
             // nodes) in one CTA.  Measured on cfg2 (J = 1..4): up 86 -> 76 us, down 57 -> 47 us at
             // nv = 1; grouping the wide levels too slowed cfg5 FP32 (fewer warps on most bytes).
-            const int J = 4, GMAX = 1024;
+            // (H2_SWEEP_J / H2_SWEEP_GMAX: A/B overrides of the grouping)
+            const char *ej = getenv("H2_SWEEP_J"), *eg = getenv("H2_SWEEP_GMAX");
+            const int J = ej ? std::max(1, atoi(ej)) : 4, GMAX = eg ? atoi(eg) : 1024;
             auto push = [&](std::vector<SweepParams> &dst, std::vector<int> &ctas, std::vector<int> &thr,
                             const std::vector<SweepLevel> &g, bool up) {
                 if (g.empty()) return;

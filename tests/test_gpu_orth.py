@@ -96,3 +96,24 @@ def test_reweigh_parity(name):
             if w.min() > 1e-8 * max(w.max(), 1e-300):
                 assert np.abs(a - b).max() <= 1e-9 * scale, (l, i)
     op.close()
+
+
+def test_reweigh_and_export_argument_checks():
+    """Wrong sizes and unknown arrays are rejected (H2_ERR_ARG), nothing is written."""
+    import torch
+    from paper_2109_05451_b200 import operator_from_h2data
+    from paper_2109_05451_b200._binding import H2Error, H2_EXPORT_S
+    h = CASES["uniform-k8"]()
+    op = operator_from_h2data(h, nv_max=1)
+    n = sum((1 << l) * h.ranks[l] ** 2 for l in range(h.q + 1))
+    with pytest.raises(H2Error):
+        op.reweigh(torch.zeros(n - 1, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        op.reweigh(torch.zeros(n, dtype=torch.float32, device="cuda"))
+    with pytest.raises(H2Error):
+        op.export(H2_EXPORT_S, h.q, 1)                          # wrong count
+    with pytest.raises(H2Error):
+        op.export(99, 0, 1)                                     # unknown array
+    with pytest.raises(H2Error):
+        op.export(H2_EXPORT_S, h.q + 1, 1)                      # level out of range
+    op.close()
