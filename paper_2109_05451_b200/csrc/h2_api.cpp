@@ -1617,6 +1617,8 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     cudaStream_t s_leafc = (h->prof || h->group || !side) ? st : h->s_leafc;
     // CTA-tile engine (FP64, nv >= cta_min_nv): the same tasks, one CTA per output node
     const bool cta = h->use_cta(nv);
+    // (H2_CTA_SWEEPS=0: the warp sweeps even where the CTA-tile engine runs the rest -- A/B switch)
+    static const bool cta_sweeps = [] { const char *e = getenv("H2_CTA_SWEEPS"); return !(e && e[0] == '0'); }();
     auto cjob = [&](const Phase &ph, int kind, int mode, const void *src, int64_t src_ld, void *dst,
                     int64_t dst_ld) {
         CtaJob j{};
@@ -1729,7 +1731,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     }
     H2_MARK(2);
     // 1c. upsweep transfers of the local branch
-    if (cta) {
+    if (cta && (cta_sweeps || !h->use_sweep)) {
         for (const Phase &ph : h->up_lv)
             H2_CUDA(h, launch_cta(cjob(ph, CK_ROWS, MODE_WRITE, xh, h->xh_plane, xh, h->xh_plane), ph.r, h->nsm, st));
     } else if (h->use_sweep) {
@@ -1819,7 +1821,7 @@ int enqueue(h2_ctx *h, int nv, cudaStream_t st, int part = PART_ALL)
     }
     H2_MARK(6);
     // 5. downsweep transfers (alg:downsweep)
-    if (cta) {
+    if (cta && (cta_sweeps || !h->use_sweep)) {
         for (const Phase &ph : h->down_lv)
             H2_CUDA(h, launch_cta(cjob(ph, CK_ROWS, MODE_ACCUM, yh, h->yh_plane, yh, h->yh_plane), ph.r, h->nsm, st));
     } else if (h->use_sweep) {
