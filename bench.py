@@ -252,8 +252,11 @@ def run_reference(args, emit):
     prim, extra = SUITES[args.config]
     legs = [lg for nm in prim for lg in legs_of(nm)]
     parts, flops_step, sample = [], 0.0, []
+    # the oracle's rate is timed on the one-GPU workload: its GFLOP/s does not depend on the global
+    # size, and building a P-GPU weak-scaled operator on the host (8x cfg2 = tens of GB) would not
+    # fit the reference arm's minutes; the config reported is the P-GPU one (structure only)
     for name, dt, nvs in legs:
-        _, _, _, h, c = build_leg_problem(name, ws, 0, True)
+        _, _, _, h, c = build_leg_problem(name, 1, 0, True)
         hh = h if dt == "f64" else h.astype(np.float32).astype(np.float64)
         Xs = {nv: make_xy(h.perm, nv, SEED) for nv in nvs}
         fl = sum(h.flops(nv) for nv in nvs)
@@ -261,7 +264,8 @@ def run_reference(args, emit):
         mask, frac = oracle_mask(h, nvs, budget, cores)
         parts.append((hh, Xs, nvs, mask, fl, frac))
         flops_step += fl
-        sample.append(f"{leg_key((name, dt, nvs))}: {frac * 100:.1f}% of the oracle work (leaf sample, full upsweep)")
+        sample.append(f"{leg_key((name, dt, nvs))}: {frac * 100:.1f}% of the oracle work (leaf sample, full upsweep)"
+                      + (f" of the one-GPU workload (rate; the {ws}-GPU global operator is not built)" if ws > 1 else ""))
 
     def step():
         return sum(time_oracle(hh, Xs, nvs, mask, fl, frac)[0] / frac for hh, Xs, nvs, mask, fl, frac in parts)
@@ -273,10 +277,15 @@ def run_reference(args, emit):
     from h2gen.configs import CONFIGS
     P = ws
     n_first = int(parts[0][0].N)
-    # per-GPU rows of rank 0 = its branch at the C-level (the same rows the GPU arm reports)
-    C = P.bit_length() - 1
-    lp = np.asarray(parts[0][0].leaf_ptr)
-    n_rank0 = int(lp[1 << (parts[0][0].q - C)]) if P > 1 else n_first
+    n_rank0 = n_first
+    if P > 1:
+        # per-GPU rows of rank 0 = its branch at the C-level (the same rows the GPU arm reports)
+        from h2gen.configs import build_structure
+        tree_p = build_structure(base_name(legs[0][0]), P)[0]
+        C = P.bit_length() - 1
+        lp = np.asarray(tree_p.leaf_ptr)
+        n_first = int(tree_p.N)
+        n_rank0 = int(lp[1 << (tree_p.q - C)])
     legs_x = [lg for nm in extra for lg in legs_of(nm) if not (P > 1 and lg[0].endswith(":sym"))]
     ours_cfg = config_dict(args, ws, legs, legs_x, n_first, n_rank0)
     out = {"metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
