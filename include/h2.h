@@ -233,8 +233,13 @@ int h2_pcg(h2_handle K, double scale, const double *diag, const int64_t *C_rowpt
  *   H2_EXPORT_S  coupling blocks of `level` (k^l x k^l each, column-major, h2_desc CSR order;
  *                one GPU, full storage), H2_EXPORT_U leaf bases (m x k^q per leaf),
  *   H2_EXPORT_VT leaf bases stored transposed (k^q x m per leaf), H2_EXPORT_E transfers of `level`
- *   (k^l x k^{l-1} per node), H2_EXPORT_FT transfers F stored transposed (k^{l-1} x k^l). */
-enum { H2_EXPORT_S = 0, H2_EXPORT_U = 1, H2_EXPORT_VT = 2, H2_EXPORT_E = 3, H2_EXPORT_FT = 4 };
+ *   (k^l x k^{l-1} per node), H2_EXPORT_FT transfers F stored transposed (k^{l-1} x k^l);
+ *   H2_EXPORT_XHAT / H2_EXPORT_YHAT the x^ / y^ coefficients of `level` left by the last matvec
+ *   (count = nv * held nodes * k^l: per vector, node-major then coefficient; y^ of the levels
+ *   above the leaves after the downsweep, the leaf level's coupling sums -- the leaf transfer is
+ *   applied inside the leaf kernel for FP64). */
+enum { H2_EXPORT_S = 0, H2_EXPORT_U = 1, H2_EXPORT_VT = 2, H2_EXPORT_E = 3, H2_EXPORT_FT = 4,
+       H2_EXPORT_XHAT = 5, H2_EXPORT_YHAT = 6 };
 int h2_orthogonalize(h2_handle h);
 int h2_export(h2_handle h, int what, int level, void *host, int64_t count);
 /* h2_reweigh: the reweighing downsweep of the recompression, root to leaves:

@@ -20,7 +20,7 @@ EXPORTS = ["h2_create", "h2_matvec", "h2_matvec_ld", "h2_matvec_host", "h2_set_s
            "h2_set_profiling", "h2_phase_times", "h2_phase_stats",
            "h2_plan_counts", "h2_plan_census", "h2_destroy", "h2_nccl_unique_id", "h2_last_error", "h2_version",
            "h2_orthogonalize", "h2_export", "h2_reweigh"]
-H2_EXPORT_S, H2_EXPORT_U, H2_EXPORT_VT, H2_EXPORT_E, H2_EXPORT_FT = 0, 1, 2, 3, 4
+H2_EXPORT_S, H2_EXPORT_U, H2_EXPORT_VT, H2_EXPORT_E, H2_EXPORT_FT, H2_EXPORT_XHAT, H2_EXPORT_YHAT = 0, 1, 2, 3, 4, 5, 6
 PHASES = ["up_leaf", "up_transfer", "exchange_top", "coupling_diag", "coupling_offdiag",
           "down_transfer", "leaf_u", "dense", "coupling_leaf"]
 KERNEL_OF_PHASE = {"up_leaf": "k_up_leaf", "up_transfer": "k_sweep<WRITE>", "exchange_top": "k_pack + k_tree",

@@ -2335,6 +2335,23 @@ extern "C" int h2_export(h2_handle h, int what, int level, void *host, int64_t c
     case H2_EXPORT_VT: src = h->Vt; n = nleaf * m * h->L.k[q]; break;
     case H2_EXPORT_E:  src = level ? h->E[level] : nullptr; n = (int64_t)h->L.held(level) * kl * kp; break;
     case H2_EXPORT_FT: src = level ? h->Ft[level] : nullptr; n = (int64_t)h->L.held(level) * kl * kp; break;
+    case H2_EXPORT_XHAT:                               // x^ / y^ of `level` after the last matvec:
+    case H2_EXPORT_YHAT: {                             // nv vectors x (held nodes x k^l), vector-major
+        const int64_t per = (int64_t)h->L.held(level) * kl;
+        if (per == 0 || count % per || count / per < 1 || count / per > h->nv_max)
+            return fail(H2_ERR_ARG, "h2_export: count must be nv * held(level) * k^l, 1 <= nv <= nv_max");
+        const int64_t nvx = count / per;
+        const bool xw = what == H2_EXPORT_XHAT;
+        const char *base = (const char *)(xw ? h->xh : h->yh);
+        const int64_t plane = xw ? h->xh_plane : h->yh_plane;
+        const int64_t off = xw ? h->xh_base[level] : h->yh_base[level];
+        cudaError_t err = cudaStreamSynchronize(h->stream);
+        for (int64_t n = 0; n < nvx && err == cudaSuccess; ++n)
+            err = cudaMemcpy((char *)host + (size_t)n * per * h->esz, base + (size_t)(off + n * plane) * h->esz,
+                             (size_t)per * h->esz, cudaMemcpyDeviceToHost);
+        if (err != cudaSuccess) return cuda_fail(h, err, "h2_export");
+        return H2_OK;
+    }
     default: return fail(H2_ERR_ARG, "h2_export: unknown array");
     }
     if (n < 0) return fail(H2_ERR_ARG, "h2_export: coupling export needs one GPU and full storage");

@@ -263,3 +263,47 @@ def test_fp32_tensor_engine(engine, N, m, k, nv, eta, seed, monkeypatch):
     out = gpu_matvec(_op(h, nv_max=max(nv, 16), dtype="f32"), X, -0.6, 1.3, Y0, "f32")
     ref = oracle.matvec(h.astype(np.float64), X, -0.6, 1.3, Y0)
     assert colmax_rel(out, ref) <= TOL32
+
+
+def test_per_phase_xhat_yhat_trees():
+    """the x^ and y^ trees the GPU leaves after a matvec, level by level, against
+    brute force -- x^^l_s = V^{lT}_s x_s with the explicit level bases (upsweep: leaf projection +
+    transfers), c^l_t = sum_s S_ts x^^l_s (coupling), y^^l = c^l + E y^^{l-1}_parent (downsweep, levels
+    above the leaves; the FP64 leaf kernel applies the last transfer itself, so the leaf level holds
+    c^q)."""
+    from paper_2109_05451_b200._binding import H2_EXPORT_XHAT, H2_EXPORT_YHAT
+    from tests.dense_assembly import explicit_bases
+    h = random_case(1500, 32, lambda l: 8 + (l % 2), 21)
+    nv = 2
+    op = _op(h, nv_max=nv)
+    X = make_xy(h.perm, nv, 7, -1.0, 1.0)
+    gpu_matvec(op, X, 1.0, 0.0, np.zeros_like(X))
+    VB = explicit_bases(h, "V")
+    q = h.q
+    xh_ref, c_ref = {}, {}
+    for l in range(q + 1):
+        k = h.ranks[l]
+        sh = q - l
+        xs = np.zeros((nv, 1 << l, k))
+        for s in range(1 << l):
+            r0, r1 = h.leaf_ptr[s << sh], h.leaf_ptr[(s + 1) << sh]
+            xs[:, s, :] = (VB[(l, s)].T @ X[:, r0:r1].T).T
+        xh_ref[l] = xs
+        c = np.zeros((nv, 1 << l, k))
+        rp, col = h.S_rowptr[l], h.S_col[l]
+        for t in range(1 << l):
+            for b in range(rp[t], rp[t + 1]):
+                c[:, t, :] += (h.S[l][b].T @ xs[:, col[b], :].T).T
+        c_ref[l] = c
+    y_ref = {0: c_ref[0]}
+    for l in range(1, q + 1):
+        y_ref[l] = c_ref[l] + np.einsum("cij,nci->ncj", h.E[l], y_ref[l - 1][:, np.arange(1 << l) >> 1, :])
+    for l in range(q + 1):
+        k = h.ranks[l]
+        got_x = op.export(H2_EXPORT_XHAT, l, nv * (1 << l) * k).reshape(nv, 1 << l, k)
+        if np.abs(c_ref[l]).max() > 0 or l == q:      # levels whose x^ feeds a coupling or transfer
+            assert np.abs(got_x - xh_ref[l]).max() <= 1e-12 * np.abs(xh_ref[l]).max(), ("x^", l)
+        got_y = op.export(H2_EXPORT_YHAT, l, nv * (1 << l) * k).reshape(nv, 1 << l, k)
+        want = c_ref[q] if l == q else y_ref[l]
+        assert np.abs(got_y - want).max() <= 1e-12 * max(np.abs(want).max(), 1e-300), ("y^", l)
+    op.close()
